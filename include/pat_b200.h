@@ -1,0 +1,207 @@
+/*
+ * pat_b200.h — C ABI of the B200-native PAT all-gather / reduce-scatter.
+ *
+ * This is the drop-in boundary for the reference's hot path (patsim, /root/reference/proj).
+ * The reference exposes a C++ template API; every entry point below names the reference
+ * interface it replaces (file:line, relative to /root/reference/proj). Plain pointers and
+ * sizes only — no C++ or torch types. Errors are return codes (never exceptions); the
+ * reference's exception classes map onto patResult_t values (see below).
+ *
+ *   reference (C++)                                          this ABI
+ *   ---------------------------------------------------------------------------------------
+ *   run_allgather(sched, Payload<T>, RunOptions)             patAllGather
+ *       include/patsim/simulate.hpp:78-84, src/simulate.cpp:151-222,304-314
+ *   run_reduce_scatter(sched, Payload<T>, ReduceOp, ...)     patReduceScatter
+ *       include/patsim/simulate.hpp:93-96, src/simulate.cpp:224-300,316-332
+ *   pat_allgather / mirror_schedule / pat_reduce_scatter      patScheduleBuild / patScheduleMirror
+ *       include/patsim/algorithms.hpp:54-62, src/algorithms.cpp:191-249
+ *   ring / bruck_nearest / bruck_farthest / rec. doubling    patScheduleBuild (algorithm arg)
+ *       include/patsim/algorithms.hpp:33-47, src/algorithms.cpp:105-155
+ *   validate(sched)                                          patScheduleValidate
+ *       include/patsim/schedule.hpp:108-115, src/schedule.cpp:194-212
+ *   max_trees / trees_from_buffer / pat_buffer_slots /       patMaxTrees / patTreesFromBuffer /
+ *   round_count_formula                                      patPatBufferSlots / patRoundCountFormula
+ *       include/patsim/algorithms.hpp:12-27, src/algorithms.cpp:49-93
+ *   ExecStats (slot occupancy, bytes, messages)              patScheduleStats
+ *       include/patsim/simulate.hpp:43-53, src/simulate.cpp:109-129
+ *   write_trace_csv                                          patScheduleTraceCsv
+ *       include/patsim/simulate.hpp:98-100, src/simulate.cpp:334-346
+ *   RunOptions{mode,threads} / in-process ranks              patCommInitAll (one process, many GPUs,
+ *       include/patsim/simulate.hpp:63-67                      several logical ranks per GPU allowed)
+ *
+ * Payload layouts are the reference's (simulate.hpp:33-41, 55-59) and NCCL's:
+ *   all-gather:     sendbuff[r] = count elements; recvbuff[r] = n*count, block o = rank o's data
+ *   reduce-scatter: sendbuff[s] = n*count, block d destined to rank d; recvbuff[d] = count
+ *
+ * Results are bit-identical to the reference executor: all-gather is a copy; reduce-scatter
+ * folds in the PAT tree order of simulate.cpp (first arrival opens an accumulator, later
+ * arrivals fold in round order, own contribution folded last at send, offset-0 arrivals
+ * folded into the output after the own contribution), with every fold rounded to the
+ * wire dtype (fp16/bf16 computed in fp32, round-to-nearest-even).
+ */
+#ifndef PAT_B200_H
+#define PAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PAT_B200_VERSION 10000 /* 1.0.0 */
+#define PAT_MAX_RANKS 8        /* one 8xB200 NVSwitch box */
+#define PAT_HANDLE_BYTES 128   /* per-rank exchange blob for multi-process init */
+
+struct CUstream_st; /* cudaStream_t without pulling in the CUDA headers */
+typedef struct CUstream_st* patStream_t;
+
+typedef struct patComm* patComm_t;
+
+typedef enum {
+  /* NCCL-compatible codes */
+  patSuccess = 0,
+  patUnhandledCudaError = 1,
+  patSystemError = 2,
+  patInternalError = 3,
+  patInvalidArgument = 4,
+  patInvalidUsage = 5,
+  patRemoteError = 6,
+  /* the reference's typed exceptions (schedule.hpp:18-32, simulate.hpp:18-31) */
+  patScheduleError = 20,       /* ScheduleError */
+  patNonPowerOfTwo = 21,       /* NonPowerOfTwoError */
+  patInvalidTreeCount = 22,    /* InvalidTreeCountError */
+  patBufferTooSmall = 23,      /* BufferTooSmallError */
+  patRankOutOfRange = 24,      /* RankOutOfRangeError */
+  patSimulationError = 30,     /* SimulationError (wrong schedule kind, ...) */
+  patPayloadShape = 31,        /* PayloadShapeError */
+  patUnsupportedOp = 32,       /* UnsupportedOpError */
+  patInvalidSchedule = 33,     /* InvalidScheduleError */
+  patTimeout = 40,             /* device-side wait exceeded config.timeout_ms */
+  patCapacity = 41             /* caller buffer too small */
+} patResult_t;
+
+/* numbering follows ncclDataType_t */
+typedef enum {
+  patInt8 = 0, patUint8 = 1, patInt32 = 2, patUint32 = 3, patInt64 = 4, patUint64 = 5,
+  patFloat16 = 6, patFloat32 = 7, patFloat64 = 8, patBfloat16 = 9, patNumTypes = 10
+} patDataType_t;
+
+/* numbering follows ncclRedOp_t (avg not provided) */
+typedef enum { patSum = 0, patProd = 1, patMax = 2, patMin = 3, patNumOps = 4 } patRedOp_t;
+
+typedef enum { patAllGatherKind = 0, patReduceScatterKind = 1 } patCollKind_t;
+typedef enum { patAlgoRing = 0, patAlgoBruckNearest = 1, patAlgoBruckFarthest = 2,
+               patAlgoRecursiveDoubling = 3, patAlgoPat = 4 } patAlgorithm_t;
+typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2 } patProtocol_t;
+
+typedef struct {
+  size_t size;              /* sizeof(patConfig_t) */
+  size_t staging_bytes;     /* per-rank inbox pool; 0 = default (channels*2*(n-1)*slice) */
+  size_t slice_bytes;       /* SIMPLE bytes per slot per pipeline step; 0 = default 128 KiB */
+  size_t ll_threshold;      /* per-rank chunk bytes up to which LL is used; 0 = default */
+  int trees;                /* PAT tree count T; 0 = max_trees(n) (full aggregation) */
+  int max_channels;         /* CTAs per rank; 0 = default */
+  int protocol;             /* patProtocol_t */
+  int timeout_ms;           /* device-side spin timeout; 0 = default 20000 */
+  int threads;              /* threads per CTA; 0 = default */
+} patConfig_t;
+
+/* Plan the library would launch for one call (introspection / benchmarks). */
+typedef struct {
+  int protocol;             /* patProtoLL or patProtoSimple */
+  int trees;
+  int rounds;               /* PAT rounds (= sync steps) */
+  int channels;             /* CTAs per rank */
+  int iterations;           /* pipeline steps per channel */
+  int threads;              /* per CTA */
+  int launches;             /* kernel launches (one per device) */
+  int slots_per_step;       /* inbox slots per pipeline step (n-1) */
+  size_t slice_bytes;       /* payload bytes per slot per step */
+  size_t pool_bytes;        /* inbox pool bytes per rank actually addressed */
+  int64_t bytes_sent_per_rank;   /* (n-1) * chunk bytes */
+  int peak_intermediate_slots;   /* reference accounting (simulate.hpp:50) */
+} patPlanInfo_t;
+
+/* ExecStats (simulate.hpp:43-53) computed from a schedule; chunk_bytes as given. */
+typedef struct {
+  int32_t rounds;
+  int32_t max_chunks_per_message;
+  int64_t messages;
+  int64_t bytes_sent_per_rank;
+  int32_t peak_intermediate_slots;
+  int32_t n_occupancy;
+  int32_t occupancy_per_round[512];
+} patExecStats_t;
+
+const char* patGetErrorString(patResult_t result);
+patResult_t patGetVersion(int* version);
+patResult_t patConfigInit(patConfig_t* config);
+
+/* ---- communicators ---------------------------------------------------------------- */
+
+/* One process drives every rank (ncclCommInitAll analogue; the reference's in-process
+ * ranks). devlist[r] is the CUDA device of rank r; a device may repeat, in which case its
+ * ranks run inside ONE cooperative kernel per call ("local mode", e.g. 8 logical ranks on
+ * one GPU). Peer access is enabled between distinct devices. NULL devlist = 0..n-1. */
+patResult_t patCommInitAll(patComm_t* comm, int nranks, const int* devlist, const patConfig_t* config);
+
+/* One process per rank (torchrun). Step 1 allocates this rank's inbox pool on `device`
+ * and writes a PAT_HANDLE_BYTES blob; the caller all-gathers the blobs (any transport) and
+ * passes all nranks blobs, rank-ordered, to step 2, which maps the peers' pools (CUDA IPC). */
+patResult_t patCommInitRankPrepare(patComm_t* comm, int nranks, int rank, int device,
+                                   const patConfig_t* config, void* handle_out);
+patResult_t patCommInitRankFinish(patComm_t comm, const void* all_handles);
+
+patResult_t patCommDestroy(patComm_t comm);
+patResult_t patCommCount(patComm_t comm, int* nranks);
+/* Ranks driven by this communicator, in the order the array arguments use. */
+patResult_t patCommLocalRanks(patComm_t comm, int* nlocal, int* ranks, int* devices);
+/* Device-reported asynchronous error (timeouts); readable without synchronising. */
+patResult_t patCommGetAsyncError(patComm_t comm, patResult_t* async_error);
+patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDataType_t dtype,
+                        patPlanInfo_t* info);
+
+/* ---- collectives (asynchronous on the given streams) ----------------------------------
+ * Array arguments are indexed by local rank (patCommLocalRanks order): one entry per rank
+ * this communicator drives. Ranks sharing a device are launched as one kernel on the stream
+ * of the first of them (the others' streams are joined with events). In-place all-gather
+ * (sendbuff == recvbuff + rank*count) is allowed. count == 0 is a no-op. */
+patResult_t patAllGather(patComm_t comm, const void* const* sendbuffs, void* const* recvbuffs,
+                         size_t sendcount, patDataType_t datatype, const patStream_t* streams);
+patResult_t patReduceScatter(patComm_t comm, const void* const* sendbuffs, void* const* recvbuffs,
+                             size_t recvcount, patDataType_t datatype, patRedOp_t op,
+                             const patStream_t* streams);
+
+/* Same collectives over an explicit, caller-supplied rank-relative schedule (any validated
+ * non-exchange schedule of the communicator's rank count: PAT with any T, ring, Bruck), the
+ * generic executor of the reference (run_allgather/run_reduce_scatter take a schedule,
+ * simulate.hpp:78-96). Errors as the reference: patSimulationError for a schedule of the
+ * wrong kind, patInvalidSchedule when validate() reports violations (simulate.cpp:72-85). */
+patResult_t patAllGatherSchedule(patComm_t comm, const int32_t* sched, size_t len, const void* const* sendbuffs,
+                                 void* const* recvbuffs, size_t sendcount, patDataType_t datatype,
+                                 const patStream_t* streams);
+patResult_t patReduceScatterSchedule(patComm_t comm, const int32_t* sched, size_t len,
+                                     const void* const* sendbuffs, void* const* recvbuffs, size_t recvcount,
+                                     patDataType_t datatype, patRedOp_t op, const patStream_t* streams);
+
+/* ---- schedules (host only; no GPU needed) ---------------------------------------------
+ * Flat int32 encoding: [kind, algorithm, n_ranks, has_params, trees, buffer_slots, nrounds,
+ * then per round: round_index, dimension, split_index, peer, exchange, nchunks, offsets...] */
+patResult_t patScheduleBuild(int kind, int algorithm, int nranks, int trees,
+                             int32_t* buf, size_t cap, size_t* len);
+patResult_t patScheduleMirror(const int32_t* sched, size_t len, int32_t* out, size_t cap, size_t* out_len);
+patResult_t patScheduleValidate(const int32_t* sched, size_t len, int* nviolations,
+                                char* first_message, size_t message_cap);
+patResult_t patScheduleStats(const int32_t* sched, size_t len, int64_t chunk_bytes, patExecStats_t* stats);
+patResult_t patScheduleTraceCsv(const int32_t* sched, size_t len, int64_t chunk_bytes,
+                                char* buf, size_t cap, size_t* out_len);
+patResult_t patMaxTrees(int nranks, int* trees);
+patResult_t patTreesFromBuffer(int64_t buffer_bytes, int64_t chunk_bytes, int nranks, int* trees);
+patResult_t patPatBufferSlots(int nranks, int trees, int* slots);
+patResult_t patRoundCountFormula(int nranks, int trees, int* rounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAT_B200_H */

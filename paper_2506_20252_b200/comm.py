@@ -1,0 +1,185 @@
+"""Communicators and collectives over the C ABI (include/pat_b200.h).
+
+Two ways to build a communicator, matching the north-star process models:
+
+* ``PatComm.init_all(n, devices)`` — one process drives all ranks (the reference's in-process
+  ranks, ``ncclCommInitAll``). ``devices`` may repeat a GPU: its ranks then run inside one
+  cooperative kernel ("local mode", used for n > #GPUs and for the 1-GPU HBM roofline).
+* ``PatComm.init_rank(n, rank, device, exchange)`` / ``from_process_group()`` — one process
+  per rank (torchrun). Each rank exports a 128-byte handle; ``exchange`` all-gathers them
+  (torch.distributed, any backend) and the peers' inbox pools are mapped with CUDA IPC.
+
+Buffers are passed as raw device pointers (ints) or torch tensors; torch is plumbing only.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Callable, Optional, Sequence
+
+from . import _lib
+from ._lib import Config, PatError, PlanInfo, check, lib, ptr_array
+
+try:  # torch is optional for the pointer-level API
+    import torch
+
+    TORCH_DTYPES = {
+        torch.int8: _lib.INT8, torch.uint8: _lib.UINT8, torch.int32: _lib.INT32, torch.int64: _lib.INT64,
+        torch.float16: _lib.FLOAT16, torch.float32: _lib.FLOAT32, torch.float64: _lib.FLOAT64,
+        torch.bfloat16: _lib.BFLOAT16,
+    }
+    for _name, _code in (("uint32", _lib.UINT32), ("uint64", _lib.UINT64)):
+        if hasattr(torch, _name):
+            TORCH_DTYPES[getattr(torch, _name)] = _code
+except ImportError:  # pragma: no cover
+    torch = None
+    TORCH_DTYPES = {}
+
+
+def make_config(**kw) -> Config:
+    c = Config()
+    lib().patConfigInit(ctypes.byref(c))
+    mapping = {"channels": "max_channels"}
+    for k, v in kw.items():
+        if v is None:
+            continue
+        setattr(c, mapping.get(k, k), int(v))
+    return c
+
+
+def _ptr(x) -> int:
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    raise TypeError(f"expected a device pointer or tensor, got {type(x)}")
+
+
+def _dtype(dtype, sample) -> int:
+    if dtype is None:
+        if torch is None or not hasattr(sample, "dtype"):
+            raise TypeError("dtype required for raw pointers")
+        return TORCH_DTYPES[sample.dtype]
+    if torch is not None and isinstance(dtype, torch.dtype):
+        return TORCH_DTYPES[dtype]
+    return int(dtype)
+
+
+class PatComm:
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        n = ctypes.c_int()
+        check(lib().patCommCount(self._h, ctypes.byref(n)), "patCommCount")
+        self.nranks = n.value
+        nl = ctypes.c_int()
+        ranks = (ctypes.c_int * _lib.MAX_RANKS)()
+        devs = (ctypes.c_int * _lib.MAX_RANKS)()
+        check(lib().patCommLocalRanks(self._h, ctypes.byref(nl), ranks, devs), "patCommLocalRanks")
+        self.local_ranks = list(ranks[: nl.value])
+        self.devices = list(devs[: nl.value])
+
+    # ------------------------------------------------------------------ construction
+    @classmethod
+    def init_all(cls, nranks: int, devices: Optional[Sequence[int]] = None, **config) -> "PatComm":
+        h = ctypes.c_void_p()
+        cfg = make_config(**config)
+        devarr = (ctypes.c_int * nranks)(*devices) if devices is not None else None
+        check(lib().patCommInitAll(ctypes.byref(h), nranks, devarr, ctypes.byref(cfg)), "patCommInitAll")
+        return cls(h)
+
+    @classmethod
+    def init_rank(cls, nranks: int, rank: int, device: int, exchange: Callable[[bytes], list], **config) -> "PatComm":
+        """exchange(my_handle_bytes) must return all ranks' handles, rank-ordered."""
+        h = ctypes.c_void_p()
+        cfg = make_config(**config)
+        blob = ctypes.create_string_buffer(_lib.HANDLE_BYTES)
+        check(lib().patCommInitRankPrepare(ctypes.byref(h), nranks, rank, device, ctypes.byref(cfg), blob),
+              "patCommInitRankPrepare")
+        try:
+            handles = exchange(bytes(blob.raw))
+            if len(handles) != nranks or any(len(x) != _lib.HANDLE_BYTES for x in handles):
+                raise PatError(4, "handle exchange returned a malformed list")
+            allh = ctypes.create_string_buffer(b"".join(handles), nranks * _lib.HANDLE_BYTES)
+            check(lib().patCommInitRankFinish(h, allh), "patCommInitRankFinish")
+        except BaseException:
+            lib().patCommDestroy(h)
+            raise
+        return cls(h)
+
+    @classmethod
+    def from_process_group(cls, group=None, device: Optional[int] = None, **config) -> "PatComm":
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if device is None:
+            device = torch.cuda.current_device()
+
+        def exchange(mine: bytes) -> list:
+            out = [None] * world
+            dist.all_gather_object(out, mine, group=group)
+            return out
+
+        return cls.init_rank(world, rank, device, exchange, **config)
+
+    def destroy(self) -> None:
+        if self._h:
+            lib().patCommDestroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ collectives
+    def _streams(self, streams):
+        if streams is None:
+            if torch is not None and torch.cuda.is_available():
+                streams = [torch.cuda.current_stream(d).cuda_stream for d in self.devices]
+            else:
+                streams = [0] * len(self.local_ranks)
+        return ptr_array([int(getattr(s, "cuda_stream", s)) for s in streams])
+
+    def all_gather(self, sendbufs, recvbufs, count: Optional[int] = None, dtype=None, streams=None, schedule=None):
+        """sendbufs[l] -> recvbufs[l] (n*count, origin order) for every local rank l."""
+        dt = _dtype(dtype, sendbufs[0])
+        if count is None:
+            count = sendbufs[0].numel()
+        sb, rb = ptr_array([_ptr(x) for x in sendbufs]), ptr_array([_ptr(x) for x in recvbufs])
+        if schedule is not None:
+            enc = schedule.encode()
+            check(lib().patAllGatherSchedule(self._h, enc.ctypes.data_as(_lib.I32P), len(enc), sb, rb, count, dt,
+                                             self._streams(streams)), "patAllGatherSchedule")
+        else:
+            check(lib().patAllGather(self._h, sb, rb, count, dt, self._streams(streams)), "patAllGather")
+
+    def reduce_scatter(self, sendbufs, recvbufs, count: Optional[int] = None, dtype=None, op: int = _lib.SUM,
+                       streams=None, schedule=None):
+        """sendbufs[l] (n*count, block d -> rank d) reduced into recvbufs[l] (count)."""
+        dt = _dtype(dtype, sendbufs[0])
+        if count is None:
+            count = recvbufs[0].numel()
+        sb, rb = ptr_array([_ptr(x) for x in sendbufs]), ptr_array([_ptr(x) for x in recvbufs])
+        if schedule is not None:
+            enc = schedule.encode()
+            check(lib().patReduceScatterSchedule(self._h, enc.ctypes.data_as(_lib.I32P), len(enc), sb, rb, count,
+                                                 dt, int(op), self._streams(streams)), "patReduceScatterSchedule")
+        else:
+            check(lib().patReduceScatter(self._h, sb, rb, count, dt, int(op), self._streams(streams)),
+                  "patReduceScatter")
+
+    def plan(self, kind: int, count: int, dtype) -> dict:
+        info = PlanInfo()
+        check(lib().patCommPlan(self._h, int(kind), count, _dtype(dtype, None) if dtype is not None else 7,
+                                ctypes.byref(info)), "patCommPlan")
+        return info.as_dict()
+
+    def async_error(self) -> int:
+        e = ctypes.c_int()
+        check(lib().patCommGetAsyncError(self._h, ctypes.byref(e)), "patCommGetAsyncError")
+        return e.value
+
+    def raise_async_error(self) -> None:
+        e = self.async_error()
+        if e:
+            raise PatError(e, "asynchronous device error")

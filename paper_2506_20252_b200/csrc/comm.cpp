@@ -1,0 +1,754 @@
+// comm.cpp — host runtime behind include/pat_b200.h.
+//
+// A communicator owns, for every rank it drives, one inbox pool in that rank's HBM
+// (flags + channels * 2 * (n-1) slots) and maps every other rank's pool into each of its
+// devices' address spaces: legacy peer access between devices of this process
+// (patCommInitAll) or CUDA IPC between processes (patCommInitRank*). A collective compiles
+// the PAT schedule for (kind, T) once, picks the protocol and slicing from the chunk size,
+// and launches ONE cooperative kernel per device covering all ranks on that device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <unistd.h>
+#include <vector>
+
+#include "../../include/pat_b200.h"
+#include "plan.hpp"
+#include "schedule.hpp"
+
+namespace pat {
+using KernelFn = void (*)(const KPlan);
+cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream);
+cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out);
+}  // namespace pat
+
+using namespace pat;
+
+namespace {
+
+constexpr size_t kFlagBytes = sizeof(uint64_t) * kMaxChannels * kFlagWords;  // 8 KiB
+constexpr uint32_t kMagic = 0x50415442;                                       // "PATB"
+constexpr size_t kDefaultSlice = 128 << 10;
+constexpr int kDefaultChannels = 32;
+constexpr size_t kDefaultLL = 64 << 10;
+constexpr int kDefaultTimeoutMs = 20000;
+
+struct Compiled {
+  Schedule sched;
+  KPlan proto;  // schedule part of the plan (rounds, slots, fin, peers)
+  int peak_slots = 0;
+};
+
+struct DevGroup {
+  int device = 0;
+  std::vector<int> lidx;           // local indices on this device
+  uint64_t* iter_state = nullptr;  // [lidx.size()][kMaxChannels]
+  int sm_count = 0;
+  std::array<char*, kMaxRanks> pool_view{};  // every rank's pool as seen from this device
+};
+
+struct Handle {
+  uint32_t magic, version;
+  int32_t nranks, rank, device, channels;
+  uint64_t pool_bytes, slot_bytes;
+  int32_t pid, pad;
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(Handle) <= PAT_HANDLE_BYTES, "handle too large");
+
+bool env_int(const char* name, long long* out) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return false;
+  *out = std::atoll(v);
+  return true;
+}
+
+}  // namespace
+
+struct patComm {
+  int n = 0;
+  patConfig_t cfg{};
+  bool multiprocess = false;
+  bool finished = false;
+  std::vector<int> lranks, ldevs;    // per local index
+  std::vector<char*> owned_pool;     // per local index
+  std::vector<DevGroup> groups;
+  std::vector<void*> ipc_opened;
+  size_t slot_bytes = 0, pool_bytes = 0;
+  int channels = 0;
+  int* err_host = nullptr;
+  int* err_dev = nullptr;
+  std::map<std::vector<int32_t>, Compiled> compiled;  // keyed by schedule encoding
+  std::map<int, Compiled*> pat_cache;                  // kind*64 + trees -> compiled PAT
+  std::map<std::array<int, 5>, int> occupancy;
+  std::vector<cudaEvent_t> events;   // per local index
+  std::mutex mu;
+};
+
+namespace {
+
+#define CUDA_TRY(x)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) {                                                               \
+      std::fprintf(stderr, "pat_b200: %s failed: %s (%s:%d)\n", #x, cudaGetErrorString(e_), \
+                   __FILE__, __LINE__);                                                    \
+      return patUnhandledCudaError;                                                        \
+    }                                                                                      \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+patResult_t to_result(Err e) { return static_cast<patResult_t>(e); }
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case patInt8: case patUint8: return 1;
+    case patFloat16: case patBfloat16: return 2;
+    case patInt32: case patUint32: case patFloat32: return 4;
+    case patInt64: case patUint64: case patFloat64: return 8;
+    default: return 0;
+  }
+}
+
+void fill_defaults(patConfig_t* c, int n) {
+  long long v;
+  if (c->max_channels <= 0) c->max_channels = env_int("PAT_CHANNELS", &v) ? (int)v : kDefaultChannels;
+  c->max_channels = std::min(std::max(c->max_channels, 1), kMaxChannels);
+  if (c->slice_bytes == 0) c->slice_bytes = env_int("PAT_SLICE_BYTES", &v) ? (size_t)v : kDefaultSlice;
+  c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(15));
+  if (c->ll_threshold == 0) c->ll_threshold = env_int("PAT_LL_THRESHOLD", &v) ? (size_t)v : kDefaultLL;
+  if (c->timeout_ms <= 0) c->timeout_ms = env_int("PAT_TIMEOUT_MS", &v) ? (int)v : kDefaultTimeoutMs;
+  if (c->protocol == patProtoAuto && env_int("PAT_PROTOCOL", &v)) c->protocol = (int)v;
+  if (c->threads <= 0) c->threads = env_int("PAT_THREADS", &v) ? (int)v : 512;
+  c->threads = std::min(std::max(c->threads / 32 * 32, 32), 1024);
+  if (c->staging_bytes != 0) {
+    // staging budget -> slot size: channels * 2 buffers * (n-1) slots
+    const size_t slots = static_cast<size_t>(c->max_channels) * 2 * std::max(n - 1, 1);
+    size_t s = (c->staging_bytes / slots) & ~size_t(15);
+    if (s < 256) s = 256;
+    c->slice_bytes = s;
+  }
+}
+
+// Compile a validated schedule into the schedule part of a KPlan (arrival slots, fold lists).
+patResult_t compile_schedule(patComm* comm, const Schedule& given, Compiled** out) {
+  std::vector<int32_t> key = encode(given);
+  auto it = comm->compiled.find(key);
+  if (it != comm->compiled.end()) {
+    *out = &it->second;
+    return patSuccess;
+  }
+  Compiled c;
+  c.sched = given;
+  if (c.sched.n != comm->n) return patPayloadShape;
+  std::string why;
+  if (validate(c.sched, &why) != 0) {
+    std::fprintf(stderr, "pat_b200: invalid schedule: %s\n", why.c_str());
+    return patInvalidSchedule;
+  }
+  const Schedule& s = c.sched;
+  const int kind = static_cast<int>(s.kind);
+  const int n = s.n;
+  if (static_cast<int>(s.rounds.size()) > kMaxRounds) return patInvalidArgument;
+  KPlan& p = c.proto;
+  std::memset(&p, 0, sizeof(p));
+  p.n = n;
+  p.kind = kind;
+  p.nrounds = static_cast<int>(s.rounds.size());
+  int slot = 0;
+  std::vector<int> slot_of_round_pos;  // flattened
+  for (int t = 0; t < p.nrounds; ++t) {
+    const Round& r = s.rounds[t];
+    if (static_cast<int>(r.chunks.size()) > kMaxChunks || r.exchange) return patInvalidArgument;
+    KRound& kr = p.rounds[t];
+    kr.peer = static_cast<int8_t>(mod_ranks(r.peer, n));
+    kr.nchunks = static_cast<int8_t>(r.chunks.size());
+    kr.slot_base = static_cast<int8_t>(slot);
+    for (size_t pos = 0; pos < r.chunks.size(); ++pos) {
+      if (slot >= kMaxSlots) return patInvalidArgument;
+      kr.chunk[pos] = static_cast<int8_t>(r.chunks[pos]);
+      p.slot_round[slot] = static_cast<int8_t>(t);
+      p.slot_offset[slot] = static_cast<int8_t>(received_offset(r, r.chunks[pos], n));
+      ++slot;
+    }
+  }
+  p.nslots = slot;
+  // sources of every send, in reference order
+  for (int t = 0; t < p.nrounds; ++t) {
+    KRound& kr = p.rounds[t];
+    for (int pos = 0; pos < kr.nchunks; ++pos) {
+      const int k = kr.chunk[pos];
+      int na = 0;
+      for (int j = 0; j < kr.slot_base; ++j) {  // slots filled by earlier rounds, round order
+        if (p.slot_offset[j] != k) continue;
+        if (na >= kMaxArr) return patInvalidArgument;
+        kr.arr[pos][na++] = static_cast<int8_t>(j);
+      }
+      if (kind == kAG) {
+        if ((k == 0) != (na == 0)) return patInternalError;  // AG: own chunk or a held arrival
+        na = std::min(na, 1);
+      }
+      kr.narr[pos] = static_cast<int8_t>(na);
+    }
+  }
+  for (int j = 0; j < p.nslots; ++j)
+    if (p.slot_offset[j] == 0) p.fin[p.nfin++] = static_cast<int8_t>(j);
+  for (int t = 0; t < p.nrounds; ++t) {
+    bool seen = false;
+    for (int k = 0; k < p.npeers; ++k) seen |= p.peers[k] == p.rounds[t].peer;
+    if (!seen) p.peers[p.npeers++] = p.rounds[t].peer;
+  }
+  c.peak_slots = schedule_stats(s, 1).peak;
+  auto ins = comm->compiled.emplace(std::move(key), std::move(c));
+  *out = &ins.first->second;
+  return patSuccess;
+}
+
+// The PAT schedule for (kind, trees) (algorithms.cpp:191-249), compiled once per communicator.
+patResult_t compile(patComm* comm, int kind, int trees, Compiled** out) {
+  const int key = kind * 64 + trees;
+  auto it = comm->pat_cache.find(key);
+  if (it != comm->pat_cache.end()) {
+    *out = it->second;
+    return patSuccess;
+  }
+  Schedule s;
+  if (Err e = build(static_cast<Kind>(kind), Algo::Pat, comm->n, trees, &s)) return to_result(e);
+  if (patResult_t e = compile_schedule(comm, s, out)) return e;
+  comm->pat_cache[key] = *out;
+  return patSuccess;
+}
+
+struct Slicing {
+  int proto, channels, iters;
+  int64_t slice;
+};
+
+Slicing choose_slicing(const patComm* comm, int64_t chunk_bytes) {
+  Slicing s{};
+  int proto = comm->cfg.protocol;
+  if (proto == patProtoAuto) proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold) ? kProtoLL : kProtoSimple;
+  s.proto = proto;
+  const int64_t cap = proto == kProtoLL ? static_cast<int64_t>(comm->slot_bytes / 2) : static_cast<int64_t>(comm->slot_bytes);
+  const int64_t minslice = proto == kProtoLL ? 512 : 16 << 10;
+  int64_t per = (chunk_bytes + comm->channels - 1) / comm->channels;
+  per = (per + 15) & ~int64_t(15);
+  per = std::max<int64_t>(per, std::min<int64_t>(minslice, cap));
+  per = std::min<int64_t>(per, cap);
+  s.slice = std::max<int64_t>(per, 16);
+  const int64_t nslices = std::max<int64_t>(1, (chunk_bytes + s.slice - 1) / s.slice);
+  s.channels = static_cast<int>(std::min<int64_t>(comm->channels, nslices));
+  s.iters = static_cast<int>((nslices + s.channels - 1) / s.channels);
+  return s;
+}
+
+patResult_t alloc_pool(patComm* comm, int device, char** pool) {
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaMalloc(pool, comm->pool_bytes));
+  CUDA_TRY(cudaMemset(*pool, 0, comm->pool_bytes));
+  return patSuccess;
+}
+
+patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
+  if (nranks < 1 || nranks > PAT_MAX_RANKS) return patInvalidArgument;
+  comm->n = nranks;
+  patConfig_t c{};
+  if (config) std::memcpy(&c, config, std::min(sizeof(c), config->size ? config->size : sizeof(c)));
+  c.size = sizeof(c);
+  fill_defaults(&c, nranks);
+  if (c.trees != 0) {
+    if (!is_pow2(c.trees) || c.trees > max_trees(nranks)) return patInvalidTreeCount;
+  }
+  comm->cfg = c;
+  comm->channels = c.max_channels;
+  comm->slot_bytes = c.slice_bytes;
+  const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
+  comm->pool_bytes = kFlagBytes + static_cast<size_t>(comm->channels) * 2 * slots * comm->slot_bytes;
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&comm->err_host), sizeof(int),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  *comm->err_host = 0;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&comm->err_dev), comm->err_host, 0));
+  return patSuccess;
+}
+
+patResult_t setup_groups(patComm* comm) {
+  std::map<int, int> gi;
+  for (size_t l = 0; l < comm->ldevs.size(); ++l) {
+    const int d = comm->ldevs[l];
+    if (!gi.count(d)) {
+      gi[d] = static_cast<int>(comm->groups.size());
+      DevGroup g;
+      g.device = d;
+      comm->groups.push_back(g);
+    }
+    comm->groups[gi[d]].lidx.push_back(static_cast<int>(l));
+  }
+  for (DevGroup& g : comm->groups) {
+    if (g.lidx.size() > static_cast<size_t>(kMaxLocal)) return patInvalidArgument;
+    CUDA_TRY(cudaSetDevice(g.device));
+    CUDA_TRY(cudaDeviceGetAttribute(&g.sm_count, cudaDevAttrMultiProcessorCount, g.device));
+    const size_t bytes = sizeof(uint64_t) * kMaxChannels * g.lidx.size();
+    CUDA_TRY(cudaMalloc(&g.iter_state, bytes));
+    CUDA_TRY(cudaMemset(g.iter_state, 0, bytes));
+  }
+  comm->events.resize(comm->lranks.size());
+  for (size_t l = 0; l < comm->lranks.size(); ++l) {
+    CUDA_TRY(cudaSetDevice(comm->ldevs[l]));
+    CUDA_TRY(cudaEventCreateWithFlags(&comm->events[l], cudaEventDisableTiming));
+  }
+  return patSuccess;
+}
+
+patResult_t check_async(patComm* comm) {
+  const int e = *reinterpret_cast<volatile int*>(comm->err_host);
+  return e ? static_cast<patResult_t>(e) : patSuccess;
+}
+
+patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs, void* const* recvbuffs,
+                           size_t count, int dtype, int op, const patStream_t* streams,
+                           const Schedule* explicit_sched = nullptr) {
+  if (!comm || !comm->finished) return patInvalidUsage;
+  const size_t es = dtype_size(dtype);
+  if (!es) return patInvalidArgument;
+  if (op < 0 || op >= patNumOps) return patUnsupportedOp;
+  if (count == 0) return patSuccess;
+  if (!sendbuffs || !recvbuffs) return patInvalidArgument;
+  if (patResult_t e = check_async(comm)) return e;
+  std::lock_guard<std::mutex> lock(comm->mu);
+  const int n = comm->n;
+  const int trees = comm->cfg.trees ? comm->cfg.trees : max_trees(n);
+  Compiled* cp = nullptr;
+  if (explicit_sched) {
+    if (static_cast<int>(explicit_sched->kind) != kind) return patSimulationError;
+    if (patResult_t e = compile_schedule(comm, *explicit_sched, &cp)) return e;
+  } else if (patResult_t e = compile(comm, kind, trees, &cp)) {
+    return e;
+  }
+  const int64_t chunk_bytes = static_cast<int64_t>(count * es);
+  const Slicing sl = choose_slicing(comm, chunk_bytes);
+  int vec = 16;
+  bool aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
+  for (size_t l = 0; l < comm->lranks.size(); ++l) {
+    if (!sendbuffs[l] || !recvbuffs[l]) return patInvalidArgument;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(sendbuffs[l]) | reinterpret_cast<uintptr_t>(recvbuffs[l]);
+    aligned16 &= (a % 16) == 0;
+    aligned8 &= (a % 8) == 0;
+  }
+  vec = aligned16 ? 16 : (aligned8 ? 8 : 0);
+  if (sl.proto == kProtoSimple && vec == 8) vec = 0;  // SIMPLE vectors are 16 bytes
+  DeviceGuard guard;
+  for (DevGroup& g : comm->groups) {
+    KPlan p = cp->proto;
+    p.nlocal = static_cast<int>(g.lidx.size());
+    p.proto = sl.proto;
+    p.vec = vec;
+    p.esize = static_cast<int>(es);
+    p.channels = sl.channels;
+    p.iters = sl.iters;
+    p.chunk_bytes = chunk_bytes;
+    p.slice_bytes = sl.slice;
+    p.slot_stride = static_cast<int64_t>(comm->slot_bytes);
+    p.chan_stride = 2 * static_cast<int64_t>(std::max(n - 1, 1)) * p.slot_stride;
+    p.timeout_ns = static_cast<uint64_t>(comm->cfg.timeout_ms) * 1000000ull;
+    p.err = comm->err_dev;
+    for (int r = 0; r < n; ++r) {
+      p.flags[r] = reinterpret_cast<uint64_t*>(g.pool_view[r]);
+      p.inbox[r] = g.pool_view[r] + kFlagBytes;
+    }
+    for (size_t i = 0; i < g.lidx.size(); ++i) {
+      const int l = g.lidx[i];
+      p.rank[i] = comm->lranks[l];
+      p.send[i] = static_cast<const char*>(sendbuffs[l]);
+      p.recv[i] = static_cast<char*>(recvbuffs[l]);
+      p.iter_state[i] = g.iter_state + i * kMaxChannels;
+    }
+    CUDA_TRY(cudaSetDevice(g.device));
+    const int threads = comm->cfg.threads;
+    const std::array<int, 5> okey{kind, dtype, op, threads, g.device};
+    auto oit = comm->occupancy.find(okey);
+    if (oit == comm->occupancy.end()) {
+      int nb = 0;
+      CUDA_TRY(max_blocks_per_sm(kind, dtype, op, threads, &nb));
+      oit = comm->occupancy.emplace(okey, nb).first;
+    }
+    if (p.nlocal * p.channels > oit->second * g.sm_count) {
+      std::fprintf(stderr, "pat_b200: %d CTAs exceed co-residency (%d per SM x %d SMs)\n",
+                   p.nlocal * p.channels, oit->second, g.sm_count);
+      return patInvalidUsage;
+    }
+    cudaStream_t s0 = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr;
+    for (size_t i = 1; i < g.lidx.size(); ++i) {  // join the other local ranks' streams
+      cudaStream_t si = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[i]]) : nullptr;
+      if (si == s0) continue;
+      CUDA_TRY(cudaEventRecord(comm->events[g.lidx[i]], si));
+      CUDA_TRY(cudaStreamWaitEvent(s0, comm->events[g.lidx[i]], 0));
+    }
+    CUDA_TRY(launch(p, dtype, op, threads, s0));
+    CUDA_TRY(cudaEventRecord(comm->events[g.lidx[0]], s0));
+    for (size_t i = 1; i < g.lidx.size(); ++i) {
+      cudaStream_t si = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[i]]) : nullptr;
+      if (si == s0) continue;
+      CUDA_TRY(cudaStreamWaitEvent(si, comm->events[g.lidx[0]], 0));
+    }
+  }
+  return patSuccess;
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+
+#pragma GCC visibility push(default)
+extern "C" {
+
+const char* patGetErrorString(patResult_t r) {
+  switch (r) {
+    case patSuccess: return "success";
+    case patUnhandledCudaError: return "unhandled CUDA error";
+    case patSystemError: return "system error (peer access / IPC)";
+    case patInternalError: return "internal error";
+    case patInvalidArgument: return "invalid argument";
+    case patInvalidUsage: return "invalid usage";
+    case patRemoteError: return "remote error";
+    case patScheduleError: return "ScheduleError";
+    case patNonPowerOfTwo: return "NonPowerOfTwoError";
+    case patInvalidTreeCount: return "InvalidTreeCountError";
+    case patBufferTooSmall: return "BufferTooSmallError";
+    case patRankOutOfRange: return "RankOutOfRangeError";
+    case patSimulationError: return "SimulationError";
+    case patPayloadShape: return "PayloadShapeError";
+    case patUnsupportedOp: return "UnsupportedOpError";
+    case patInvalidSchedule: return "InvalidScheduleError";
+    case patTimeout: return "device wait timed out";
+    case patCapacity: return "output buffer too small";
+  }
+  return "unknown error";
+}
+
+patResult_t patGetVersion(int* v) {
+  if (!v) return patInvalidArgument;
+  *v = PAT_B200_VERSION;
+  return patSuccess;
+}
+
+patResult_t patConfigInit(patConfig_t* c) {
+  if (!c) return patInvalidArgument;
+  std::memset(c, 0, sizeof(*c));
+  c->size = sizeof(*c);
+  return patSuccess;
+}
+
+patResult_t patCommInitAll(patComm_t* out, int nranks, const int* devlist, const patConfig_t* config) {
+  if (!out) return patInvalidArgument;
+  *out = nullptr;
+  auto comm = std::make_unique<patComm>();
+  if (patResult_t e = common_init(comm.get(), nranks, config)) return e;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  DeviceGuard guard;
+  for (int r = 0; r < nranks; ++r) {
+    const int d = devlist ? devlist[r] : r;
+    if (d < 0 || d >= ndev) return patInvalidArgument;
+    comm->lranks.push_back(r);
+    comm->ldevs.push_back(d);
+  }
+  for (int r = 0; r < nranks; ++r) {
+    char* pool = nullptr;
+    if (patResult_t e = alloc_pool(comm.get(), comm->ldevs[r], &pool)) return e;
+    comm->owned_pool.push_back(pool);
+  }
+  // peer access between every pair of distinct devices
+  std::vector<int> devs(comm->ldevs);
+  std::sort(devs.begin(), devs.end());
+  devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+  for (int a : devs)
+    for (int b : devs) {
+      if (a == b) continue;
+      int can = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) {
+        std::fprintf(stderr, "pat_b200: device %d cannot access peer %d\n", a, b);
+        return patSystemError;
+      }
+      CUDA_TRY(cudaSetDevice(a));
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return patSystemError;
+    }
+  if (patResult_t e = setup_groups(comm.get())) return e;
+  for (DevGroup& g : comm->groups)
+    for (int r = 0; r < nranks; ++r) g.pool_view[r] = comm->owned_pool[r];
+  comm->finished = true;
+  *out = comm.release();
+  return patSuccess;
+}
+
+patResult_t patCommInitRankPrepare(patComm_t* out, int nranks, int rank, int device, const patConfig_t* config,
+                                   void* handle_out) {
+  if (!out || !handle_out) return patInvalidArgument;
+  *out = nullptr;
+  if (rank < 0 || rank >= nranks) return patRankOutOfRange;
+  auto comm = std::make_unique<patComm>();
+  comm->multiprocess = true;
+  if (patResult_t e = common_init(comm.get(), nranks, config)) return e;
+  DeviceGuard guard;
+  comm->lranks.push_back(rank);
+  comm->ldevs.push_back(device);
+  char* pool = nullptr;
+  if (patResult_t e = alloc_pool(comm.get(), device, &pool)) return e;
+  comm->owned_pool.push_back(pool);
+  Handle h{};
+  h.magic = kMagic;
+  h.version = PAT_B200_VERSION;
+  h.nranks = nranks;
+  h.rank = rank;
+  h.device = device;
+  h.channels = comm->channels;
+  h.pool_bytes = comm->pool_bytes;
+  h.slot_bytes = comm->slot_bytes;
+  h.pid = static_cast<int32_t>(getpid());
+  CUDA_TRY(cudaIpcGetMemHandle(&h.ipc, pool));
+  std::memset(handle_out, 0, PAT_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  if (patResult_t e = setup_groups(comm.get())) return e;
+  *out = comm.release();
+  return patSuccess;
+}
+
+patResult_t patCommInitRankFinish(patComm_t comm, const void* all_handles) {
+  if (!comm || !all_handles || !comm->multiprocess || comm->finished) return patInvalidUsage;
+  DeviceGuard guard;
+  DevGroup& g = comm->groups[0];
+  CUDA_TRY(cudaSetDevice(g.device));
+  for (int r = 0; r < comm->n; ++r) {
+    Handle h;
+    std::memcpy(&h, static_cast<const char*>(all_handles) + static_cast<size_t>(r) * PAT_HANDLE_BYTES, sizeof(h));
+    if (h.magic != kMagic || h.version != PAT_B200_VERSION || h.nranks != comm->n || h.rank != r ||
+        h.pool_bytes != comm->pool_bytes || h.slot_bytes != comm->slot_bytes || h.channels != comm->channels) {
+      std::fprintf(stderr, "pat_b200: handle %d inconsistent (rank %d, pool %llu vs %llu)\n", r, h.rank,
+                   (unsigned long long)h.pool_bytes, (unsigned long long)comm->pool_bytes);
+      return patInvalidUsage;
+    }
+    if (r == comm->lranks[0]) {
+      g.pool_view[r] = comm->owned_pool[0];
+      continue;
+    }
+    void* ptr = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+    comm->ipc_opened.push_back(ptr);
+    g.pool_view[r] = static_cast<char*>(ptr);
+  }
+  comm->finished = true;
+  return patSuccess;
+}
+
+patResult_t patCommDestroy(patComm_t comm) {
+  if (!comm) return patInvalidArgument;
+  {
+    DeviceGuard guard;
+    for (size_t l = 0; l < comm->ldevs.size(); ++l) {
+      cudaSetDevice(comm->ldevs[l]);
+      cudaDeviceSynchronize();
+    }
+    for (DevGroup& g : comm->groups) {
+      cudaSetDevice(g.device);
+      for (void* p : comm->ipc_opened) cudaIpcCloseMemHandle(p);
+      comm->ipc_opened.clear();
+      if (g.iter_state) cudaFree(g.iter_state);
+    }
+    for (size_t l = 0; l < comm->owned_pool.size(); ++l) {
+      cudaSetDevice(comm->ldevs[l]);
+      cudaFree(comm->owned_pool[l]);
+    }
+    for (size_t l = 0; l < comm->events.size(); ++l)
+      if (comm->events[l]) cudaEventDestroy(comm->events[l]);
+    if (comm->err_host) cudaFreeHost(comm->err_host);
+  }
+  delete comm;
+  return patSuccess;
+}
+
+patResult_t patCommCount(patComm_t comm, int* n) {
+  if (!comm || !n) return patInvalidArgument;
+  *n = comm->n;
+  return patSuccess;
+}
+
+patResult_t patCommLocalRanks(patComm_t comm, int* nlocal, int* ranks, int* devices) {
+  if (!comm || !nlocal) return patInvalidArgument;
+  *nlocal = static_cast<int>(comm->lranks.size());
+  for (size_t l = 0; l < comm->lranks.size(); ++l) {
+    if (ranks) ranks[l] = comm->lranks[l];
+    if (devices) devices[l] = comm->ldevs[l];
+  }
+  return patSuccess;
+}
+
+patResult_t patCommGetAsyncError(patComm_t comm, patResult_t* e) {
+  if (!comm || !e) return patInvalidArgument;
+  *e = check_async(comm);
+  return patSuccess;
+}
+
+patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDataType_t dtype, patPlanInfo_t* info) {
+  if (!comm || !info) return patInvalidArgument;
+  const size_t es = dtype_size(dtype);
+  if (!es) return patInvalidArgument;
+  std::lock_guard<std::mutex> lock(comm->mu);
+  const int trees = comm->cfg.trees ? comm->cfg.trees : max_trees(comm->n);
+  Compiled* cp = nullptr;
+  if (patResult_t e = compile(comm, kind, trees, &cp)) return e;
+  const int64_t cb = static_cast<int64_t>(count * es);
+  const Slicing sl = choose_slicing(comm, cb);
+  std::memset(info, 0, sizeof(*info));
+  info->protocol = sl.proto;
+  info->trees = trees;
+  info->rounds = cp->proto.nrounds;
+  info->channels = sl.channels;
+  info->iterations = sl.iters;
+  info->threads = comm->cfg.threads;
+  info->launches = static_cast<int>(comm->groups.size());
+  info->slots_per_step = cp->proto.nslots;
+  info->slice_bytes = static_cast<size_t>(sl.slice);
+  info->pool_bytes = static_cast<size_t>(sl.channels) * 2 * cp->proto.nslots * comm->slot_bytes + kFlagBytes;
+  info->bytes_sent_per_rank = static_cast<int64_t>(comm->n - 1) * cb;
+  info->peak_intermediate_slots = cp->peak_slots;
+  return patSuccess;
+}
+
+patResult_t patAllGather(patComm_t comm, const void* const* sendbuffs, void* const* recvbuffs, size_t sendcount,
+                         patDataType_t datatype, const patStream_t* streams) {
+  return run_collective(comm, kAG, sendbuffs, recvbuffs, sendcount, datatype, patSum, streams);
+}
+
+patResult_t patReduceScatter(patComm_t comm, const void* const* sendbuffs, void* const* recvbuffs,
+                             size_t recvcount, patDataType_t datatype, patRedOp_t op, const patStream_t* streams) {
+  return run_collective(comm, kRS, sendbuffs, recvbuffs, recvcount, datatype, op, streams);
+}
+
+patResult_t patAllGatherSchedule(patComm_t comm, const int32_t* sched, size_t len, const void* const* sendbuffs,
+                                 void* const* recvbuffs, size_t sendcount, patDataType_t datatype,
+                                 const patStream_t* streams) {
+  Schedule s;
+  if (Err e = decode(sched, len, &s)) return to_result(e);
+  return run_collective(comm, kAG, sendbuffs, recvbuffs, sendcount, datatype, patSum, streams, &s);
+}
+
+patResult_t patReduceScatterSchedule(patComm_t comm, const int32_t* sched, size_t len, const void* const* sendbuffs,
+                                     void* const* recvbuffs, size_t recvcount, patDataType_t datatype,
+                                     patRedOp_t op, const patStream_t* streams) {
+  Schedule s;
+  if (Err e = decode(sched, len, &s)) return to_result(e);
+  return run_collective(comm, kRS, sendbuffs, recvbuffs, recvcount, datatype, op, streams, &s);
+}
+
+// ---------------------------------------------------------------- schedules (host only)
+
+static patResult_t put(const std::vector<int32_t>& v, int32_t* buf, size_t cap, size_t* len) {
+  if (len) *len = v.size();
+  if (!buf || cap < v.size()) return patCapacity;
+  std::memcpy(buf, v.data(), v.size() * sizeof(int32_t));
+  return patSuccess;
+}
+
+patResult_t patScheduleBuild(int kind, int algorithm, int nranks, int trees, int32_t* buf, size_t cap, size_t* len) {
+  if (kind < 0 || kind > 1 || algorithm < 0 || algorithm > 4) return patInvalidArgument;
+  Schedule s;
+  if (Err e = build(static_cast<Kind>(kind), static_cast<Algo>(algorithm), nranks, trees, &s)) return to_result(e);
+  return put(encode(s), buf, cap, len);
+}
+
+patResult_t patScheduleMirror(const int32_t* in, size_t len, int32_t* out, size_t cap, size_t* out_len) {
+  Schedule s;
+  if (Err e = decode(in, len, &s)) return to_result(e);
+  return put(encode(mirror(s)), out, cap, out_len);
+}
+
+patResult_t patScheduleValidate(const int32_t* sched, size_t len, int* nviolations, char* first, size_t cap) {
+  if (!nviolations) return patInvalidArgument;
+  Schedule s;
+  if (Err e = decode(sched, len, &s)) return to_result(e);
+  std::string msg;
+  *nviolations = validate(s, &msg);
+  if (first && cap) {
+    std::strncpy(first, msg.c_str(), cap - 1);
+    first[cap - 1] = 0;
+  }
+  return patSuccess;
+}
+
+patResult_t patScheduleStats(const int32_t* sched, size_t len, int64_t chunk_bytes, patExecStats_t* st) {
+  if (!st) return patInvalidArgument;
+  Schedule s;
+  if (Err e = decode(sched, len, &s)) return to_result(e);
+  const Stats x = schedule_stats(s, chunk_bytes);
+  std::memset(st, 0, sizeof(*st));
+  st->rounds = x.rounds;
+  st->max_chunks_per_message = x.max_chunks;
+  st->messages = x.messages;
+  st->bytes_sent_per_rank = x.bytes_sent_per_rank;
+  st->peak_intermediate_slots = x.peak;
+  st->n_occupancy = static_cast<int32_t>(x.occupancy.size());
+  for (size_t i = 0; i < x.occupancy.size() && i < 512; ++i) st->occupancy_per_round[i] = x.occupancy[i];
+  return patSuccess;
+}
+
+patResult_t patScheduleTraceCsv(const int32_t* sched, size_t len, int64_t chunk_bytes, char* buf, size_t cap,
+                                size_t* out_len) {
+  Schedule s;
+  if (Err e = decode(sched, len, &s)) return to_result(e);
+  std::string out = "round,dim,split,sender,receiver,chunks,bytes\n";
+  char line[160];
+  for (const Round& r : s.rounds)
+    for (int snd = 0; snd < s.n; ++snd) {
+      const int recv = r.exchange ? (snd ^ std::abs(r.peer)) : mod_ranks(int64_t{snd} + r.peer, s.n);
+      std::snprintf(line, sizeof line, "%d,%d,%d,%d,%d,%zu,%lld\n", r.index, r.dim, r.split, snd, recv,
+                    r.chunks.size(), static_cast<long long>(chunk_bytes * static_cast<int64_t>(r.chunks.size())));
+      out += line;
+    }
+  if (out_len) *out_len = out.size();
+  if (!buf || cap <= out.size()) return patCapacity;
+  std::memcpy(buf, out.c_str(), out.size() + 1);
+  return patSuccess;
+}
+
+patResult_t patMaxTrees(int n, int* t) {
+  if (!t || n < 1) return patScheduleError;
+  *t = max_trees(n);
+  return patSuccess;
+}
+
+patResult_t patTreesFromBuffer(int64_t b, int64_t c, int n, int* t) {
+  if (!t) return patInvalidArgument;
+  return to_result(trees_from_buffer(b, c, n, t));
+}
+
+patResult_t patPatBufferSlots(int n, int trees, int* slots) {
+  if (!slots) return patInvalidArgument;
+  *slots = pat_buffer_slots(n, trees);
+  return patSuccess;
+}
+
+patResult_t patRoundCountFormula(int n, int trees, int* rounds) {
+  if (!rounds) return patInvalidArgument;
+  return to_result(round_count_formula(n, trees, rounds));
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

@@ -1,0 +1,535 @@
+// kernels.cu — sm_100a kernels for PAT all-gather and reduce-scatter.
+//
+// One cooperative launch per device per collective. CTA (lr, c) runs channel c of local rank
+// lr through `iters` pipeline steps; step i moves slice (i*channels + c) of every chunk
+// through all PAT rounds. Per round the rank pushes its <= T chunk slices into the inbox of
+// peer (r + peer) over NVLink (or HBM in local mode), then signals; receivers fold or copy
+// from their own inbox. This replaces the reference executor's send/deliver phases
+// (simulate.cpp:180-218 all-gather, :247-296 reduce-scatter) and its Mailbox rendezvous +
+// lockstep join (simulate.cpp:49-70, 131-149) with per-step release/acquire flags.
+//
+// Two protocols:
+//  * LL (small messages): 16-byte lines {data32, flag, data32, flag} stored with one
+//    st.volatile.v4 into the peer's inbox; the receiver polls the line itself, so data and
+//    signal travel together and no fence or separate flag is needed. 50% wire efficiency.
+//  * SIMPLE (bulk): 16-byte vector stores of the slice, fence.sc.sys per thread, CTA barrier,
+//    then one st.relaxed.sys flag word per (channel, round) at the receiver.
+// Inbox slots are double-buffered by step parity; a rank re-uses a peer's slot buffer only
+// after that peer published "done with step g-2" (credit flags), so the pool is bounded:
+// channels * 2 * (n-1) slots per rank, independent of the message size.
+//
+// Reduction order (reduce-scatter) is the reference's exactly: a forwarded offset carries
+// fold(arrivals in round order) (+) own contribution (simulate.cpp:257-266, 281-285); the
+// output is own (+) offset-0 arrivals in round order (simulate.cpp:239, 278-279). Each fold
+// is rounded to the wire dtype (fp16/bf16 computed in fp32, RNE).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "plan.hpp"
+
+namespace pat {
+
+// ------------------------------------------------------------------------- memory primitives
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint4 ld16(const void* p) {  // L2-coherent (bypasses a stale L1)
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st16(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_ll(void* p, uint2 v, uint32_t flag) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(flag), "r"(v.y),
+               "r"(flag)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_volatile16(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+template <int B>
+__device__ __forceinline__ uint64_t ld_cg_bytes(const char* p) {
+  if constexpr (B == 1) {
+    unsigned short v;
+    asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+    return v & 0xff;
+  } else if constexpr (B == 2) {
+    unsigned short v;
+    asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+    return v;
+  } else if constexpr (B == 4) {
+    uint32_t v;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+  } else {
+    uint64_t v;
+    asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+  }
+}
+__device__ __forceinline__ uint64_t ld_elem(const char* p, int esize) {
+  switch (esize) {
+    case 1: return ld_cg_bytes<1>(p);
+    case 2: return ld_cg_bytes<2>(p);
+    case 4: return ld_cg_bytes<4>(p);
+    default: return ld_cg_bytes<8>(p);
+  }
+}
+__device__ __forceinline__ void st_elem(char* p, uint64_t v, int esize) {
+  switch (esize) {
+    case 1: *reinterpret_cast<volatile uint8_t*>(p) = static_cast<uint8_t>(v); break;
+    case 2: *reinterpret_cast<volatile uint16_t*>(p) = static_cast<uint16_t>(v); break;
+    case 4: *reinterpret_cast<volatile uint32_t*>(p) = static_cast<uint32_t>(v); break;
+    default: *reinterpret_cast<volatile uint64_t*>(p) = v; break;
+  }
+}
+
+// ------------------------------------------------------------------------- element folds
+
+enum : int { kSum = 0, kProd = 1, kMax = 2, kMin = 3 };
+enum : int { kI8 = 0, kU8 = 1, kI32 = 2, kU32 = 3, kI64 = 4, kU64 = 5, kF16 = 6, kF32 = 7, kF64 = 8, kBF16 = 9 };
+
+template <int DT> struct DType;
+template <> struct DType<kI8> { using S = int8_t; using U = uint8_t; static constexpr int cls = 0; };
+template <> struct DType<kU8> { using S = uint8_t; using U = uint8_t; static constexpr int cls = 0; };
+template <> struct DType<kI32> { using S = int32_t; using U = uint32_t; static constexpr int cls = 0; };
+template <> struct DType<kU32> { using S = uint32_t; using U = uint32_t; static constexpr int cls = 0; };
+template <> struct DType<kI64> { using S = int64_t; using U = uint64_t; static constexpr int cls = 0; };
+template <> struct DType<kU64> { using S = uint64_t; using U = uint64_t; static constexpr int cls = 0; };
+template <> struct DType<kF32> { using S = float; using U = float; static constexpr int cls = 1; };
+template <> struct DType<kF64> { using S = double; using U = double; static constexpr int cls = 1; };
+template <> struct DType<kF16> { using S = uint16_t; using U = uint16_t; static constexpr int cls = 2; };
+template <> struct DType<kBF16> { using S = uint16_t; using U = uint16_t; static constexpr int cls = 3; };
+
+template <int OP, typename T>
+__device__ __forceinline__ T apply(T x, T y) {
+  if constexpr (OP == kSum) return x + y;
+  else if constexpr (OP == kProd) return x * y;
+  else if constexpr (OP == kMax) return y > x ? y : x;
+  else return y < x ? y : x;
+}
+
+// a = a (op) b; `a` is the accumulator (left operand), as fold_one in simulate.cpp:31-39.
+template <int DT, int OP>
+__device__ __forceinline__ typename DType<DT>::S fold1(typename DType<DT>::S a, typename DType<DT>::S b) {
+  using D = DType<DT>;
+  using S = typename D::S;
+  using U = typename D::U;
+  if constexpr (D::cls == 0) {
+    if constexpr (OP == kSum) return static_cast<S>(static_cast<U>(a) + static_cast<U>(b));
+    else if constexpr (OP == kProd) return static_cast<S>(static_cast<U>(a) * static_cast<U>(b));
+    else return apply<OP>(a, b);
+  } else if constexpr (D::cls == 1) {
+    return apply<OP>(a, b);
+  } else if constexpr (D::cls == 2) {
+    const float r = apply<OP>(__half2float(__ushort_as_half(a)), __half2float(__ushort_as_half(b)));
+    return __half_as_ushort(__float2half_rn(r));
+  } else {
+    const float r = apply<OP>(__bfloat162float(__ushort_as_bfloat16(a)), __bfloat162float(__ushort_as_bfloat16(b)));
+    return __bfloat16_as_ushort(__float2bfloat16_rn(r));
+  }
+}
+
+template <int DT, int OP, typename V>
+__device__ __forceinline__ void fold_vec(V& a, const V& b) {
+  using S = typename DType<DT>::S;
+  constexpr int N = sizeof(V) / sizeof(S);
+  union U {
+    V v;
+    S e[N];
+  } x, y;
+  x.v = a;
+  y.v = b;
+#pragma unroll
+  for (int i = 0; i < N; ++i) x.e[i] = fold1<DT, OP>(x.e[i], y.e[i]);
+  a = x.v;
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ uint64_t fold_elem_bits(uint64_t a, uint64_t b) {
+  using S = typename DType<DT>::S;
+  S x, y;
+  memcpy(&x, &a, sizeof(S));
+  memcpy(&y, &b, sizeof(S));
+  x = fold1<DT, OP>(x, y);
+  uint64_t r = 0;
+  memcpy(&r, &x, sizeof(S));
+  return r;
+}
+
+// ------------------------------------------------------------------------- waits
+
+struct Waiter {
+  uint64_t timeout_ns;
+  int* err;
+  bool aborted;
+};
+
+__device__ __noinline__ void report_timeout(Waiter& w) {
+  if (!w.aborted) {
+    atomicCAS_system(w.err, 0, 40 /* patTimeout */);
+    w.aborted = true;
+  }
+}
+
+// Spin until *flag >= want (acquire). Thread-level; callers broadcast with a barrier.
+__device__ __forceinline__ void wait_flag(const uint64_t* flag, uint64_t want, Waiter& w) {
+  if (w.aborted) return;
+  uint64_t start = 0;
+  uint32_t spins = 0;
+  while (ld_acquire_sys(flag) < want) {
+    if ((++spins & 1023u) == 0) {
+      const uint64_t now = globaltimer();
+      if (start == 0) start = now;
+      else if (now - start > w.timeout_ns) { report_timeout(w); return; }
+    }
+  }
+}
+
+// Poll one LL line until both flag words carry `flag`; returns its 8 data bytes.
+__device__ __forceinline__ uint2 ld_ll(const char* line, uint32_t flag, Waiter& w) {
+  uint4 v = ld_volatile16(line);
+  if (v.y == flag && v.w == flag) return make_uint2(v.x, v.z);
+  uint64_t start = 0;
+  uint32_t spins = 0;
+  while (!w.aborted) {
+    v = ld_volatile16(line);
+    if (v.y == flag && v.w == flag) break;
+    if ((++spins & 1023u) == 0) {
+      const uint64_t now = globaltimer();
+      if (start == 0) start = now;
+      else if (now - start > w.timeout_ns) report_timeout(w);
+    }
+  }
+  return make_uint2(v.x, v.z);
+}
+
+// ------------------------------------------------------------------------- CTA data movers
+
+// dst = fold_left(src[0], ..., src[m-1]) over `len` bytes (16-byte vectors; len % 16 == 0).
+template <int DT, int OP>
+__device__ __forceinline__ void cta_fold16(char* dst, const char* const* src, int m, int64_t len) {
+  const int64_t nu = len >> 4;
+  const int64_t B = blockDim.x;
+  int64_t u = threadIdx.x;
+  if (m == 1) {
+    const char* s0 = src[0];
+    for (; u + 3 * B < nu; u += 4 * B) {
+      const uint4 a = ld16(s0 + 16 * u), b = ld16(s0 + 16 * (u + B));
+      const uint4 c = ld16(s0 + 16 * (u + 2 * B)), d = ld16(s0 + 16 * (u + 3 * B));
+      st16(dst + 16 * u, a);
+      st16(dst + 16 * (u + B), b);
+      st16(dst + 16 * (u + 2 * B), c);
+      st16(dst + 16 * (u + 3 * B), d);
+    }
+    for (; u < nu; u += B) st16(dst + 16 * u, ld16(s0 + 16 * u));
+    return;
+  }
+  for (; u + B < nu; u += 2 * B) {
+    uint4 a0 = ld16(src[0] + 16 * u), a1 = ld16(src[0] + 16 * (u + B));
+    for (int k = 1; k < m; ++k) {
+      const uint4 b0 = ld16(src[k] + 16 * u), b1 = ld16(src[k] + 16 * (u + B));
+      fold_vec<DT, OP>(a0, b0);
+      fold_vec<DT, OP>(a1, b1);
+    }
+    st16(dst + 16 * u, a0);
+    st16(dst + 16 * (u + B), a1);
+  }
+  for (; u < nu; u += B) {
+    uint4 a = ld16(src[0] + 16 * u);
+    for (int k = 1; k < m; ++k) fold_vec<DT, OP>(a, ld16(src[k] + 16 * u));
+    st16(dst + 16 * u, a);
+  }
+}
+
+// Element-granular variant for buffers that are not 16-byte aligned.
+template <int DT, int OP>
+__device__ __forceinline__ void cta_fold_elems(char* dst, const char* const* src, int m, int64_t len, int esize) {
+  const int64_t ne = len / esize;
+  for (int64_t e = threadIdx.x; e < ne; e += blockDim.x) {
+    uint64_t a = ld_elem(src[0] + e * esize, esize);
+    for (int k = 1; k < m; ++k) a = fold_elem_bits<DT, OP>(a, ld_elem(src[k] + e * esize, esize));
+    st_elem(dst + e * esize, a, esize);
+  }
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ void cta_fold(char* dst, const char* const* src, int m, int64_t len, const KPlan& p) {
+  if (len <= 0) return;
+  if (p.vec == 16) cta_fold16<DT, OP>(dst, src, m, len);
+  else cta_fold_elems<DT, OP>(dst, src, m, len, p.esize);
+}
+
+// 8-byte user words for LL (zero padded past `valid`).
+__device__ __forceinline__ uint2 load_word(const char* p, int valid, const KPlan& pl) {
+  if (valid == 8 && pl.vec >= 8) {
+    const uint64_t v = ld_cg_bytes<8>(p);
+    return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
+  }
+  uint64_t v = 0;
+  for (int b = 0; b < valid; b += pl.esize) v |= ld_elem(p + b, pl.esize) << (8 * b);
+  return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
+}
+__device__ __forceinline__ void store_word(char* p, uint2 w, int valid, const KPlan& pl) {
+  const uint64_t v = static_cast<uint64_t>(w.x) | (static_cast<uint64_t>(w.y) << 32);
+  if (valid == 8 && pl.vec >= 8) {
+    *reinterpret_cast<uint64_t*>(p) = v;
+    return;
+  }
+  for (int b = 0; b < valid; b += pl.esize) {
+    const uint64_t mask = pl.esize == 8 ? ~0ull : ((1ull << (8 * pl.esize)) - 1);
+    st_elem(p + b, (v >> (8 * b)) & mask, pl.esize);
+  }
+}
+
+// ------------------------------------------------------------------------- one pipeline step
+
+struct Step {
+  uint64_t g;        // absolute pipeline step of this channel
+  int64_t off, len;  // byte range of the slice within every chunk
+  int R, lr, c, buf;
+};
+
+__device__ __forceinline__ char* slot_ptr(const KPlan& p, int rank, int c, int buf, int j) {
+  return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j) * p.slot_stride;
+}
+
+// SIMPLE: CTA-cooperative copies/folds; flags per (channel, round).
+template <int DT, int OP, int KIND>
+__device__ void step_simple(const KPlan& p, const Step& s, Waiter& w) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const char* snd = p.send[s.lr];
+  char* out = p.recv[s.lr];
+  uint64_t* myflags = p.flags[s.R] + s.c * kFlagWords;
+  uint32_t waited = 0;
+  auto ensure = [&](int t) {
+    if (!((waited >> t) & 1u)) {
+      if (threadIdx.x == 0) wait_flag(myflags + t, s.g + 1, w);
+      __syncthreads();
+      waited |= 1u << t;
+    }
+  };
+  const char* srcs[kMaxArr + 1];
+
+  if constexpr (KIND == kAG) {
+    if (out + s.R * Cb != snd) {  // own chunk placement (simulate.cpp:160-165); skipped in place
+      srcs[0] = snd + s.off;
+      cta_fold<DT, OP>(out + s.R * Cb + s.off, srcs, 1, s.len, p);
+    }
+  }
+  for (int t = 0; t < p.nrounds; ++t) {
+    const KRound& r = p.rounds[t];
+    const int P = (s.R + r.peer) % n;
+    for (int pos = 0; pos < r.nchunks; ++pos) {
+      char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
+      int m = 0;
+      if constexpr (KIND == kAG) {
+        if (r.narr[pos] == 0) {
+          srcs[m++] = snd + s.off;
+        } else {
+          const int j = r.arr[pos][0];
+          ensure(p.slot_round[j]);
+          srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, j);
+        }
+      } else {
+        const int dest = (s.R - r.chunk[pos] + n) % n;
+        for (int a = 0; a < r.narr[pos]; ++a) {
+          const int j = r.arr[pos][a];
+          ensure(p.slot_round[j]);
+          srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, j);
+        }
+        srcs[m++] = snd + dest * Cb + s.off;  // own contribution folded last
+      }
+      cta_fold<DT, OP>(dst, srcs, m, s.len, p);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) st_relaxed_sys(p.flags[P] + s.c * kFlagWords + t, s.g + 1);
+  }
+  for (int t = 0; t < p.nrounds; ++t) ensure(t);
+  if constexpr (KIND == kAG) {
+    for (int j = 0; j < p.nslots; ++j) {
+      const int origin = (s.R - p.slot_offset[j] + n) % n;
+      srcs[0] = slot_ptr(p, s.R, s.c, s.buf, j);
+      cta_fold<DT, OP>(out + origin * Cb + s.off, srcs, 1, s.len, p);
+    }
+  } else {
+    int m = 0;
+    srcs[m++] = snd + s.R * Cb + s.off;  // output starts as own contribution (simulate.cpp:239)
+    for (int f = 0; f < p.nfin; ++f) srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, p.fin[f]);
+    cta_fold<DT, OP>(out + s.off, srcs, m, s.len, p);
+  }
+}
+
+// LL: every thread owns the same 8-byte words of the slice in every chunk and round, so it
+// only ever waits on lines it polls itself — no CTA barrier inside the step.
+template <int DT, int OP, int KIND>
+__device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const char* snd = p.send[s.lr];
+  char* out = p.recv[s.lr];
+  const uint32_t flag = static_cast<uint32_t>(s.g + 1);
+  const int64_t nlines = (s.len + 7) >> 3;
+  const int B = blockDim.x;
+
+  if constexpr (KIND == kAG) {
+    if (out + s.R * Cb != snd)
+      for (int64_t q = threadIdx.x; q < nlines; q += B) {
+        const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+        store_word(out + s.R * Cb + s.off + 8 * q, load_word(snd + s.off + 8 * q, valid, p), valid, p);
+      }
+  }
+  for (int t = 0; t < p.nrounds; ++t) {
+    const KRound& r = p.rounds[t];
+    const int P = (s.R + r.peer) % n;
+    for (int pos = 0; pos < r.nchunks; ++pos) {
+      char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
+      if constexpr (KIND == kAG) {
+        const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
+        for (int64_t q = threadIdx.x; q < nlines; q += B) {
+          const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+          const uint2 v = fwd ? ld_ll(fwd + 16 * q, flag, w) : load_word(snd + s.off + 8 * q, valid, p);
+          st_ll(dst + 16 * q, v, flag);
+        }
+      } else {
+        const int dest = (s.R - r.chunk[pos] + n) % n;
+        const char* own = snd + dest * Cb + s.off;
+        const int na = r.narr[pos];
+        for (int64_t q = threadIdx.x; q < nlines; q += B) {
+          const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+          uint2 acc;
+          if (na == 0) {
+            acc = load_word(own + 8 * q, valid, p);
+          } else {
+            acc = ld_ll(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) + 16 * q, flag, w);
+            for (int a = 1; a < na; ++a)
+              fold_vec<DT, OP>(acc, ld_ll(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][a]) + 16 * q, flag, w));
+            fold_vec<DT, OP>(acc, load_word(own + 8 * q, valid, p));
+          }
+          st_ll(dst + 16 * q, acc, flag);
+        }
+      }
+    }
+  }
+  if constexpr (KIND == kAG) {
+    for (int j = 0; j < p.nslots; ++j) {
+      const int origin = (s.R - p.slot_offset[j] + n) % n;
+      const char* slot = slot_ptr(p, s.R, s.c, s.buf, j);
+      for (int64_t q = threadIdx.x; q < nlines; q += B) {
+        const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+        store_word(out + origin * Cb + s.off + 8 * q, ld_ll(slot + 16 * q, flag, w), valid, p);
+      }
+    }
+  } else {
+    for (int64_t q = threadIdx.x; q < nlines; q += B) {
+      const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+      uint2 acc = load_word(snd + s.R * Cb + s.off + 8 * q, valid, p);
+      for (int f = 0; f < p.nfin; ++f)
+        fold_vec<DT, OP>(acc, ld_ll(slot_ptr(p, s.R, s.c, s.buf, p.fin[f]) + 16 * q, flag, w));
+      store_word(out + s.off + 8 * q, acc, valid, p);
+    }
+  }
+}
+
+template <int DT, int OP, int KIND>
+__global__ void __launch_bounds__(1024) pat_kernel(const __grid_constant__ KPlan p) {
+  const int lr = blockIdx.x / p.channels;
+  const int c = blockIdx.x - lr * p.channels;
+  const int R = p.rank[lr];
+  __shared__ uint64_t s_base;
+  if (threadIdx.x == 0) s_base = p.iter_state[lr][c];
+  __syncthreads();
+  const uint64_t base = s_base;
+  Waiter w{p.timeout_ns, p.err, false};
+  uint64_t* myflags = p.flags[R] + c * kFlagWords;
+
+  for (int i = 0; i < p.iters; ++i) {
+    Step s;
+    s.g = base + i;
+    s.off = (static_cast<int64_t>(i) * p.channels + c) * p.slice_bytes;
+    s.len = max(int64_t{0}, min(p.slice_bytes, p.chunk_bytes - s.off));
+    s.R = R;
+    s.lr = lr;
+    s.c = c;
+    s.buf = static_cast<int>(s.g & 1);
+    // credits: a peer's slot buffer (g & 1) is free once it finished step g-2
+    if (s.g >= 2 && threadIdx.x == 0)
+      for (int k = 0; k < p.npeers; ++k) wait_flag(myflags + 8 + (R + p.peers[k]) % p.n, s.g - 1, w);
+    __syncthreads();
+    if (p.proto == kProtoLL) step_ll<DT, OP, KIND>(p, s, w);
+    else step_simple<DT, OP, KIND>(p, s, w);
+    __syncthreads();
+    // done with step g: every rank may re-use buffer (g & 1) of this rank's inbox
+    if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
+      st_release_sys(p.flags[threadIdx.x] + c * kFlagWords + 8 + R, s.g + 1);
+  }
+  if (threadIdx.x == 0) p.iter_state[lr][c] = base + p.iters;
+}
+
+// ------------------------------------------------------------------------- dispatch
+
+using KernelFn = void (*)(const KPlan);
+
+#define PAT_RS_ROW(DT) \
+  { pat_kernel<DT, kSum, kRS>, pat_kernel<DT, kProd, kRS>, pat_kernel<DT, kMax, kRS>, pat_kernel<DT, kMin, kRS> }
+
+static const KernelFn kRsTable[10][4] = {
+    PAT_RS_ROW(kI8), PAT_RS_ROW(kU8), PAT_RS_ROW(kI32), PAT_RS_ROW(kU32), PAT_RS_ROW(kI64),
+    PAT_RS_ROW(kU64), PAT_RS_ROW(kF16), PAT_RS_ROW(kF32), PAT_RS_ROW(kF64), PAT_RS_ROW(kBF16)};
+static const KernelFn kAgKernel = pat_kernel<kU8, kSum, kAG>;
+
+KernelFn kernel_for(int kind, int dtype, int op) {
+  if (kind == kAG) return kAgKernel;
+  return kRsTable[dtype][op];
+}
+
+cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel_for(kind, dtype, op), threads, 0);
+}
+
+cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plan.nlocal * plan.channels);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel_for(plan.kind, dtype, op), plan);
+}
+
+}  // namespace pat

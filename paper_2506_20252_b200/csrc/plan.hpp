@@ -1,0 +1,62 @@
+// plan.hpp — the launch plan shared by the host runtime (comm.cpp) and the sm_100a kernels
+// (kernels.cu). One KPlan is passed by value (__grid_constant__) per kernel launch; it holds
+// the compiled PAT schedule, the slicing, and the pointer table of every rank's inbox pool as
+// seen from the launching device.
+#pragma once
+
+#include <cstdint>
+
+namespace pat {
+
+constexpr int kMaxRanks = 8;    // one NVSwitch box
+constexpr int kMaxRounds = 8;   // >= n-1 (single-tree PAT / ring at n = 8)
+constexpr int kMaxChunks = 8;   // chunk offsets per round
+constexpr int kMaxSlots = 8;    // inbox slots per pipeline step (= n-1 arrivals)
+constexpr int kMaxArr = 8;      // arrivals folded into one forwarded offset
+constexpr int kMaxLocal = 8;    // ranks driven by one kernel (local mode)
+constexpr int kMaxChannels = 64;
+constexpr int kFlagWords = 16;  // per channel: data flag per round [0,8) + done-from per rank [8,16)
+
+enum Proto : int { kProtoLL = 1, kProtoSimple = 2 };
+enum KindK : int { kAG = 0, kRS = 1 };
+
+// One PAT round compiled for the kernel.
+struct KRound {
+  int8_t peer;        // send peer delta, (r + peer) mod n, already in [1, n)
+  int8_t nchunks;
+  int8_t slot_base;   // first inbox slot this round fills at the receiver
+  int8_t pad;
+  int8_t chunk[kMaxChunks];   // offsets k, send order
+  int8_t narr[kMaxChunks];    // AG: 0 = own chunk, 1 = forward of slot arr[pos][0]
+                              // RS: arrivals folded (in round order) before the own contribution
+  int8_t arr[kMaxChunks][kMaxArr];
+};
+
+struct KPlan {
+  int n, nrounds, nslots, nlocal;
+  int kind, proto, vec, esize;
+  int channels, iters;
+  int64_t chunk_bytes;   // bytes of one rank chunk (AG sendcount*esize, RS recvcount*esize)
+  int64_t slice_bytes;   // payload bytes per slot per pipeline step
+  int64_t slot_stride;   // inbox bytes per slot
+  int64_t chan_stride;   // inbox bytes per channel (2 buffers * nslots * slot_stride)
+  uint64_t timeout_ns;
+  KRound rounds[kMaxRounds];
+  int8_t slot_round[kMaxSlots];    // round whose arrival fills slot j
+  int8_t slot_offset[kMaxSlots];   // received offset k' held in slot j
+  int8_t nfin;                     // RS: slots holding offset-0 arrivals, round order
+  int8_t fin[kMaxSlots];
+  int8_t npeers;                   // distinct send peers (credit waits)
+  int8_t peers[kMaxRounds];
+  // ranks driven by this launch
+  int rank[kMaxLocal];
+  const char* send[kMaxLocal];
+  char* recv[kMaxLocal];
+  uint64_t* iter_state[kMaxLocal];  // [kMaxChannels] pipeline-step counters per rank
+  // every rank's pool, mapped into this device's address space
+  char* inbox[kMaxRanks];
+  uint64_t* flags[kMaxRanks];       // [kMaxChannels][kFlagWords]
+  int* err;                         // mapped pinned host word (first async error)
+};
+
+}  // namespace pat

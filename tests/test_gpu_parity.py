@@ -1,0 +1,359 @@
+"""GPU parity: the sm_100a PAT kernels, called through the C ABI, against the CPU oracle and
+against the reference's own outputs (tests/golden/executor.npz).
+
+Bar: bit-exact everywhere (all-gather is a copy; reduce-scatter reproduces the reference's
+PAT fold order with per-hop rounding in the wire dtype, so floats are bit-exact too).
+Ranks that outnumber the GPUs run as logical ranks inside one cooperative kernel per GPU.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2506_20252_b200 import PatComm, PatError, _lib  # noqa: E402
+from paper_2506_20252_b200 import schedule as S  # noqa: E402
+from paper_2506_20252_b200 import simulate as SIM  # noqa: E402
+
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+NP = {O.INT8: np.int8, O.UINT8: np.uint8, O.INT32: np.int32, O.UINT32: np.uint32, O.INT64: np.int64,
+      O.UINT64: np.uint64, O.FLOAT16: np.uint16, O.BFLOAT16: np.uint16, O.FLOAT32: np.float32,
+      O.FLOAT64: np.float64}
+
+_COMMS = {}
+
+
+def comm_for(n, devices=None, **cfg):
+    devices = tuple(devices if devices is not None else [0] * n)
+    key = (n, devices, tuple(sorted(cfg.items())))
+    if key not in _COMMS:
+        _COMMS[key] = PatComm.init_all(n, list(devices), **cfg)
+    return _COMMS[key]
+
+
+def to_dev(a: np.ndarray, dev, pad_front=0):
+    """Byte tensor on `dev` holding `a`, optionally starting `pad_front` bytes into the allocation."""
+    raw = np.ascontiguousarray(a).view(np.uint8)
+    t = torch.zeros(raw.size + pad_front + 64, dtype=torch.uint8, device=dev)
+    t[pad_front:pad_front + raw.size] = torch.from_numpy(raw.copy()).to(dev)
+    return t, t.data_ptr() + pad_front
+
+
+def sync_all(devs):
+    for d in sorted(set(devs)):
+        torch.cuda.synchronize(d)
+
+
+def gpu_allgather(comm, devices, payload, elems, dtype, pad=0, inplace=False, schedule=None):
+    n = len(devices)
+    es = payload.itemsize
+    keep, sptr, rptr = [], [], []
+    for r in range(n):
+        chunk = payload[r * elems:(r + 1) * elems]
+        if inplace:
+            full = np.zeros(n * elems, payload.dtype)
+            full[r * elems:(r + 1) * elems] = chunk
+            t, p = to_dev(full, f"cuda:{devices[r]}", pad)
+            keep.append(t)
+            rptr.append(p)
+            sptr.append(p + r * elems * es)
+        else:
+            ts, ps = to_dev(chunk, f"cuda:{devices[r]}", pad)
+            tr, pr = to_dev(np.zeros(n * elems, payload.dtype), f"cuda:{devices[r]}", pad)
+            keep += [ts, tr]
+            sptr.append(ps)
+            rptr.append(pr)
+    comm.all_gather(sptr, rptr, elems, dtype, schedule=schedule)
+    sync_all(devices)
+    comm.raise_async_error()
+    outs = []
+    for r in range(n):
+        t = keep[r] if inplace else keep[2 * r + 1]
+        b = t.cpu().numpy()[pad:pad + n * elems * es]
+        outs.append(b.view(payload.dtype))
+    return outs
+
+
+def gpu_reduce_scatter(comm, devices, payload, elems, dtype, op, pad=0, schedule=None):
+    n = len(devices)
+    es = payload.itemsize
+    keep, sptr, rptr = [], [], []
+    for r in range(n):
+        ts, ps = to_dev(payload[r * n * elems:(r + 1) * n * elems], f"cuda:{devices[r]}", pad)
+        tr, pr = to_dev(np.zeros(elems, payload.dtype), f"cuda:{devices[r]}", pad)
+        keep += [ts, tr]
+        sptr.append(ps)
+        rptr.append(pr)
+    comm.reduce_scatter(sptr, rptr, elems, dtype, op, schedule=schedule)
+    sync_all(devices)
+    comm.raise_async_error()
+    return [keep[2 * r + 1].cpu().numpy()[pad:pad + elems * es].view(payload.dtype) for r in range(n)]
+
+
+def oracle_ag(n, trees, dtype, payload, elems):
+    out, _ = O.run_allgather(O.pat_allgather(n, trees), dtype, payload, elems)
+    return out
+
+
+def oracle_rs(n, trees, dtype, op, payload, elems):
+    out, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, trees), dtype, op, payload, elems)
+    return out
+
+
+def same(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+# ------------------------------------------------------------------ golden: the reference's own outputs
+
+def test_reference_outputs_bit_exact_via_simulate_api(golden_dir):
+    ex = np.load(os.path.join(golden_dir, "executor.npz"))
+    for key in ex["index"]:
+        n, t, seed, dt = (int(x[1:]) for x in str(key).split("_"))
+        if seed != 0 or n > 8:
+            continue
+        elems = 4
+        p = ex[f"ag_in_{key}"]
+        res = SIM.run_allgather(S.pat_allgather(n, t), SIM.Payload(n, elems, [p[r * elems:(r + 1) * elems] for r in range(n)]))
+        assert same(np.concatenate(res.outputs), ex[f"ag_out_{key}"]), key
+        p = ex[f"rs_in_{key}"]
+        op = SIM.ReduceOp.WrappingIntSum if dt == O.INT64 else SIM.ReduceOp.FloatSum
+        res = SIM.run_reduce_scatter(S.pat_reduce_scatter(n, t),
+                                     SIM.Payload(n, elems, [p[c * elems:(c + 1) * elems] for c in range(n * n)]), op)
+        assert same(np.concatenate(res.outputs), ex[f"rs_out_{key}"]), key  # float64 bit-exact
+        ref_stats = [int(x) for x in ex[f"rs_stats_{key}"][6:]]
+        assert res.stats["occupancy_per_round"] == ref_stats
+
+
+def test_simulate_api_errors():
+    s = S.pat_allgather(4, 2)
+    good = SIM.Payload(4, 2, [np.zeros(2, np.int64) for _ in range(4)])
+    with pytest.raises(PatError) as ei:
+        SIM.run_allgather(s, SIM.Payload(4, 2, good.chunks[:3]))
+    assert ei.value.kind == "PayloadShapeError"
+    with pytest.raises(PatError) as ei:
+        SIM.run_allgather(S.pat_reduce_scatter(4, 2), good)
+    assert ei.value.kind == "SimulationError"
+    bad = S.pat_allgather(4, 2)
+    bad.rounds[0].chunk_offsets = [3]
+    with pytest.raises(PatError) as ei:
+        SIM.run_allgather(bad, good)
+    assert ei.value.kind == "InvalidScheduleError"
+    rs = SIM.Payload(4, 2, [np.zeros(2, np.int64) for _ in range(16)])
+    with pytest.raises(PatError) as ei:
+        SIM.run_reduce_scatter(S.pat_reduce_scatter(4, 2), rs, SIM.ReduceOp.FloatSum)
+    assert ei.value.kind == "UnsupportedOpError"
+
+
+# ------------------------------------------------------------------ local mode (n logical ranks, one GPU)
+
+@pytest.mark.parametrize("n", range(1, 9))
+@pytest.mark.parametrize("elems", [1, 3, 64, 1000, 40000])
+def test_allgather_local_all_trees(n, elems):
+    for t in O.valid_tree_counts(n):
+        comm = comm_for(n, trees=t)
+        p = O.random_payload(O.FLOAT32, n, elems, n * 100 + t)
+        got = gpu_allgather(comm, [0] * n, p, elems, O.FLOAT32)
+        want = oracle_ag(n, t, O.FLOAT32, p, elems)
+        for r in range(n):
+            assert same(got[r], want[r]), (n, t, elems, r)
+
+
+@pytest.mark.parametrize("dt", [O.FLOAT32, O.BFLOAT16, O.FLOAT16, O.INT32, O.INT64, O.FLOAT64, O.UINT8, O.INT8,
+                                O.UINT32, O.UINT64])
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 7, 8])
+def test_reduce_scatter_local_dtypes(dt, n):
+    for elems in (1, 7, 300, 20000):
+        for t in O.valid_tree_counts(n):
+            comm = comm_for(n, trees=t)
+            p = O.random_payload(dt, n * n, elems, 7 * n + t + elems)
+            got = gpu_reduce_scatter(comm, [0] * n, p, elems, dt, O.SUM)
+            want = oracle_rs(n, t, dt, O.SUM, p, elems)
+            for r in range(n):
+                assert same(got[r], want[r]), (dt, n, t, elems, r)
+
+
+@pytest.mark.parametrize("op", [O.MAX, O.MIN, O.PROD])
+@pytest.mark.parametrize("dt", [O.FLOAT32, O.BFLOAT16, O.INT32, O.FLOAT16])
+def test_reduce_scatter_ops(op, dt):
+    for n in (3, 8):
+        comm = comm_for(n)
+        elems = 5000
+        p = O.random_payload(dt, n * n, elems, 11)
+        got = gpu_reduce_scatter(comm, [0] * n, p, elems, dt, op)
+        want = oracle_rs(n, O.max_trees(n), dt, op, p, elems)
+        for r in range(n):
+            assert same(got[r], want[r]), (op, dt, n, r)
+
+
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_SIMPLE])
+def test_protocols_forced(proto):
+    for n in (2, 5, 8):
+        comm = comm_for(n, protocol=proto)
+        for elems in (1, 5, 4096, 70001, 300000):
+            p = O.random_payload(O.FLOAT32, n, elems, elems)
+            got = gpu_allgather(comm, [0] * n, p, elems, O.FLOAT32)
+            want = oracle_ag(n, O.max_trees(n), O.FLOAT32, p, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (proto, n, elems)
+            q = O.random_payload(O.BFLOAT16, n * n, elems, elems + 1)
+            got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.BFLOAT16, O.SUM)
+            want = oracle_rs(n, O.max_trees(n), O.BFLOAT16, O.SUM, q, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (proto, n, elems)
+
+
+def test_misaligned_and_inplace():
+    n = 6
+    comm = comm_for(n)
+    for pad in (2, 4, 8):
+        for elems in (3, 1001, 100003):
+            p = O.random_payload(O.FLOAT16, n, elems, pad)
+            got = gpu_allgather(comm, [0] * n, p, elems, O.FLOAT16, pad=pad)
+            want = oracle_ag(n, O.max_trees(n), O.FLOAT16, p, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (pad, elems)
+            q = O.random_payload(O.FLOAT16, n * n, elems, pad + 1)
+            got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.FLOAT16, O.SUM, pad=pad)
+            want = oracle_rs(n, O.max_trees(n), O.FLOAT16, O.SUM, q, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (pad, elems)
+    for elems in (17, 65536, 300000):
+        p = O.random_payload(O.INT32, n, elems, 3)
+        got = gpu_allgather(comm, [0] * n, p, elems, O.INT32, inplace=True)
+        want = oracle_ag(n, O.max_trees(n), O.INT32, p, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), elems
+
+
+def test_small_slots_many_pipeline_steps():
+    """A tiny staging budget forces many pipeline steps per channel (credit flow control)."""
+    n = 8
+    comm = comm_for(n, staging_bytes=n * 64 * 1024, channels=4)
+    for elems in (1 << 16, 300001):
+        p = O.random_payload(O.INT32, n, elems, 5)
+        got = gpu_allgather(comm, [0] * n, p, elems, O.INT32)
+        want = oracle_ag(n, 4, O.INT32, p, elems)
+        assert all(same(got[r], want[r]) for r in range(n))
+        q = O.random_payload(O.FLOAT32, n * n, elems, 6)
+        got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.FLOAT32, O.SUM)
+        want = oracle_rs(n, 4, O.FLOAT32, O.SUM, q, elems)
+        assert all(same(got[r], want[r]) for r in range(n))
+    plan = comm.plan(1, 300001, O.FLOAT32)
+    assert plan["iterations"] > 1 and plan["channels"] == 4
+
+
+def test_back_to_back_calls_mixed_sizes():
+    """Iteration counters and credits persist across calls of different sizes and kinds."""
+    n = 8
+    comm = comm_for(n)
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(0)
+    sizes = [int(x) for x in rng.integers(1, 200000, 40)]
+    bufs = []
+    for i, elems in enumerate(sizes):
+        if i % 2 == 0:
+            p = O.random_payload(O.FLOAT32, n, elems, i)
+            s = [torch.from_numpy(p[r * elems:(r + 1) * elems].copy()).to(dev) for r in range(n)]
+            o = [torch.empty(n * elems, dtype=torch.float32, device=dev) for _ in range(n)]
+            comm.all_gather(s, o, elems, O.FLOAT32)
+            bufs.append(("ag", elems, p, o, s))
+        else:
+            p = O.random_payload(O.INT32, n * n, elems, i)
+            s = [torch.from_numpy(p[r * n * elems:(r + 1) * n * elems].copy()).to(dev) for r in range(n)]
+            o = [torch.empty(elems, dtype=torch.int32, device=dev) for _ in range(n)]
+            comm.reduce_scatter(s, o, elems, O.INT32, O.SUM)
+            bufs.append(("rs", elems, p, o, s))
+    torch.cuda.synchronize()
+    comm.raise_async_error()
+    for kind, elems, p, o, _ in bufs:
+        if kind == "ag":
+            want = oracle_ag(n, 4, O.FLOAT32, p, elems)
+        else:
+            want = oracle_rs(n, 4, O.INT32, O.SUM, p, elems)
+        for r in range(n):
+            assert same(o[r].cpu().numpy(), want[r]), (kind, elems, r)
+
+
+def test_explicit_schedules_generic_executor():
+    """Ring / Bruck / single-tree PAT through patAllGatherSchedule / patReduceScatterSchedule."""
+    for n in (3, 5, 8):
+        comm = comm_for(n)
+        elems = 3000
+        for ag in (S.ring_allgather(n), S.bruck_nearest(n), S.bruck_farthest(n), S.pat_allgather(n, 1)):
+            p = O.random_payload(O.FLOAT32, n, elems, 9)
+            got = gpu_allgather(comm, [0] * n, p, elems, O.FLOAT32, schedule=ag)
+            want, _ = O.run_allgather(ag.encode(), O.FLOAT32, p, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (n, ag.algorithm)
+            rs = S.mirror_schedule(ag)
+            q = O.random_payload(O.FLOAT32, n * n, elems, 10)
+            got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.FLOAT32, O.SUM, schedule=rs)
+            want, _ = O.run_reduce_scatter(rs.encode(), O.FLOAT32, O.SUM, q, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (n, rs.algorithm)
+
+
+def test_large_property_checks():
+    """Full-size properties: AG output = concatenation; RS int32 = column
+    sums mod 2^32; RS fp32 sampled columns = closed-form PAT tree."""
+    n = 8
+    comm = comm_for(n)
+    dev = torch.device("cuda:0")
+    elems = 8 << 20  # 32 MiB fp32 per rank
+    g = torch.Generator(device=dev).manual_seed(0)
+    sends = [torch.randint(-2**31, 2**31 - 1, (elems,), dtype=torch.int32, device=dev, generator=g) for _ in range(n)]
+    outs = [torch.empty(n * elems, dtype=torch.int32, device=dev) for _ in range(n)]
+    comm.all_gather(sends, outs, elems, O.INT32)
+    torch.cuda.synchronize()
+    cat = torch.cat(sends)
+    for r in range(n):
+        assert torch.equal(outs[r], cat)
+    del outs, cat
+    rs_elems = 2 << 20
+    rs_send = [torch.randint(-2**31, 2**31 - 1, (n * rs_elems,), dtype=torch.int32, device=dev, generator=g)
+               for _ in range(n)]
+    rs_out = [torch.empty(rs_elems, dtype=torch.int32, device=dev) for _ in range(n)]
+    comm.reduce_scatter(rs_send, rs_out, rs_elems, O.INT32, O.SUM)
+    torch.cuda.synchronize()
+    stack = torch.stack(rs_send).view(n, n, rs_elems).to(torch.int64)
+    for r in range(n):
+        want = stack[:, r, :].sum(0)
+        want = ((want + 2**31) % 2**32 - 2**31).to(torch.int32)
+        assert torch.equal(rs_out[r], want)
+    f_send = [torch.rand(n * rs_elems, device=dev, generator=g) for _ in range(n)]
+    f_out = [torch.empty(rs_elems, device=dev) for _ in range(n)]
+    comm.reduce_scatter(f_send, f_out, rs_elems, O.FLOAT32, O.SUM)
+    torch.cuda.synchronize()
+    fs = torch.stack(f_send).view(n, n, rs_elems).cpu().numpy()
+    cols = np.random.default_rng(1).integers(0, rs_elems, 64)
+    for r in range(n):
+        o = f_out[r].cpu().numpy()
+        for e in cols:
+            col = np.array([fs[(r + j) % n, r, e] for j in range(n)], np.float32)
+            assert O.tree_fold(n, O.FLOAT32, O.SUM, col) == o[e]
+
+
+# ------------------------------------------------------------------ multiple GPUs (NVLink peers)
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 7, 8])
+def test_multi_gpu_parity(n):
+    devices = [r % NGPU for r in range(n)]
+    if n <= NGPU:
+        devices = list(range(n))
+    comm = comm_for(n, devices)
+    for elems in (1, 999, 65536, 1 << 20):
+        p = O.random_payload(O.FLOAT32, n, elems, elems)
+        got = gpu_allgather(comm, devices, p, elems, O.FLOAT32)
+        want = oracle_ag(n, O.max_trees(n), O.FLOAT32, p, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (n, elems)
+        for dt in (O.INT32, O.BFLOAT16):
+            q = O.random_payload(dt, n * n, elems, elems + 3)
+            got = gpu_reduce_scatter(comm, devices, q, elems, dt, O.SUM)
+            want = oracle_rs(n, O.max_trees(n), dt, O.SUM, q, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (n, elems, dt)
+
+
+def test_no_async_error_left():
+    for c in _COMMS.values():
+        assert c.async_error() == 0
