@@ -1,0 +1,406 @@
+"""Benchmark of the PAT hot path: one step = one PAT all-gather + one PAT reduce-scatter(sum).
+
+Workload (BASELINE.json configs[0]): 1 MiB fp32 per rank (262,144 elements), all-gather of
+one chunk per rank and reduce-scatter of n chunks per rank into one.
+  * N = 1 (plain `python bench.py`): n = 8 logical ranks on cuda:0, one cooperative kernel
+    per collective ("local mode"; every rank's data in one GPU's HBM -> HBM roofline).
+  * N > 1 (torchrun, one process per GPU): n = N ranks over NVLink, inbox pools mapped with
+    CUDA IPC. NCCL's Ring all-gather / reduce-scatter is timed on the same buffers as a
+    comparison (`nccl_ring`).
+
+metric: aggregate bus bandwidth of the step = 2 * n * (n-1) * C bytes / step time (GB/s);
+every rank receives (n-1)*C per collective (test_simulate.cpp:101-111). Per-collective
+latencies are reported beside it.
+
+`--impl reference` times the reference's own CPU executor (oracle/_ref, compiled from
+/root/reference/proj/src) on the host cores on the same n and C (int64 all-gather + float64
+reduce-scatter: equal bytes), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CHUNK_BYTES = 1 << 20  # 1 MiB per rank
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+NVLINK_MEASURED_GBS = 770.0  # peer copy per direction (B200_PROFILING.md)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="pat", choices=["pat", "reference"])
+    ap.add_argument("--chunk-bytes", type=int, default=CHUNK_BYTES)
+    ap.add_argument("--ranks", type=int, default=0, help="logical ranks at N=1 (default 8)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1:
+        return int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ.get("LOCAL_RANK", 0))
+    return 0, 1, 0
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------ reference CPU path
+
+def reference_time(n: int, chunk_bytes: int, seconds: float, mode: int = 1):
+    """The reference executor (oracle/_ref) on the host: run_allgather(int64) +
+    run_reduce_scatter(float64, FloatSum) with equal bytes per chunk. Returns
+    (seconds per step, steps, threads)."""
+    import ctypes
+
+    import numpy as np
+
+    import oracle as O
+
+    R = O.ref()
+    elems = chunk_bytes // 8
+    ag = O.pat_allgather(n, O.max_trees(n))
+    rs = O.pat_reduce_scatter(n, O.max_trees(n))
+    pin = np.zeros(n * elems, np.int64)
+    R.ref_random_payload(0, O.INT64, n, elems, 0, pin.ctypes.data)
+    pout = np.zeros(n * n * elems, np.int64)
+    qin = np.zeros(n * n * elems, np.float64)
+    R.ref_random_payload(1, O.FLOAT64, n, elems, 0, qin.ctypes.data)
+    qout = np.zeros(n * elems, np.float64)
+    threads = os.cpu_count() or 1
+    st = np.zeros(600, np.int64)
+
+    def one():
+        rc = R.ref_run_allgather(ag.ctypes.data_as(O.I32P), len(ag), O.INT64, elems, pin.ctypes.data,
+                                 pout.ctypes.data, st.ctypes.data_as(O.I64P), mode, threads)
+        rc |= R.ref_run_reduce_scatter(rs.ctypes.data_as(O.I32P), len(rs), O.FLOAT64, elems, qin.ctypes.data,
+                                       qout.ctypes.data, st.ctypes.data_as(O.I64P), mode, threads)
+        assert rc == 0
+
+    one()  # warm-up
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        one()
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or steps >= 10000:
+            break
+    return el / steps, steps, threads if mode else 1
+
+
+def busbw_gbs(n: int, chunk_bytes: int, seconds: float) -> float:
+    return 2.0 * n * (n - 1) * chunk_bytes / seconds / 1e9
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons every ~5 ms on one GPU."""
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ PAT arm
+
+def run_pat(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_20252_b200 import FLOAT32, SUM, PatComm
+
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    C = args.chunk_bytes
+    elems = C // 4
+    if world > 1:
+        os.environ.setdefault("NCCL_ALGO", "Ring")  # affects only the NCCL comparison below
+        dist.init_process_group("nccl", device_id=dev)
+        n = world
+        comm = PatComm.from_process_group(device=local)
+        ranks_here = [rank]
+        placement = f"{n} ranks on {n} GPUs (1 process per GPU, CUDA IPC pools)"
+    else:
+        n = args.ranks or 8
+        comm = PatComm.init_all(n, [local] * n)
+        ranks_here = list(range(n))
+        placement = f"{n} logical ranks on 1 GPU (one cooperative kernel per collective)"
+    L = len(ranks_here)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    ag_send = [torch.rand(elems, device=dev, generator=g) for _ in range(L)]
+    ag_recv = [torch.empty(n * elems, device=dev) for _ in range(L)]
+    rs_send = [torch.rand(n * elems, device=dev, generator=g) for _ in range(L)]
+    rs_recv = [torch.empty(elems, device=dev) for _ in range(L)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        comm.all_gather(ag_send, ag_recv, elems, FLOAT32)
+        comm.reduce_scatter(rs_send, rs_recv, elems, FLOAT32, SUM)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    comm.raise_async_error()
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        for k in range(K):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[k][0].record(stream)
+            comm.all_gather(ag_send, ag_recv, elems, FLOAT32)
+            ev[k][1].record(stream)
+            comm.reduce_scatter(rs_send, rs_recv, elems, FLOAT32, SUM)
+            ev[k][2].record(stream)
+        barrier()
+    comm.raise_async_error()
+    ag_ms = sum(e[0].elapsed_time(e[1]) for e in ev)
+    rs_ms = sum(e[1].elapsed_time(e[2]) for e in ev)
+    tot = torch.tensor([ag_ms + rs_ms, ag_ms, rs_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    tot_ms, ag_ms, rs_ms = (float(x) for x in tot.tolist())
+    ms_per_step = tot_ms / K
+    value = busbw_gbs(n, C, ms_per_step / 1e3)
+
+    # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region
+    h_ag_send = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(L)]
+    h_rs_send = [torch.empty(n * elems, dtype=torch.float32).pin_memory() for _ in range(L)]
+    h_ag_recv = [torch.empty(n * elems, dtype=torch.float32).pin_memory() for _ in range(L)]
+    h_rs_recv = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(L)]
+    for i in range(L):
+        h_ag_send[i].copy_(ag_send[i].cpu())
+        h_rs_send[i].copy_(rs_send[i].cpu())
+    E = max(3, min(K, 20))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(E):
+        for i in range(L):
+            ag_send[i].copy_(h_ag_send[i], non_blocking=True)
+            rs_send[i].copy_(h_rs_send[i], non_blocking=True)
+        step()
+        for i in range(L):
+            h_ag_recv[i].copy_(ag_recv[i], non_blocking=True)
+            h_rs_recv[i].copy_(rs_recv[i], non_blocking=True)
+    e1.record(stream)
+    barrier()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / E], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+    h2d = L * (elems + n * elems) * 4
+    d2h = L * (n * elems + elems) * 4
+
+    # ---- NCCL Ring comparison (N > 1)
+    nccl = None
+    if world > 1 and not args.no_nccl:
+        agt = torch.empty(n * elems, device=dev)
+        rst = torch.empty(elems, device=dev)
+        for _ in range(args.warmup):
+            dist.all_gather_into_tensor(agt, ag_send[0])
+            dist.reduce_scatter_tensor(rst, rs_send[0])
+        barrier()
+        nev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+        for k in range(K):
+            flush.zero_()
+            nev[k][0].record(stream)
+            dist.all_gather_into_tensor(agt, ag_send[0])
+            nev[k][1].record(stream)
+            dist.reduce_scatter_tensor(rst, rs_send[0])
+            nev[k][2].record(stream)
+        barrier()
+        nt = torch.tensor([sum(e[0].elapsed_time(e[2]) for e in nev), sum(e[0].elapsed_time(e[1]) for e in nev),
+                           sum(e[1].elapsed_time(e[2]) for e in nev)], dtype=torch.float64, device=dev)
+        dist.all_reduce(nt, op=dist.ReduceOp.MAX)
+        nt = nt.tolist()
+        nccl = {"algo": os.environ.get("NCCL_ALGO"), "ms_per_step": nt[0] / K,
+                "busbw_gbs": busbw_gbs(n, C, nt[0] / K / 1e3),
+                "ag_us": 1e3 * nt[1] / K, "rs_us": 1e3 * nt[2] / K,
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
+
+    # ---- roofline of the dominant kernel
+    peaks, peak_src = load_peaks()
+    dom = "reduce_scatter" if rs_ms >= ag_ms else "all_gather"
+    dom_us = 1e3 * max(ag_ms, rs_ms) / K
+    if world == 1:
+        algo_bytes = (n * n + n) * C  # local mode: read n*C + write n^2*C (AG) / read n^2*C + write n*C (RS)
+        peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+        roof = {"bound": "hbm", "kernel": f"pat_kernel ({dom})", "unit": "GB/s",
+                "algorithmic_bytes_per_launch": algo_bytes, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        algo_bytes = (n - 1) * C  # per rank, received over NVLink
+        peak = NVLINK_MEASURED_GBS
+        roof = {"bound": "nvlink", "kernel": f"pat_kernel ({dom})", "unit": "GB/s",
+                "algorithmic_bytes_per_launch": algo_bytes,
+                "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"}
+    achieved = algo_bytes / (dom_us * 1e-6) / 1e9
+    roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
+                 "launch_us": dom_us})
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tr = json.load(open(tpath))
+            key = f"{'local' if world == 1 else 'nvlink'}_n{n}_{dom}"
+            if key in tr:
+                roof["traffic"] = tr[key]["dram_bytes_per_launch"]
+                roof["traffic_source"] = tr[key].get("source")
+        except Exception:
+            pass
+
+    clk = clocks.summary()
+    if world > 1:
+        allc = [None] * world
+        dist.all_gather_object(allc, clk)
+        clk = {"sm_mhz": statistics.median([c["sm_mhz"] for c in allc if c["sm_mhz"]] or [0]),
+               "sm_max_mhz": allc[0]["sm_max_mhz"], "reasons": sorted({r for c in allc for r in c["reasons"]}),
+               "samples": sum(c["samples"] for c in allc)}
+
+    plan_ag = comm.plan(0, elems, FLOAT32)
+    plan_rs = comm.plan(1, elems, FLOAT32)
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                sec, steps, thr = reference_time(n, C, args.cpu_seconds)
+                cpu = {"value": busbw_gbs(n, C, sec), "unit": "GB/s", "cores": thr, "kind": "reference",
+                       "ms_per_step": sec * 1e3,
+                       "sample": f"{steps} steps of the reference executor (oracle/_ref = /root/reference/proj/src "
+                                 f"compiled), n={n}, {C} B/rank, run_allgather(int64)+run_reduce_scatter(f64), "
+                                 f"ExecMode::Parallel x{thr} threads, {args.cpu_seconds:.0f} s budget"}
+            except Exception as e:  # the reference library must be built in-tree
+                cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+        out = {
+            "metric": "PAT all-gather + reduce-scatter(sum) aggregate bus bandwidth, 1 MiB fp32 per rank",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.rand on device)",
+            "config": {"workload": "BASELINE configs[0]: PAT AG + RS(sum), 1 MiB fp32 per rank",
+                       "nranks": n, "placement": placement, "chunk_bytes": C, "trees": plan_ag["trees"],
+                       "rounds": plan_ag["rounds"], "l2": "flushed (256 MiB write) before every timed step",
+                       "plan_allgather": plan_ag, "plan_reduce_scatter": plan_rs},
+            "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K},
+            "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host"},
+            "gpu_launches": 2 * K,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        if nccl:
+            out["nccl_ring"] = nccl
+    comm.destroy()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    n = world if world > 1 else (args.ranks or 8)
+    C = args.chunk_bytes
+    per = []
+    for _ in range(args.warmup):
+        reference_time(n, C, 0.0)
+    budget = max(1.0, min(args.cpu_seconds, 60.0))
+    sec, steps, thr = reference_time(n, C, budget)
+    value = busbw_gbs(n, C, sec)
+    del per
+    return {"impl": "reference", "metric": "PAT all-gather + reduce-scatter(sum) aggregate bus bandwidth, 1 MiB fp32 per rank",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int64 AG + f64 RS (equal bytes)", "data": "synthetic (reference mt19937_64 payloads)",
+            "config": {"workload": "BASELINE configs[0]: PAT AG + RS(sum), 1 MiB per rank", "nranks": n,
+                       "chunk_bytes": C, "placement": "in-process ranks on host cores"},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": thr, "kind": "reference",
+                             "sample": f"{steps} steps, ExecMode::Parallel x{thr} threads, ~{budget:.0f} s"},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        out = run_pat(args, rank, world, local)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

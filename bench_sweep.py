@@ -1,0 +1,136 @@
+"""Size sweeps of PAT all-gather / reduce-scatter against NCCL Ring (BASELINE configs 2-5).
+
+Run under torchrun, one process per GPU (N >= 2), or plain (N = 1: logical ranks in local mode):
+
+  torchrun --nproc-per-node 4 --master-addr 127.0.0.1 bench_sweep.py --out gpurun_out/sweep4.json
+
+Every point: W warm-up calls, then K calls timed with CUDA events per call (median), the max
+over ranks. Latency points (<= 1 MiB) are back-to-back calls without an L2 flush (the
+nccl-tests convention); bandwidth points (>= 1 MiB) flush L2 before every call.
+Writes one JSON object per line: {"coll", "impl", "n", "dtype", "bytes_per_rank", "us", "busbw_gbs"}.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/sweep.json")
+    ap.add_argument("--min-bytes", type=int, default=8)
+    ap.add_argument("--max-bytes", type=int, default=1 << 30)
+    ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--dtypes", default="f32,bf16")
+    ap.add_argument("--colls", default="ag,rs")
+    ap.add_argument("--ranks", type=int, default=8, help="logical ranks when run without torchrun")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--protocol", type=int, default=0)
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_20252_b200 import BFLOAT16, FLOAT32, SUM, PatComm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    cfg = {"protocol": args.protocol} if args.protocol else {}
+    if world > 1:
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        dist.init_process_group("nccl", device_id=dev)
+        n = world
+        comm = PatComm.from_process_group(device=local, **cfg)
+        L = 1
+    else:
+        n = args.ranks
+        comm = PatComm.init_all(n, [local] * n, **cfg)
+        L = n
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    dts = {"f32": (torch.float32, FLOAT32), "bf16": (torch.bfloat16, BFLOAT16)}
+    out = open(args.out, "w") if rank == 0 else None
+
+    def timed(fn, big):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
+        for a, b in evs:
+            if big:
+                flush.zero_()
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        ts = sorted(a.elapsed_time(b) for a, b in evs)
+        med = torch.tensor([ts[len(ts) // 2] * 1e3], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(med, op=dist.ReduceOp.MAX)
+        return float(med.item())
+
+    sizes = []
+    b = args.min_bytes
+    while b <= args.max_bytes:
+        sizes.append(b)
+        b *= 2
+    for dname in args.dtypes.split(","):
+        tdt, pdt = dts[dname]
+        es = torch.empty(0, dtype=tdt).element_size()
+        for C in sizes:
+            elems = max(1, C // es)
+            need = (n + 1) * elems * es * L * 2
+            if need > 40 * (1 << 30):
+                break
+            big = C >= (1 << 20)
+            for coll in args.colls.split(","):
+                if coll == "ag":
+                    s = [torch.ones(elems, dtype=tdt, device=dev) for _ in range(L)]
+                    r = [torch.empty(n * elems, dtype=tdt, device=dev) for _ in range(L)]
+                    fn = lambda: comm.all_gather(s, r, elems, pdt)
+                else:
+                    s = [torch.ones(n * elems, dtype=tdt, device=dev) for _ in range(L)]
+                    r = [torch.empty(elems, dtype=tdt, device=dev) for _ in range(L)]
+                    fn = lambda: comm.reduce_scatter(s, r, elems, pdt, SUM)
+                us = timed(fn, big)
+                rec = {"coll": coll, "impl": "pat", "n": n, "gpus": world, "dtype": dname,
+                       "bytes_per_rank": elems * es, "us": us,
+                       "busbw_gbs": (n - 1) * elems * es / (us * 1e-6) / 1e9,
+                       "plan": comm.plan(0 if coll == "ag" else 1, elems, pdt)}
+                if out:
+                    out.write(json.dumps(rec) + "\n")
+                    out.flush()
+                if world > 1 and not args.no_nccl:
+                    if coll == "ag":
+                        nfn = lambda: dist.all_gather_into_tensor(r[0], s[0])
+                    else:
+                        nfn = lambda: dist.reduce_scatter_tensor(r[0], s[0])
+                    us = timed(nfn, big)
+                    rec = {"coll": coll, "impl": "nccl-" + os.environ.get("NCCL_ALGO", "auto"), "n": n,
+                           "gpus": world, "dtype": dname, "bytes_per_rank": elems * es, "us": us,
+                           "busbw_gbs": (n - 1) * elems * es / (us * 1e-6) / 1e9}
+                    if out:
+                        out.write(json.dumps(rec) + "\n")
+                        out.flush()
+                del s, r
+        torch.cuda.empty_cache()
+    comm.raise_async_error()
+    comm.destroy()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

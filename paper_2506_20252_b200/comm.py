@@ -64,6 +64,20 @@ def _dtype(dtype, sample) -> int:
     return int(dtype)
 
 
+def make_exchange(group=None) -> Callable[[bytes], list]:
+    """All-gather of the per-rank init handles over a torch.distributed group (any backend)."""
+    import torch.distributed as dist
+
+    def exchange(mine: bytes) -> list:
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, bytes(mine), group=group)
+        if any(not isinstance(x, (bytes, bytearray)) or len(x) != _lib.HANDLE_BYTES for x in out):
+            raise PatError(4, "handle exchange returned a malformed list")
+        return [bytes(x) for x in out]
+
+    return exchange
+
+
 class PatComm:
     def __init__(self, handle: ctypes.c_void_p):
         self._h = handle
@@ -112,13 +126,7 @@ class PatComm:
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         if device is None:
             device = torch.cuda.current_device()
-
-        def exchange(mine: bytes) -> list:
-            out = [None] * world
-            dist.all_gather_object(out, mine, group=group)
-            return out
-
-        return cls.init_rank(world, rank, device, exchange, **config)
+        return cls.init_rank(world, rank, device, make_exchange(group), **config)
 
     def destroy(self) -> None:
         if self._h:

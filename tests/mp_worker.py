@@ -1,0 +1,73 @@
+"""Worker for tests/test_gpu_multiprocess.py: one process per GPU (torchrun), inbox pools
+mapped with CUDA IPC; every rank checks its own output bit-exact against the CPU oracle."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle as O  # noqa: E402
+from paper_2506_20252_b200 import PatComm  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    n = world
+    fails = 0
+    for proto in (0, 1, 2):
+        comm = PatComm.from_process_group(device=local, protocol=proto)
+        for trees in O.valid_tree_counts(n):
+            for elems in (1, 37, 4096, 65537, 1 << 20):
+                for dt in (O.FLOAT32, O.BFLOAT16, O.INT32):
+                    if proto and elems == 1 << 20 and dt != O.FLOAT32:
+                        continue
+                    seed = 1000 * trees + elems + dt
+                    p = O.random_payload(dt, n, elems, seed)
+                    mine = p[rank * elems:(rank + 1) * elems].copy()
+                    npdt = mine.dtype
+                    s = torch.from_numpy(mine.view(np.uint8)).to(dev)
+                    r = torch.zeros(n * elems * mine.itemsize, dtype=torch.uint8, device=dev)
+                    sched = None
+                    if trees != O.max_trees(n):
+                        from paper_2506_20252_b200 import schedule as S
+                        sched = S.pat_allgather(n, trees)
+                    comm.all_gather([s], [r], elems, dt, schedule=sched)
+                    torch.cuda.synchronize(dev)
+                    want, _ = O.run_allgather(O.pat_allgather(n, trees), dt, p, elems)
+                    got = r.cpu().numpy().view(npdt)
+                    if got.tobytes() != want[rank].tobytes():
+                        fails += 1
+                        print(f"rank {rank} AG mismatch proto={proto} T={trees} elems={elems} dt={dt}", flush=True)
+                    q = O.random_payload(dt, n * n, elems, seed + 1)
+                    s = torch.from_numpy(q[rank * n * elems:(rank + 1) * n * elems].copy().view(np.uint8)).to(dev)
+                    r = torch.zeros(elems * mine.itemsize, dtype=torch.uint8, device=dev)
+                    if sched is not None:
+                        from paper_2506_20252_b200 import schedule as S
+                        sched = S.pat_reduce_scatter(n, trees)
+                    comm.reduce_scatter([s], [r], elems, dt, O.SUM, schedule=sched)
+                    torch.cuda.synchronize(dev)
+                    want, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, trees), dt, O.SUM, q, elems)
+                    got = r.cpu().numpy().view(npdt)
+                    if got.tobytes() != want[rank].tobytes():
+                        fails += 1
+                        print(f"rank {rank} RS mismatch proto={proto} T={trees} elems={elems} dt={dt}", flush=True)
+        comm.raise_async_error()
+        comm.destroy()
+    t = torch.tensor([fails], device=dev)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(f"MP_RESULT fails={int(t.item())} world={world}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
