@@ -105,6 +105,11 @@ typedef struct {
   int protocol;             /* patProtocol_t */
   int timeout_ms;           /* device-side spin timeout; 0 = default 20000 */
   int threads;              /* threads per CTA; 0 = default */
+  int depth;                /* inbox buffers per channel (pipeline depth); 0 = default 2 */
+  int direct;               /* all-gather zero-copy push into peers' recvbufs: -1 off, 0 auto, 1 on.
+                               auto = single-process communicator whose recvbufs are reachable
+                               (same device, or cudaMalloc memory with peer access) */
+  int send_warps;           /* SIMPLE: warps per CTA that push (rest deliver); 0 = half */
 } patConfig_t;
 
 /* Plan the library would launch for one call (introspection / benchmarks). */

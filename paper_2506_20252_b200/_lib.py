@@ -53,6 +53,9 @@ class Config(ctypes.Structure):
         ("protocol", ctypes.c_int),
         ("timeout_ms", ctypes.c_int),
         ("threads", ctypes.c_int),
+        ("depth", ctypes.c_int),
+        ("direct", ctypes.c_int),
+        ("send_warps", ctypes.c_int),
     ]
 
 

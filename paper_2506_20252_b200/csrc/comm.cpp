@@ -116,6 +116,25 @@ struct DeviceGuard {
 
 patResult_t to_result(Err e) { return static_cast<patResult_t>(e); }
 
+// cudaMalloc (legacy) allocations are reachable from every peer-enabled device; VMM /
+// stream-ordered pool memory is not, so zero-copy is only auto-enabled for the former.
+bool legacy_ipc_capable(const void* ptr) {
+  using Fn = int (*)(void*, int, unsigned long long);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<Fn>(nullptr);
+    return reinterpret_cast<Fn>(f);
+  }();
+  if (!fn) return false;
+  int v = 0;
+  constexpr int kIsLegacyIpcCapable = 10;  // CU_POINTER_ATTRIBUTE_IS_LEGACY_CUDA_IPC_CAPABLE
+  if (fn(&v, kIsLegacyIpcCapable, reinterpret_cast<unsigned long long>(ptr)) != 0) return false;
+  return v != 0;
+}
+
 size_t dtype_size(int dt) {
   switch (dt) {
     case patInt8: case patUint8: return 1;
@@ -136,10 +155,15 @@ void fill_defaults(patConfig_t* c, int n) {
   if (c->timeout_ms <= 0) c->timeout_ms = env_int("PAT_TIMEOUT_MS", &v) ? (int)v : kDefaultTimeoutMs;
   if (c->protocol == patProtoAuto && env_int("PAT_PROTOCOL", &v)) c->protocol = (int)v;
   if (c->threads <= 0) c->threads = env_int("PAT_THREADS", &v) ? (int)v : 512;
-  c->threads = std::min(std::max(c->threads / 32 * 32, 32), 1024);
+  c->threads = std::min(std::max(c->threads / 32 * 32, 64), 1024);
+  if (c->depth <= 0) c->depth = env_int("PAT_DEPTH", &v) ? (int)v : 2;
+  c->depth = std::min(std::max(c->depth, 1), 16);
+  if (c->direct == 0 && env_int("PAT_DIRECT", &v)) c->direct = (int)v;
+  if (c->send_warps <= 0) c->send_warps = env_int("PAT_SEND_WARPS", &v) ? (int)v : c->threads / 64;
+  c->send_warps = std::min(std::max(c->send_warps, 1), c->threads / 32 - 1);
   if (c->staging_bytes != 0) {
     // staging budget -> slot size: channels * 2 buffers * (n-1) slots
-    const size_t slots = static_cast<size_t>(c->max_channels) * 2 * std::max(n - 1, 1);
+    const size_t slots = static_cast<size_t>(c->max_channels) * c->depth * std::max(n - 1, 1);
     size_t s = (c->staging_bytes / slots) & ~size_t(15);
     if (s < 256) s = 256;
     c->slice_bytes = s;
@@ -279,7 +303,7 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   comm->channels = c.max_channels;
   comm->slot_bytes = c.slice_bytes;
   const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
-  comm->pool_bytes = kFlagBytes + static_cast<size_t>(comm->channels) * 2 * slots * comm->slot_bytes;
+  comm->pool_bytes = kFlagBytes + static_cast<size_t>(comm->channels) * c.depth * slots * comm->slot_bytes;
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&comm->err_host), sizeof(int),
                          cudaHostAllocMapped | cudaHostAllocPortable));
   *comm->err_host = 0;
@@ -352,6 +376,16 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   }
   vec = aligned16 ? 16 : (aligned8 ? 8 : 0);
   if (sl.proto == kProtoSimple && vec == 8) vec = 0;  // SIMPLE vectors are 16 bytes
+  // one device holds every rank: .gpu-scope flags; zero-copy all-gather is always safe
+  const bool single_device = !comm->multiprocess && comm->groups.size() == 1;
+  bool direct = false;
+  if (kind == kAG && sl.proto == kProtoSimple && !comm->multiprocess && comm->cfg.direct >= 0) {
+    direct = single_device || comm->cfg.direct > 0;
+    if (!direct) {  // auto: cudaMalloc'd recvbufs are reachable through the enabled peer access
+      direct = true;
+      for (size_t l = 0; l < comm->lranks.size() && direct; ++l) direct = legacy_ipc_capable(recvbuffs[l]);
+    }
+  }
   DeviceGuard guard;
   for (DevGroup& g : comm->groups) {
     KPlan p = cp->proto;
@@ -364,7 +398,13 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.chunk_bytes = chunk_bytes;
     p.slice_bytes = sl.slice;
     p.slot_stride = static_cast<int64_t>(comm->slot_bytes);
-    p.chan_stride = 2 * static_cast<int64_t>(std::max(n - 1, 1)) * p.slot_stride;
+    p.depth = comm->cfg.depth;
+    p.chan_stride = static_cast<int64_t>(p.depth) * std::max(n - 1, 1) * p.slot_stride;
+    p.send_warps = comm->cfg.send_warps;
+    p.gpu_scope = single_device ? 1 : 0;
+    p.direct = direct ? 1 : 0;
+    if (direct)
+      for (size_t l = 0; l < comm->lranks.size(); ++l) p.peer_recv[comm->lranks[l]] = static_cast<char*>(recvbuffs[l]);
     p.timeout_ns = static_cast<uint64_t>(comm->cfg.timeout_ms) * 1000000ull;
     p.err = comm->err_dev;
     for (int r = 0; r < n; ++r) {
@@ -626,7 +666,7 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   info->launches = static_cast<int>(comm->groups.size());
   info->slots_per_step = cp->proto.nslots;
   info->slice_bytes = static_cast<size_t>(sl.slice);
-  info->pool_bytes = static_cast<size_t>(sl.channels) * 2 * cp->proto.nslots * comm->slot_bytes + kFlagBytes;
+  info->pool_bytes = static_cast<size_t>(sl.channels) * comm->cfg.depth * cp->proto.nslots * comm->slot_bytes + kFlagBytes;
   info->bytes_sent_per_rank = static_cast<int64_t>(comm->n - 1) * cb;
   info->peak_intermediate_slots = cp->peak_slots;
   return patSuccess;

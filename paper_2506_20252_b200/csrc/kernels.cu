@@ -12,11 +12,16 @@
 //  * LL (small messages): 16-byte lines {data32, flag, data32, flag} stored with one
 //    st.volatile.v4 into the peer's inbox; the receiver polls the line itself, so data and
 //    signal travel together and no fence or separate flag is needed. 50% wire efficiency.
-//  * SIMPLE (bulk): 16-byte vector stores of the slice, fence.sc.sys per thread, CTA barrier,
-//    then one st.relaxed.sys flag word per (channel, round) at the receiver.
-// Inbox slots are double-buffered by step parity; a rank re-uses a peer's slot buffer only
-// after that peer published "done with step g-2" (credit flags), so the pool is bounded:
-// channels * 2 * (n-1) slots per rank, independent of the message size.
+//    Every thread owns the same words of every chunk in every round: no CTA barriers.
+//  * SIMPLE (bulk): warp-specialised. Sender warps push 16-byte vectors of the slice into the
+//    peer (inbox slot, or the peer's recvbuf directly in direct all-gather mode), then one
+//    thread issues fence.acq_rel + st.relaxed of the (channel, round) flag at the receiver
+//    (NCCL-style: named barrier, then a single release). Receiver warps wait for the flags
+//    and deliver (all-gather) or fold the output (reduce-scatter), so step g+1's pushes
+//    overlap step g's delivery.
+// Inbox slots are `depth`-buffered by step; a rank re-uses a peer's slot buffer only after
+// that peer published "done with step g-depth" (credit flags), so the pool is bounded:
+// channels * depth * (n-1) slots per rank, independent of the message size.
 //
 // Reduction order (reduce-scatter) is the reference's exactly: a forwarded offset carries
 // fold(arrivals in round order) (+) own contribution (simulate.cpp:257-266, 281-285); the
@@ -35,16 +40,27 @@ namespace pat {
 
 // ------------------------------------------------------------------------- memory primitives
 
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+// Flags and fences at .gpu scope when every rank lives on this device, .sys across GPUs.
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, bool gpu) {
   uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  if (gpu) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v, bool gpu) {
+  if (gpu) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, bool gpu) {
+  if (gpu) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel(bool gpu) {
+  if (gpu) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -186,12 +202,14 @@ __device__ __forceinline__ uint64_t fold_elem_bits(uint64_t a, uint64_t b) {
   return r;
 }
 
+
 // ------------------------------------------------------------------------- waits
 
 struct Waiter {
   uint64_t timeout_ns;
   int* err;
   bool aborted;
+  bool gpu;  // flag scope
 };
 
 __device__ __noinline__ void report_timeout(Waiter& w) {
@@ -206,7 +224,7 @@ __device__ __forceinline__ void wait_flag(const uint64_t* flag, uint64_t want, W
   if (w.aborted) return;
   uint64_t start = 0;
   uint32_t spins = 0;
-  while (ld_acquire_sys(flag) < want) {
+  while (ld_acquire(flag, w.gpu) < want) {
     if ((++spins & 1023u) == 0) {
       const uint64_t now = globaltimer();
       if (start == 0) start = now;
@@ -233,14 +251,15 @@ __device__ __forceinline__ uint2 ld_ll(const char* line, uint32_t flag, Waiter& 
   return make_uint2(v.x, v.z);
 }
 
-// ------------------------------------------------------------------------- CTA data movers
+// ------------------------------------------------------------------------- group data movers
 
-// dst = fold_left(src[0], ..., src[m-1]) over `len` bytes (16-byte vectors; len % 16 == 0).
+// dst = fold_left(src[0], ..., src[m-1]) over `len` bytes (16-byte vectors; len % 16 == 0),
+// by the `nthr` threads of one warp group (thread index `tid` within the group).
 template <int DT, int OP>
-__device__ __forceinline__ void cta_fold16(char* dst, const char* const* src, int m, int64_t len) {
+__device__ __forceinline__ void grp_fold16(char* dst, const char* const* src, int m, int64_t len, int tid, int nthr) {
   const int64_t nu = len >> 4;
-  const int64_t B = blockDim.x;
-  int64_t u = threadIdx.x;
+  const int64_t B = nthr;
+  int64_t u = tid;
   if (m == 1) {
     const char* s0 = src[0];
     for (; u + 3 * B < nu; u += 4 * B) {
@@ -273,9 +292,10 @@ __device__ __forceinline__ void cta_fold16(char* dst, const char* const* src, in
 
 // Element-granular variant for buffers that are not 16-byte aligned.
 template <int DT, int OP>
-__device__ __forceinline__ void cta_fold_elems(char* dst, const char* const* src, int m, int64_t len, int esize) {
+__device__ __forceinline__ void grp_fold_elems(char* dst, const char* const* src, int m, int64_t len, int esize,
+                                               int tid, int nthr) {
   const int64_t ne = len / esize;
-  for (int64_t e = threadIdx.x; e < ne; e += blockDim.x) {
+  for (int64_t e = tid; e < ne; e += nthr) {
     uint64_t a = ld_elem(src[0] + e * esize, esize);
     for (int k = 1; k < m; ++k) a = fold_elem_bits<DT, OP>(a, ld_elem(src[k] + e * esize, esize));
     st_elem(dst + e * esize, a, esize);
@@ -283,10 +303,11 @@ __device__ __forceinline__ void cta_fold_elems(char* dst, const char* const* src
 }
 
 template <int DT, int OP>
-__device__ __forceinline__ void cta_fold(char* dst, const char* const* src, int m, int64_t len, const KPlan& p) {
+__device__ __forceinline__ void grp_fold(char* dst, const char* const* src, int m, int64_t len, const KPlan& p,
+                                         int tid, int nthr) {
   if (len <= 0) return;
-  if (p.vec == 16) cta_fold16<DT, OP>(dst, src, m, len);
-  else cta_fold_elems<DT, OP>(dst, src, m, len, p.esize);
+  if (p.vec == 16) grp_fold16<DT, OP>(dst, src, m, len, tid, nthr);
+  else grp_fold_elems<DT, OP>(dst, src, m, len, p.esize, tid, nthr);
 }
 
 // 8-byte user words for LL (zero padded past `valid`).
@@ -311,7 +332,7 @@ __device__ __forceinline__ void store_word(char* p, uint2 w, int valid, const KP
   }
 }
 
-// ------------------------------------------------------------------------- one pipeline step
+// ------------------------------------------------------------------------- steps
 
 struct Step {
   uint64_t g;        // absolute pipeline step of this channel
@@ -319,48 +340,70 @@ struct Step {
   int R, lr, c, buf;
 };
 
+__device__ __forceinline__ Step make_step(const KPlan& p, uint64_t base, int i, int R, int lr, int c) {
+  Step s;
+  s.g = base + i;
+  s.off = (static_cast<int64_t>(i) * p.channels + c) * p.slice_bytes;
+  s.len = max(int64_t{0}, min(p.slice_bytes, p.chunk_bytes - s.off));
+  s.R = R;
+  s.lr = lr;
+  s.c = c;
+  s.buf = static_cast<int>(s.g % static_cast<uint64_t>(p.depth));
+  return s;
+}
+
 __device__ __forceinline__ char* slot_ptr(const KPlan& p, int rank, int c, int buf, int j) {
   return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j) * p.slot_stride;
 }
 
-// SIMPLE: CTA-cooperative copies/folds; flags per (channel, round).
+__device__ __forceinline__ uint64_t* chan_flags(const KPlan& p, int rank, int c) {
+  return p.flags[rank] + c * kFlagWords;
+}
+
+// Credits: before pushing step g into a peer's inbox buffer g % depth, the peer must have
+// finished step g - depth (published as done_from[peer] >= g - depth + 1).
+__device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Waiter& w) {
+  if (s.g < static_cast<uint64_t>(p.depth)) return;
+  const uint64_t* mine = chan_flags(p, s.R, s.c);
+  for (int k = 0; k < p.npeers; ++k) wait_flag(mine + 8 + (s.R + p.peers[k]) % p.n, s.g - p.depth + 1, w);
+}
+
+// SIMPLE sender role: pushes every round of step s (warps [0, send_warps)).
 template <int DT, int OP, int KIND>
-__device__ void step_simple(const KPlan& p, const Step& s, Waiter& w) {
+__device__ void send_step(const KPlan& p, const Step& s, Waiter& w, int tid, int nthr) {
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const char* snd = p.send[s.lr];
   char* out = p.recv[s.lr];
-  uint64_t* myflags = p.flags[s.R] + s.c * kFlagWords;
+  const uint64_t* myflags = chan_flags(p, s.R, s.c);
+  const bool gpu = p.gpu_scope;
   uint32_t waited = 0;
-  auto ensure = [&](int t) {
+  auto ensure = [&](int t) {  // arrivals of round t (needed for forwarding)
     if (!((waited >> t) & 1u)) {
-      if (threadIdx.x == 0) wait_flag(myflags + t, s.g + 1, w);
-      __syncthreads();
+      if (tid == 0) wait_flag(myflags + t, s.g + 1, w);
+      named_bar(1, nthr);
       waited |= 1u << t;
     }
   };
+  if (tid == 0 && !p.direct) wait_credits(p, s, w);
+  named_bar(1, nthr);
   const char* srcs[kMaxArr + 1];
-
-  if constexpr (KIND == kAG) {
-    if (out + s.R * Cb != snd) {  // own chunk placement (simulate.cpp:160-165); skipped in place
-      srcs[0] = snd + s.off;
-      cta_fold<DT, OP>(out + s.R * Cb + s.off, srcs, 1, s.len, p);
-    }
-  }
   for (int t = 0; t < p.nrounds; ++t) {
     const KRound& r = p.rounds[t];
     const int P = (s.R + r.peer) % n;
     for (int pos = 0; pos < r.nchunks; ++pos) {
-      char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
       int m = 0;
+      char* dst;
       if constexpr (KIND == kAG) {
+        const int origin = (s.R - r.chunk[pos] + n) % n;
         if (r.narr[pos] == 0) {
           srcs[m++] = snd + s.off;
         } else {
           const int j = r.arr[pos][0];
           ensure(p.slot_round[j]);
-          srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, j);
+          srcs[m++] = p.direct ? out + origin * Cb + s.off : slot_ptr(p, s.R, s.c, s.buf, j);
         }
+        dst = p.direct ? p.peer_recv[P] + origin * Cb + s.off : slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
       } else {
         const int dest = (s.R - r.chunk[pos] + n) % n;
         for (int a = 0; a < r.narr[pos]; ++a) {
@@ -369,26 +412,70 @@ __device__ void step_simple(const KPlan& p, const Step& s, Waiter& w) {
           srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, j);
         }
         srcs[m++] = snd + dest * Cb + s.off;  // own contribution folded last
+        dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
       }
-      cta_fold<DT, OP>(dst, srcs, m, s.len, p);
+      grp_fold<DT, OP>(dst, srcs, m, s.len, p, tid, nthr);
     }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) st_relaxed_sys(p.flags[P] + s.c * kFlagWords + t, s.g + 1);
+    named_bar(1, nthr);
+    if (tid == 0) {
+      fence_acq_rel(gpu);
+      st_relaxed(chan_flags(p, P, s.c) + t, s.g + 1, gpu);
+    }
   }
-  for (int t = 0; t < p.nrounds; ++t) ensure(t);
+}
+
+// SIMPLE receiver role: delivers (AG) or folds the output (RS) of step s, then — once the
+// sender role is also done with this step's inbox — publishes done(g) to every rank.
+template <int DT, int OP, int KIND>
+__device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int nthr,
+                          volatile uint64_t* sent_steps) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const char* snd = p.send[s.lr];
+  char* out = p.recv[s.lr];
+  const uint64_t* myflags = chan_flags(p, s.R, s.c);
+  const bool gpu = p.gpu_scope;
+  const char* srcs[kMaxArr + 1];
   if constexpr (KIND == kAG) {
-    for (int j = 0; j < p.nslots; ++j) {
-      const int origin = (s.R - p.slot_offset[j] + n) % n;
-      srcs[0] = slot_ptr(p, s.R, s.c, s.buf, j);
-      cta_fold<DT, OP>(out + origin * Cb + s.off, srcs, 1, s.len, p);
+    if (out + s.R * Cb != snd) {  // own chunk placement (simulate.cpp:160-165); skipped in place
+      srcs[0] = snd + s.off;
+      grp_fold<DT, OP>(out + s.R * Cb + s.off, srcs, 1, s.len, p, tid, nthr);
     }
-  } else {
+  }
+  for (int t = 0; t < p.nrounds; ++t) {
+    if (tid == 0) wait_flag(myflags + t, s.g + 1, w);
+    named_bar(2, nthr);
+    if constexpr (KIND == kAG) {
+      if (!p.direct) {
+        const KRound& r = p.rounds[t];
+        for (int pos = 0; pos < r.nchunks; ++pos) {
+          const int j = r.slot_base + pos;
+          const int origin = (s.R - p.slot_offset[j] + n) % n;
+          srcs[0] = slot_ptr(p, s.R, s.c, s.buf, j);
+          grp_fold<DT, OP>(out + origin * Cb + s.off, srcs, 1, s.len, p, tid, nthr);
+        }
+      }
+    }
+  }
+  if constexpr (KIND == kRS) {
     int m = 0;
     srcs[m++] = snd + s.R * Cb + s.off;  // output starts as own contribution (simulate.cpp:239)
     for (int f = 0; f < p.nfin; ++f) srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, p.fin[f]);
-    cta_fold<DT, OP>(out + s.off, srcs, m, s.len, p);
+    grp_fold<DT, OP>(out + s.off, srcs, m, s.len, p, tid, nthr);
   }
+  if (tid == 0) {  // the sender role must be done reading this step's inbox too
+    uint64_t start = 0;
+    uint32_t spins = 0;
+    while (*sent_steps < s.g + 1 && !w.aborted) {
+      if ((++spins & 1023u) == 0) {
+        const uint64_t now = globaltimer();
+        if (start == 0) start = now;
+        else if (now - start > w.timeout_ns) report_timeout(w);
+      }
+    }
+  }
+  named_bar(2, nthr);
+  if (tid < n && tid != s.R) st_release(chan_flags(p, tid, s.c) + 8 + s.R, s.g + 1, gpu);
 }
 
 // LL: every thread owns the same 8-byte words of the slice in every chunk and round, so it
@@ -468,32 +555,52 @@ __global__ void __launch_bounds__(1024) pat_kernel(const __grid_constant__ KPlan
   const int c = blockIdx.x - lr * p.channels;
   const int R = p.rank[lr];
   __shared__ uint64_t s_base;
-  if (threadIdx.x == 0) s_base = p.iter_state[lr][c];
+  __shared__ volatile uint64_t s_sent;
+  if (threadIdx.x == 0) {
+    s_base = p.iter_state[lr][c];
+    s_sent = 0;
+  }
   __syncthreads();
   const uint64_t base = s_base;
-  Waiter w{p.timeout_ns, p.err, false};
-  uint64_t* myflags = p.flags[R] + c * kFlagWords;
+  Waiter w{p.timeout_ns, p.err, false, p.gpu_scope != 0};
 
-  for (int i = 0; i < p.iters; ++i) {
-    Step s;
-    s.g = base + i;
-    s.off = (static_cast<int64_t>(i) * p.channels + c) * p.slice_bytes;
-    s.len = max(int64_t{0}, min(p.slice_bytes, p.chunk_bytes - s.off));
-    s.R = R;
-    s.lr = lr;
-    s.c = c;
-    s.buf = static_cast<int>(s.g & 1);
-    // credits: a peer's slot buffer (g & 1) is free once it finished step g-2
-    if (s.g >= 2 && threadIdx.x == 0)
-      for (int k = 0; k < p.npeers; ++k) wait_flag(myflags + 8 + (R + p.peers[k]) % p.n, s.g - 1, w);
-    __syncthreads();
-    if (p.proto == kProtoLL) step_ll<DT, OP, KIND>(p, s, w);
-    else step_simple<DT, OP, KIND>(p, s, w);
-    __syncthreads();
-    // done with step g: every rank may re-use buffer (g & 1) of this rank's inbox
+  if (p.direct && KIND == kAG) {
+    // entry handshake: a peer may be written directly only once it entered this call
     if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
-      st_release_sys(p.flags[threadIdx.x] + c * kFlagWords + 8 + R, s.g + 1);
+      st_release(chan_flags(p, threadIdx.x, c) + 16 + R, base + 1, w.gpu);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < p.npeers; ++k)
+        wait_flag(chan_flags(p, R, c) + 16 + (R + p.peers[k]) % p.n, base + 1, w);
+    __syncthreads();
   }
+
+  if (p.proto == kProtoLL) {
+    for (int i = 0; i < p.iters; ++i) {
+      const Step s = make_step(p, base, i, R, lr, c);
+      if (threadIdx.x == 0) wait_credits(p, s, w);
+      __syncthreads();
+      step_ll<DT, OP, KIND>(p, s, w);
+      __syncthreads();
+      if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
+        st_release(chan_flags(p, threadIdx.x, c) + 8 + R, s.g + 1, w.gpu);
+    }
+  } else {
+    const int nsend = p.send_warps * 32;
+    if (static_cast<int>(threadIdx.x) < nsend) {
+      for (int i = 0; i < p.iters; ++i) {
+        const Step s = make_step(p, base, i, R, lr, c);
+        send_step<DT, OP, KIND>(p, s, w, threadIdx.x, nsend);
+        if (threadIdx.x == 0) s_sent = s.g + 1;  // after the group's last barrier of the step
+      }
+    } else {
+      const int tid = threadIdx.x - nsend, nrecv = blockDim.x - nsend;
+      for (int i = 0; i < p.iters; ++i) {
+        const Step s = make_step(p, base, i, R, lr, c);
+        recv_step<DT, OP, KIND>(p, s, w, tid, nrecv, &s_sent);
+      }
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) p.iter_state[lr][c] = base + p.iters;
 }
 

@@ -15,7 +15,8 @@ constexpr int kMaxSlots = 8;    // inbox slots per pipeline step (= n-1 arrivals
 constexpr int kMaxArr = 8;      // arrivals folded into one forwarded offset
 constexpr int kMaxLocal = 8;    // ranks driven by one kernel (local mode)
 constexpr int kMaxChannels = 64;
-constexpr int kFlagWords = 16;  // per channel: data flag per round [0,8) + done-from per rank [8,16)
+constexpr int kFlagWords = 32;  // per channel: data flag per round [0,8), done-from per rank [8,16),
+                                // ready-from per rank [16,24) (direct mode entry handshake)
 
 enum Proto : int { kProtoLL = 1, kProtoSimple = 2 };
 enum KindK : int { kAG = 0, kRS = 1 };
@@ -36,6 +37,10 @@ struct KPlan {
   int n, nrounds, nslots, nlocal;
   int kind, proto, vec, esize;
   int channels, iters;
+  int depth;        // inbox buffers per channel (pipeline depth); buffer of step g = g % depth
+  int send_warps;   // SIMPLE: warps [0, send_warps) push, the rest deliver / fold
+  int gpu_scope;    // all ranks on this device: flags and fences at .gpu scope instead of .sys
+  int direct;       // AG: push straight into the peers' recvbufs (peer_recv), no inbox
   int64_t chunk_bytes;   // bytes of one rank chunk (AG sendcount*esize, RS recvcount*esize)
   int64_t slice_bytes;   // payload bytes per slot per pipeline step
   int64_t slot_stride;   // inbox bytes per slot
@@ -55,6 +60,7 @@ struct KPlan {
   uint64_t* iter_state[kMaxLocal];  // [kMaxChannels] pipeline-step counters per rank
   // every rank's pool, mapped into this device's address space
   char* inbox[kMaxRanks];
+  char* peer_recv[kMaxRanks];       // direct mode: every rank's recvbuf as seen from this device
   uint64_t* flags[kMaxRanks];       // [kMaxChannels][kFlagWords]
   int* err;                         // mapped pinned host word (first async error)
 };
