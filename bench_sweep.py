@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--ranks", type=int, default=8, help="logical ranks when run without torchrun")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--protocol", type=int, default=0)
+    ap.add_argument("--mode", default="loop", choices=["loop", "events", "graph"],
+                    help="loop: K back-to-back calls between two events (nccl-tests style); events: one "
+                         "event pair per call (median); graph: K calls captured in a CUDA graph")
     args = ap.parse_args()
 
     import torch
@@ -66,16 +69,44 @@ def main():
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
-        for a, b in evs:
-            if big:
-                flush.zero_()
-            a.record(stream)
-            fn()
-            b.record(stream)
-        torch.cuda.synchronize(dev)
-        ts = sorted(a.elapsed_time(b) for a, b in evs)
-        med = torch.tensor([ts[len(ts) // 2] * 1e3], dtype=torch.float64, device=dev)
+        if args.mode == "events":
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.iters)]
+            for a, b in evs:
+                if big:
+                    flush.zero_()
+                a.record(stream)
+                fn()
+                b.record(stream)
+            torch.cuda.synchronize(dev)
+            ts = sorted(a.elapsed_time(b) for a, b in evs)
+            us = ts[len(ts) // 2] * 1e3
+        else:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if args.mode == "graph":
+                g = torch.cuda.CUDAGraph()
+                s2 = torch.cuda.Stream(dev)
+                s2.wait_stream(stream)
+                with torch.cuda.stream(s2):
+                    with torch.cuda.graph(g, stream=s2):
+                        for _ in range(args.iters):
+                            fn()
+                stream.wait_stream(s2)
+                g.replay()
+                torch.cuda.synchronize(dev)
+                if world > 1:
+                    dist.barrier()
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+            else:
+                a.record(stream)
+                for _ in range(args.iters):
+                    fn()
+                b.record(stream)
+            torch.cuda.synchronize(dev)
+            us = a.elapsed_time(b) * 1e3 / args.iters
+        med = torch.tensor([us], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(med, op=dist.ReduceOp.MAX)
         return float(med.item())

@@ -37,8 +37,8 @@ namespace {
 
 constexpr size_t kFlagBytes = sizeof(uint64_t) * kMaxChannels * kFlagWords;  // 8 KiB
 constexpr uint32_t kMagic = 0x50415442;                                       // "PATB"
-constexpr size_t kDefaultSlice = 128 << 10;
-constexpr int kDefaultChannels = 32;
+constexpr size_t kDefaultStepBytes = 256 << 10;  // inbox bytes per channel per pipeline step
+constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
 constexpr size_t kDefaultLL = 64 << 10;
 constexpr int kDefaultTimeoutMs = 20000;
 
@@ -149,7 +149,9 @@ void fill_defaults(patConfig_t* c, int n) {
   long long v;
   if (c->max_channels <= 0) c->max_channels = env_int("PAT_CHANNELS", &v) ? (int)v : kDefaultChannels;
   c->max_channels = std::min(std::max(c->max_channels, 1), kMaxChannels);
-  if (c->slice_bytes == 0) c->slice_bytes = env_int("PAT_SLICE_BYTES", &v) ? (size_t)v : kDefaultSlice;
+  if (c->slice_bytes == 0)  // one step carries (n-1) slices: keep the step volume fixed across n
+    c->slice_bytes = env_int("PAT_SLICE_BYTES", &v) ? (size_t)v
+                                                    : std::max<size_t>(4096, kDefaultStepBytes / std::max(n - 1, 1));
   c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(15));
   if (c->ll_threshold == 0) c->ll_threshold = env_int("PAT_LL_THRESHOLD", &v) ? (size_t)v : kDefaultLL;
   if (c->timeout_ms <= 0) c->timeout_ms = env_int("PAT_TIMEOUT_MS", &v) ? (int)v : kDefaultTimeoutMs;
@@ -264,22 +266,42 @@ struct Slicing {
   int64_t slice;
 };
 
-Slicing choose_slicing(const patComm* comm, int64_t chunk_bytes) {
+Slicing choose_slicing(const patComm* comm, int64_t chunk_bytes, int max_channels) {
   Slicing s{};
+  const int channels = std::max(1, std::min(comm->channels, max_channels));
   int proto = comm->cfg.protocol;
   if (proto == patProtoAuto) proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold) ? kProtoLL : kProtoSimple;
   s.proto = proto;
   const int64_t cap = proto == kProtoLL ? static_cast<int64_t>(comm->slot_bytes / 2) : static_cast<int64_t>(comm->slot_bytes);
   const int64_t minslice = proto == kProtoLL ? 512 : 16 << 10;
-  int64_t per = (chunk_bytes + comm->channels - 1) / comm->channels;
+  int64_t per = (chunk_bytes + channels - 1) / channels;
   per = (per + 15) & ~int64_t(15);
   per = std::max<int64_t>(per, std::min<int64_t>(minslice, cap));
   per = std::min<int64_t>(per, cap);
   s.slice = std::max<int64_t>(per, 16);
   const int64_t nslices = std::max<int64_t>(1, (chunk_bytes + s.slice - 1) / s.slice);
-  s.channels = static_cast<int>(std::min<int64_t>(comm->channels, nslices));
+  s.channels = static_cast<int>(std::min<int64_t>(channels, nslices));
   s.iters = static_cast<int>((nslices + s.channels - 1) / s.channels);
   return s;
+}
+
+// Channels per rank such that every device's launch stays co-resident (cooperative launch).
+patResult_t channel_cap(patComm* comm, int kind, int dtype, int op, int* cap) {
+  *cap = kMaxChannels;
+  const int threads = comm->cfg.threads;
+  for (DevGroup& g : comm->groups) {
+    const std::array<int, 5> okey{kind, dtype, op, threads, g.device};
+    auto oit = comm->occupancy.find(okey);
+    if (oit == comm->occupancy.end()) {
+      int nb = 0;
+      CUDA_TRY(cudaSetDevice(g.device));
+      CUDA_TRY(max_blocks_per_sm(kind, dtype, op, threads, &nb));
+      oit = comm->occupancy.emplace(okey, nb).first;
+    }
+    *cap = std::min(*cap, oit->second * g.sm_count / static_cast<int>(g.lidx.size()));
+  }
+  if (*cap < 1) return patInvalidUsage;
+  return patSuccess;
 }
 
 patResult_t alloc_pool(patComm* comm, int device, char** pool) {
@@ -365,7 +387,10 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     return e;
   }
   const int64_t chunk_bytes = static_cast<int64_t>(count * es);
-  const Slicing sl = choose_slicing(comm, chunk_bytes);
+  DeviceGuard guard;
+  int cap = 0;
+  if (patResult_t e = channel_cap(comm, kind, dtype, op, &cap)) return e;
+  const Slicing sl = choose_slicing(comm, chunk_bytes, cap);
   int vec = 16;
   bool aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
   for (size_t l = 0; l < comm->lranks.size(); ++l) {
@@ -386,7 +411,6 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       for (size_t l = 0; l < comm->lranks.size() && direct; ++l) direct = legacy_ipc_capable(recvbuffs[l]);
     }
   }
-  DeviceGuard guard;
   for (DevGroup& g : comm->groups) {
     KPlan p = cp->proto;
     p.nlocal = static_cast<int>(g.lidx.size());
@@ -420,18 +444,6 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     }
     CUDA_TRY(cudaSetDevice(g.device));
     const int threads = comm->cfg.threads;
-    const std::array<int, 5> okey{kind, dtype, op, threads, g.device};
-    auto oit = comm->occupancy.find(okey);
-    if (oit == comm->occupancy.end()) {
-      int nb = 0;
-      CUDA_TRY(max_blocks_per_sm(kind, dtype, op, threads, &nb));
-      oit = comm->occupancy.emplace(okey, nb).first;
-    }
-    if (p.nlocal * p.channels > oit->second * g.sm_count) {
-      std::fprintf(stderr, "pat_b200: %d CTAs exceed co-residency (%d per SM x %d SMs)\n",
-                   p.nlocal * p.channels, oit->second, g.sm_count);
-      return patInvalidUsage;
-    }
     cudaStream_t s0 = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr;
     for (size_t i = 1; i < g.lidx.size(); ++i) {  // join the other local ranks' streams
       cudaStream_t si = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[i]]) : nullptr;
@@ -655,7 +667,10 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   Compiled* cp = nullptr;
   if (patResult_t e = compile(comm, kind, trees, &cp)) return e;
   const int64_t cb = static_cast<int64_t>(count * es);
-  const Slicing sl = choose_slicing(comm, cb);
+  DeviceGuard guard;
+  int cap = 0;
+  if (patResult_t e = channel_cap(comm, kind, dtype, 0, &cap)) return e;
+  const Slicing sl = choose_slicing(comm, cb, cap);
   std::memset(info, 0, sizeof(*info));
   info->protocol = sl.proto;
   info->trees = trees;

@@ -260,28 +260,33 @@ __device__ __forceinline__ void grp_fold16(char* dst, const char* const* src, in
   const int64_t nu = len >> 4;
   const int64_t B = nthr;
   int64_t u = tid;
-  if (m == 1) {
+  if (m == 1) {  // copy: 8 independent 16-byte loads in flight per thread
     const char* s0 = src[0];
-    for (; u + 3 * B < nu; u += 4 * B) {
-      const uint4 a = ld16(s0 + 16 * u), b = ld16(s0 + 16 * (u + B));
-      const uint4 c = ld16(s0 + 16 * (u + 2 * B)), d = ld16(s0 + 16 * (u + 3 * B));
-      st16(dst + 16 * u, a);
-      st16(dst + 16 * (u + B), b);
-      st16(dst + 16 * (u + 2 * B), c);
-      st16(dst + 16 * (u + 3 * B), d);
+    constexpr int U = 8;
+    for (; u + (U - 1) * B < nu; u += U * B) {
+      uint4 v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) v[k] = ld16(s0 + 16 * (u + k * B));
+#pragma unroll
+      for (int k = 0; k < U; ++k) st16(dst + 16 * (u + k * B), v[k]);
     }
     for (; u < nu; u += B) st16(dst + 16 * u, ld16(s0 + 16 * u));
     return;
   }
-  for (; u + B < nu; u += 2 * B) {
-    uint4 a0 = ld16(src[0] + 16 * u), a1 = ld16(src[0] + 16 * (u + B));
+  constexpr int U = 4;
+  for (; u + (U - 1) * B < nu; u += U * B) {
+    uint4 a[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) a[i] = ld16(src[0] + 16 * (u + i * B));
     for (int k = 1; k < m; ++k) {
-      const uint4 b0 = ld16(src[k] + 16 * u), b1 = ld16(src[k] + 16 * (u + B));
-      fold_vec<DT, OP>(a0, b0);
-      fold_vec<DT, OP>(a1, b1);
+      uint4 b[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) b[i] = ld16(src[k] + 16 * (u + i * B));
+#pragma unroll
+      for (int i = 0; i < U; ++i) fold_vec<DT, OP>(a[i], b[i]);
     }
-    st16(dst + 16 * u, a0);
-    st16(dst + 16 * (u + B), a1);
+#pragma unroll
+    for (int i = 0; i < U; ++i) st16(dst + 16 * (u + i * B), a[i]);
   }
   for (; u < nu; u += B) {
     uint4 a = ld16(src[0] + 16 * u);
