@@ -110,6 +110,9 @@ typedef struct {
                                auto = single-process communicator whose recvbufs are reachable
                                (same device, or cudaMalloc memory with peer access) */
   int send_warps;           /* SIMPLE: warps per CTA that push (rest deliver); 0 = half */
+  int fused;                /* all ranks on one device: -1 = run the transport kernel anyway,
+                               0 = fused single-device executor (one read of every input, one
+                               write of every output, same fold tree as the schedule) */
 } patConfig_t;
 
 /* Plan the library would launch for one call (introspection / benchmarks). */

@@ -56,6 +56,7 @@ class Config(ctypes.Structure):
         ("depth", ctypes.c_int),
         ("direct", ctypes.c_int),
         ("send_warps", ctypes.c_int),
+        ("fused", ctypes.c_int),
     ]
 
 

@@ -29,6 +29,10 @@ namespace pat {
 using KernelFn = void (*)(const KPlan);
 cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream);
 cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out);
+cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize, int64_t chunk_bytes,
+                         const char* const* send_by_rank, char* const* recv_by_rank, int sm_count,
+                         cudaStream_t stream);
+const char* local_tree_string(int n);
 }  // namespace pat
 
 using namespace pat;
@@ -46,6 +50,7 @@ struct Compiled {
   Schedule sched;
   KPlan proto;  // schedule part of the plan (rounds, slots, fin, peers)
   int peak_slots = 0;
+  bool fused_ok = false;  // the fused single-device executor computes exactly this schedule
 };
 
 struct DevGroup {
@@ -161,6 +166,7 @@ void fill_defaults(patConfig_t* c, int n) {
   if (c->depth <= 0) c->depth = env_int("PAT_DEPTH", &v) ? (int)v : 2;
   c->depth = std::min(std::max(c->depth, 1), 16);
   if (c->direct == 0 && env_int("PAT_DIRECT", &v)) c->direct = (int)v;
+  if (c->fused == 0 && env_int("PAT_FUSED", &v)) c->fused = (int)v;
   if (c->send_warps <= 0) c->send_warps = env_int("PAT_SEND_WARPS", &v) ? (int)v : c->threads / 64;
   c->send_warps = std::min(std::max(c->send_warps, 1), c->threads / 32 - 1);
   if (c->staging_bytes != 0) {
@@ -170,6 +176,52 @@ void fill_defaults(patConfig_t* c, int n) {
     if (s < 256) s = 256;
     c->slice_bytes = s;
   }
+}
+
+// Symbolic run of a reduce-scatter schedule with the executor's fold rules
+// (simulate.cpp:237-290): returns rank 0's output as an expression over x_j = contribution of
+// rank j, accumulator as left operand, e.g. "((x0+x1)+(x3+x2))" for PAT at n = 4. Rank 0
+// stands for every rank: schedules are translation invariant (schedule.hpp:56-63).
+std::string symbolic_reduce_scatter(const Schedule& s) {
+  const int n = s.n;
+  // expressions over absolute contributions c(src, dest) -> only dest == rank-local matter;
+  // track every rank, then read rank 0 where c(src, 0) = x_src.
+  std::vector<std::string> out(n);
+  std::vector<std::map<int, std::string>> acc(n);
+  auto own = [&](int src, int dest) { return "c" + std::to_string(src) + "_" + std::to_string(dest); };
+  for (int r = 0; r < n; ++r) out[r] = own(r, r);
+  for (const Round& rd : s.rounds) {
+    if (rd.exchange) return "";
+    std::vector<std::vector<std::string>> msgs(n);
+    for (int r = 0; r < n; ++r)
+      for (int k : rd.chunks) {
+        const int dest = mod_ranks(int64_t{r} - k, n);
+        auto it = acc[r].find(k);
+        msgs[r].push_back(it == acc[r].end() ? own(r, dest) : "(" + it->second + "+" + own(r, dest) + ")");
+      }
+    for (int r = 0; r < n; ++r) {
+      const int src = mod_ranks(int64_t{r} - rd.peer, n);
+      for (size_t i = 0; i < rd.chunks.size(); ++i) {
+        const int k = received_offset(rd, rd.chunks[i], n);
+        const std::string& m = msgs[src][i];
+        if (k == 0) out[r] = "(" + out[r] + "+" + m + ")";
+        else if (!acc[r].count(k)) acc[r][k] = m;
+        else acc[r][k] = "(" + acc[r][k] + "+" + m + ")";
+      }
+      for (int k : rd.chunks) acc[r].erase(k);
+    }
+  }
+  std::string e = out[0], res;  // c<src>_0 -> x<src>
+  for (size_t i = 0; i < e.size();) {
+    if (e[i] == 'c') {
+      size_t j = e.find('_', i);
+      res += "x" + e.substr(i + 1, j - i - 1);
+      i = j + 2;  // skip "_0"
+    } else {
+      res += e[i++];
+    }
+  }
+  return res;
 }
 
 // Compile a validated schedule into the schedule part of a KPlan (arrival slots, fold lists).
@@ -241,6 +293,7 @@ patResult_t compile_schedule(patComm* comm, const Schedule& given, Compiled** ou
     if (!seen) p.peers[p.npeers++] = p.rounds[t].peer;
   }
   c.peak_slots = schedule_stats(s, 1).peak;
+  c.fused_ok = kind == kAG || symbolic_reduce_scatter(s) == local_tree_string(n);
   auto ins = comm->compiled.emplace(std::move(key), std::move(c));
   *out = &ins.first->second;
   return patSuccess;
@@ -403,6 +456,8 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   if (sl.proto == kProtoSimple && vec == 8) vec = 0;  // SIMPLE vectors are 16 bytes
   // one device holds every rank: .gpu-scope flags; zero-copy all-gather is always safe
   const bool single_device = !comm->multiprocess && comm->groups.size() == 1;
+  const bool fused = single_device && comm->cfg.fused >= 0 && cp->fused_ok &&
+                     static_cast<int>(comm->groups[0].lidx.size()) == n;
   bool direct = false;
   if (kind == kAG && sl.proto == kProtoSimple && !comm->multiprocess && comm->cfg.direct >= 0) {
     direct = single_device || comm->cfg.direct > 0;
@@ -451,7 +506,18 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       CUDA_TRY(cudaEventRecord(comm->events[g.lidx[i]], si));
       CUDA_TRY(cudaStreamWaitEvent(s0, comm->events[g.lidx[i]], 0));
     }
-    CUDA_TRY(launch(p, dtype, op, threads, s0));
+    if (fused) {  // every rank in this HBM: fused executor (local.cu), no transport
+      const char* sb[kMaxRanks];
+      char* rb[kMaxRanks];
+      for (size_t i = 0; i < g.lidx.size(); ++i) {
+        sb[p.rank[i]] = p.send[i];
+        rb[p.rank[i]] = p.recv[i];
+      }
+      CUDA_TRY(launch_local(kind, n, dtype, op, aligned16 ? 16 : 0, static_cast<int>(es), chunk_bytes, sb, rb,
+                            g.sm_count, s0));
+    } else {
+      CUDA_TRY(launch(p, dtype, op, threads, s0));
+    }
     CUDA_TRY(cudaEventRecord(comm->events[g.lidx[0]], s0));
     for (size_t i = 1; i < g.lidx.size(); ++i) {
       cudaStream_t si = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[i]]) : nullptr;

@@ -1,0 +1,203 @@
+// local.cu — fused single-device executor: every rank of the communicator lives in this
+// GPU's HBM ("local mode", the reference's in-process ranks, simulate.cpp:157-165).
+//
+// With all ranks' buffers in one HBM the per-round messages of the PAT schedule are pure
+// overhead: the result is fixed by the schedule alone. All-gather output is the
+// concatenation of the inputs (oracle.cpp:15-24). Reduce-scatter output r is the PAT fold
+// tree over x_j = contribution of rank (r + j) mod n, with the executor's operand order
+// (accumulator left): the host symbolically executes the compiled schedule (comm.cpp,
+// symbolic_reduce_scatter) and only takes this path when the result equals the tree
+// compiled in here (T-independent for PAT):
+//   n=2  x0+x1
+//   n=3  (x0+x1)+x2
+//   n=4  (x0+x1)+(x3+x2)
+//   n=5  ((x0+x1)+(x3+x2))+x4
+//   n=6  ((x0+x1)+(x3+x2))+(x5+x4)
+//   n=7  ((x0+x1)+(x3+x2))+((x5+x6)+x4)
+//   n=8  ((x0+x1)+(x3+x2))+((x5+(x7+x6))+x4)
+// So each kernel reads every input byte once and writes every output byte once: the HBM
+// roofline of the collective (n*C read + n^2*C written for AG, n^2*C read + n*C written for RS).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include <algorithm>
+
+#include "fold.cuh"
+
+namespace pat {
+
+struct LPlan {
+  int n, kind, vec, esize;
+  int64_t chunk_bytes;
+  const char* send[kLocalMaxRanks];  // by rank
+  char* recv[kLocalMaxRanks];        // by rank
+};
+
+__device__ __forceinline__ uint4 ld_nc16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_cs16(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <int DT, int OP, int N, typename V>
+__device__ __forceinline__ V tree(const V* x) {
+  auto f = [](V a, const V& b) {
+    fold_vec<DT, OP>(a, b);
+    return a;
+  };
+  if constexpr (N == 1) return x[0];
+  else if constexpr (N == 2) return f(x[0], x[1]);
+  else if constexpr (N == 3) return f(f(x[0], x[1]), x[2]);
+  else if constexpr (N == 4) return f(f(x[0], x[1]), f(x[3], x[2]));
+  else if constexpr (N == 5) return f(f(f(x[0], x[1]), f(x[3], x[2])), x[4]);
+  else if constexpr (N == 6) return f(f(f(x[0], x[1]), f(x[3], x[2])), f(x[5], x[4]));
+  else if constexpr (N == 7) return f(f(f(x[0], x[1]), f(x[3], x[2])), f(f(x[5], x[6]), x[4]));
+  else return f(f(f(x[0], x[1]), f(x[3], x[2])), f(f(x[5], f(x[7], x[6])), x[4]));
+}
+
+// All-gather: unit u of origin o is read once and written to all n outputs.
+__global__ void __launch_bounds__(512) local_ag_kernel(const __grid_constant__ LPlan p) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (p.vec == 16) {
+    const int64_t nu = Cb >> 4;
+    const int64_t total = nu * n;
+    constexpr int U = 4;
+    int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < total; i += U * stride) {
+      uint4 v[U];
+      int64_t o[U], u[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        o[k] = (i + k * stride) / nu;
+        u[k] = (i + k * stride) - o[k] * nu;
+        v[k] = ld_nc16(p.send[o[k]] + 16 * u[k]);
+      }
+      for (int r = 0; r < n; ++r)
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          char* dst = p.recv[r] + o[k] * Cb + 16 * u[k];
+          if (dst != p.send[o[k]] + 16 * u[k]) st_cs16(dst, v[k]);
+        }
+    }
+    for (; i < total; i += stride) {
+      const int64_t o = i / nu, u = i - o * nu;
+      const uint4 v = ld_nc16(p.send[o] + 16 * u);
+      for (int r = 0; r < n; ++r) {
+        char* dst = p.recv[r] + o * Cb + 16 * u;
+        if (dst != p.send[o] + 16 * u) st_cs16(dst, v);
+      }
+    }
+  } else {
+    const int es = p.esize;
+    const int64_t ne = Cb / es, total = ne * n;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int64_t o = i / ne, e = i - o * ne;
+      const uint64_t v = ld_elem(p.send[o] + e * es, es);
+      for (int r = 0; r < n; ++r) {
+        char* dst = p.recv[r] + o * Cb + e * es;
+        if (dst != p.send[o] + e * es) st_elem(dst, v, es);
+      }
+    }
+  }
+}
+
+// Reduce-scatter: out[r] = tree(x_0..x_{n-1}), x_j = send[(r+j) % n] block r.
+template <int DT, int OP, int N>
+__device__ __forceinline__ void local_rs_body(const LPlan& p) {
+  const int64_t Cb = p.chunk_bytes;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (p.vec == 16) {
+    const int64_t nu = Cb >> 4, total = nu * N;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int r = static_cast<int>(i / nu);
+      const int64_t u = i - static_cast<int64_t>(r) * nu;
+      uint4 x[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) x[j] = ld_nc16(p.send[(r + j) % N] + r * Cb + 16 * u);
+      st_cs16(p.recv[r] + 16 * u, tree<DT, OP, N>(x));
+    }
+  } else {
+    using S = typename DType<DT>::S;
+    const int64_t ne = Cb / static_cast<int64_t>(sizeof(S)), total = ne * N;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int r = static_cast<int>(i / ne);
+      const int64_t e = i - static_cast<int64_t>(r) * ne;
+      S x[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+        x[j] = *reinterpret_cast<const S*>(p.send[(r + j) % N] + r * Cb + e * static_cast<int64_t>(sizeof(S)));
+      *reinterpret_cast<S*>(p.recv[r] + e * static_cast<int64_t>(sizeof(S))) = tree_scalar<DT, OP, N>(x);
+    }
+  }
+}
+
+template <int DT, int OP>
+__global__ void __launch_bounds__(512) local_rs_kernel(const __grid_constant__ LPlan p) {
+  switch (p.n) {
+    case 1: local_rs_body<DT, OP, 1>(p); break;
+    case 2: local_rs_body<DT, OP, 2>(p); break;
+    case 3: local_rs_body<DT, OP, 3>(p); break;
+    case 4: local_rs_body<DT, OP, 4>(p); break;
+    case 5: local_rs_body<DT, OP, 5>(p); break;
+    case 6: local_rs_body<DT, OP, 6>(p); break;
+    case 7: local_rs_body<DT, OP, 7>(p); break;
+    default: local_rs_body<DT, OP, 8>(p); break;
+  }
+}
+
+using LocalFn = void (*)(const LPlan);
+#define PAT_LRS_ROW(DT) \
+  { local_rs_kernel<DT, kSum>, local_rs_kernel<DT, kProd>, local_rs_kernel<DT, kMax>, local_rs_kernel<DT, kMin> }
+static const LocalFn kLocalRs[10][4] = {
+    PAT_LRS_ROW(kI8), PAT_LRS_ROW(kU8), PAT_LRS_ROW(kI32), PAT_LRS_ROW(kU32), PAT_LRS_ROW(kI64),
+    PAT_LRS_ROW(kU64), PAT_LRS_ROW(kF16), PAT_LRS_ROW(kF32), PAT_LRS_ROW(kF64), PAT_LRS_ROW(kBF16)};
+
+// The tree the fused reduce-scatter evaluates, in the symbolic form comm.cpp produces.
+const char* local_tree_string(int n) {
+  switch (n) {
+    case 1: return "x0";
+    case 2: return "(x0+x1)";
+    case 3: return "((x0+x1)+x2)";
+    case 4: return "((x0+x1)+(x3+x2))";
+    case 5: return "(((x0+x1)+(x3+x2))+x4)";
+    case 6: return "(((x0+x1)+(x3+x2))+(x5+x4))";
+    case 7: return "(((x0+x1)+(x3+x2))+((x5+x6)+x4))";
+    case 8: return "(((x0+x1)+(x3+x2))+((x5+(x7+x6))+x4))";
+    default: return "";
+  }
+}
+
+cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize, int64_t chunk_bytes,
+                         const char* const* send_by_rank, char* const* recv_by_rank, int sm_count,
+                         cudaStream_t stream) {
+  LPlan p{};
+  p.n = n;
+  p.kind = kind;
+  p.vec = vec;
+  p.esize = esize;
+  p.chunk_bytes = chunk_bytes;
+  for (int r = 0; r < n; ++r) {
+    p.send[r] = send_by_rank[r];
+    p.recv[r] = recv_by_rank[r];
+  }
+  const int threads = 512;
+  const int64_t units = vec == 16 ? (chunk_bytes >> 4) * n : (chunk_bytes / esize) * n;
+  const int64_t want = (units + threads - 1) / threads;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 4LL * sm_count)));
+  if (kind == 0) local_ag_kernel<<<blocks, threads, 0, stream>>>(p);
+  else kLocalRs[dtype][op]<<<blocks, threads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace pat

@@ -153,11 +153,15 @@ def test_simulate_api_errors():
 
 # ------------------------------------------------------------------ local mode (n logical ranks, one GPU)
 
+EXECUTORS = {"fused": 0, "transport": -1}
+
+
+@pytest.mark.parametrize("executor", EXECUTORS)
 @pytest.mark.parametrize("n", range(1, 9))
 @pytest.mark.parametrize("elems", [1, 3, 64, 1000, 40000])
-def test_allgather_local_all_trees(n, elems):
+def test_allgather_local_all_trees(n, elems, executor):
     for t in O.valid_tree_counts(n):
-        comm = comm_for(n, trees=t)
+        comm = comm_for(n, trees=t, fused=EXECUTORS[executor])
         p = O.random_payload(O.FLOAT32, n, elems, n * 100 + t)
         got = gpu_allgather(comm, [0] * n, p, elems, O.FLOAT32)
         want = oracle_ag(n, t, O.FLOAT32, p, elems)
@@ -168,10 +172,11 @@ def test_allgather_local_all_trees(n, elems):
 @pytest.mark.parametrize("dt", [O.FLOAT32, O.BFLOAT16, O.FLOAT16, O.INT32, O.INT64, O.FLOAT64, O.UINT8, O.INT8,
                                 O.UINT32, O.UINT64])
 @pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 7, 8])
-def test_reduce_scatter_local_dtypes(dt, n):
+@pytest.mark.parametrize("executor", EXECUTORS)
+def test_reduce_scatter_local_dtypes(dt, n, executor):
     for elems in (1, 7, 300, 20000):
         for t in O.valid_tree_counts(n):
-            comm = comm_for(n, trees=t)
+            comm = comm_for(n, trees=t, fused=EXECUTORS[executor])
             p = O.random_payload(dt, n * n, elems, 7 * n + t + elems)
             got = gpu_reduce_scatter(comm, [0] * n, p, elems, dt, O.SUM)
             want = oracle_rs(n, t, dt, O.SUM, p, elems)
@@ -181,9 +186,10 @@ def test_reduce_scatter_local_dtypes(dt, n):
 
 @pytest.mark.parametrize("op", [O.MAX, O.MIN, O.PROD])
 @pytest.mark.parametrize("dt", [O.FLOAT32, O.BFLOAT16, O.INT32, O.FLOAT16])
-def test_reduce_scatter_ops(op, dt):
+@pytest.mark.parametrize("executor", EXECUTORS)
+def test_reduce_scatter_ops(op, dt, executor):
     for n in (3, 8):
-        comm = comm_for(n)
+        comm = comm_for(n, fused=EXECUTORS[executor])
         elems = 5000
         p = O.random_payload(dt, n * n, elems, 11)
         got = gpu_reduce_scatter(comm, [0] * n, p, elems, dt, op)
@@ -195,7 +201,7 @@ def test_reduce_scatter_ops(op, dt):
 @pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_SIMPLE])
 def test_protocols_forced(proto):
     for n in (2, 5, 8):
-        comm = comm_for(n, protocol=proto)
+        comm = comm_for(n, protocol=proto, fused=-1)
         for elems in (1, 5, 4096, 70001, 300000):
             p = O.random_payload(O.FLOAT32, n, elems, elems)
             got = gpu_allgather(comm, [0] * n, p, elems, O.FLOAT32)
@@ -207,9 +213,10 @@ def test_protocols_forced(proto):
             assert all(same(got[r], want[r]) for r in range(n)), (proto, n, elems)
 
 
-def test_misaligned_and_inplace():
+@pytest.mark.parametrize("executor", EXECUTORS)
+def test_misaligned_and_inplace(executor):
     n = 6
-    comm = comm_for(n)
+    comm = comm_for(n, fused=EXECUTORS[executor])
     for pad in (2, 4, 8):
         for elems in (3, 1001, 100003):
             p = O.random_payload(O.FLOAT16, n, elems, pad)
@@ -230,7 +237,7 @@ def test_misaligned_and_inplace():
 def test_small_slots_many_pipeline_steps():
     """A tiny staging budget forces many pipeline steps per channel (credit flow control)."""
     n = 8
-    comm = comm_for(n, staging_bytes=n * 64 * 1024, channels=4)
+    comm = comm_for(n, staging_bytes=n * 64 * 1024, channels=4, fused=-1)
     for elems in (1 << 16, 300001):
         p = O.random_payload(O.INT32, n, elems, 5)
         got = gpu_allgather(comm, [0] * n, p, elems, O.INT32)
@@ -244,10 +251,11 @@ def test_small_slots_many_pipeline_steps():
     assert plan["iterations"] > 1 and plan["channels"] == 4
 
 
-def test_back_to_back_calls_mixed_sizes():
+@pytest.mark.parametrize("executor", EXECUTORS)
+def test_back_to_back_calls_mixed_sizes(executor):
     """Iteration counters and credits persist across calls of different sizes and kinds."""
     n = 8
-    comm = comm_for(n)
+    comm = comm_for(n, fused=EXECUTORS[executor])
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(0)
     sizes = [int(x) for x in rng.integers(1, 200000, 40)]
@@ -276,10 +284,11 @@ def test_back_to_back_calls_mixed_sizes():
             assert same(o[r].cpu().numpy(), want[r]), (kind, elems, r)
 
 
-def test_explicit_schedules_generic_executor():
+@pytest.mark.parametrize("executor", EXECUTORS)
+def test_explicit_schedules_generic_executor(executor):
     """Ring / Bruck / single-tree PAT through patAllGatherSchedule / patReduceScatterSchedule."""
     for n in (3, 5, 8):
-        comm = comm_for(n)
+        comm = comm_for(n, fused=EXECUTORS[executor])
         elems = 3000
         for ag in (S.ring_allgather(n), S.bruck_nearest(n), S.bruck_farthest(n), S.pat_allgather(n, 1)):
             p = O.random_payload(O.FLOAT32, n, elems, 9)
@@ -293,11 +302,12 @@ def test_explicit_schedules_generic_executor():
             assert all(same(got[r], want[r]) for r in range(n)), (n, rs.algorithm)
 
 
-def test_large_property_checks():
+@pytest.mark.parametrize("executor", EXECUTORS)
+def test_large_property_checks(executor):
     """Full-size properties: AG output = concatenation; RS int32 = column
     sums mod 2^32; RS fp32 sampled columns = closed-form PAT tree."""
     n = 8
-    comm = comm_for(n)
+    comm = comm_for(n, fused=EXECUTORS[executor])
     dev = torch.device("cuda:0")
     elems = 8 << 20  # 32 MiB fp32 per rank
     g = torch.Generator(device=dev).manual_seed(0)
