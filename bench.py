@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 
 CHUNK_BYTES = 1 << 20  # 1 MiB per rank
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+L2_BYTES = 126 * 1000 * 1000
 NVLINK_MEASURED_GBS = 770.0  # peer copy per direction (B200_PROFILING.md)
 
 
@@ -188,19 +189,28 @@ def run_pat(args, rank, world, local):
         n = args.ranks or 8
         comm = PatComm.init_all(n, [local] * n)
         ranks_here = list(range(n))
-        placement = f"{n} logical ranks on 1 GPU (one cooperative kernel per collective)"
+        placement = f"{n} logical ranks on 1 GPU (fused single-device executor, local.cu)"
     L = len(ranks_here)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    ag_send = [torch.rand(elems, device=dev, generator=g) for _ in range(L)]
-    ag_recv = [torch.empty(n * elems, device=dev) for _ in range(L)]
-    rs_send = [torch.rand(n * elems, device=dev, generator=g) for _ in range(L)]
-    rs_recv = [torch.empty(elems, device=dev) for _ in range(L)]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    # Inputs larger than L2: the step's buffers are rotated over S sets whose total exceeds
+    # twice the 126 MB L2, so every timed step starts cold.
+    step_bytes = L * 2 * (n + 1) * C
+    S = max(2, -(-(2 * L2_BYTES) // step_bytes) + 1)
+    sets = []
+    for _ in range(S):
+        sets.append({
+            "ag_send": [torch.rand(elems, device=dev, generator=g) for _ in range(L)],
+            "ag_recv": [torch.empty(n * elems, device=dev) for _ in range(L)],
+            "rs_send": [torch.rand(n * elems, device=dev, generator=g) for _ in range(L)],
+            "rs_recv": [torch.empty(elems, device=dev) for _ in range(L)],
+        })
+    ag_send, ag_recv, rs_send, rs_recv = (sets[0][k] for k in ("ag_send", "ag_recv", "rs_send", "rs_recv"))
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        comm.all_gather(ag_send, ag_recv, elems, FLOAT32)
-        comm.reduce_scatter(rs_send, rs_recv, elems, FLOAT32, SUM)
+    def step(bs=None):
+        bs = bs or sets[0]
+        comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
+        comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
 
     def barrier():
         if world > 1:
@@ -208,19 +218,38 @@ def run_pat(args, rank, world, local):
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
-        step()
+        for bs in sets:
+            step(bs)
     barrier()
     comm.raise_async_error()
+    # The timed loop replays CUDA graphs of the C-ABI calls (one AG and one RS graph per buffer
+    # set): the launches are the library's own kernels, without Python/ctypes host overhead.
+    graphs = []
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(stream)
+    with torch.cuda.stream(cap):
+        for bs in sets:
+            ga, gr = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ga, stream=cap):
+                comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
+            with torch.cuda.graph(gr, stream=cap):
+                comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
+            graphs.append((ga, gr))
+    stream.wait_stream(cap)
+    for ga, gr in graphs:
+        ga.replay()
+        gr.replay()
+    barrier()
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     with ClockSampler(local) as clocks:
         barrier()
         for k in range(K):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ga, gr = graphs[k % S]
             ev[k][0].record(stream)
-            comm.all_gather(ag_send, ag_recv, elems, FLOAT32)
+            ga.replay()
             ev[k][1].record(stream)
-            comm.reduce_scatter(rs_send, rs_recv, elems, FLOAT32, SUM)
+            gr.replay()
             ev[k][2].record(stream)
         barrier()
     comm.raise_async_error()
@@ -265,19 +294,44 @@ def run_pat(args, rank, world, local):
     # ---- NCCL Ring comparison (N > 1)
     nccl = None
     if world > 1 and not args.no_nccl:
-        agt = torch.empty(n * elems, device=dev)
-        rst = torch.empty(elems, device=dev)
         for _ in range(args.warmup):
-            dist.all_gather_into_tensor(agt, ag_send[0])
-            dist.reduce_scatter_tensor(rst, rs_send[0])
+            for bs in sets:
+                dist.all_gather_into_tensor(bs["ag_recv"][0], bs["ag_send"][0])
+                dist.reduce_scatter_tensor(bs["rs_recv"][0], bs["rs_send"][0])
+        barrier()
+        # same timing method as the PAT arm: graph replay when NCCL captures, else eager
+        ngraphs, mode = [], "graph"
+        try:
+            cap2 = torch.cuda.Stream(dev)
+            cap2.wait_stream(stream)
+            with torch.cuda.stream(cap2):
+                for bs in sets:
+                    ga, gr = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(ga, stream=cap2):
+                        dist.all_gather_into_tensor(bs["ag_recv"][0], bs["ag_send"][0])
+                    with torch.cuda.graph(gr, stream=cap2):
+                        dist.reduce_scatter_tensor(bs["rs_recv"][0], bs["rs_send"][0])
+                    ngraphs.append((ga, gr))
+            stream.wait_stream(cap2)
+            for ga, gr in ngraphs:
+                ga.replay()
+                gr.replay()
+        except Exception:
+            mode, ngraphs = "eager", []
         barrier()
         nev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
         for k in range(K):
-            flush.zero_()
+            bs = sets[k % S]
             nev[k][0].record(stream)
-            dist.all_gather_into_tensor(agt, ag_send[0])
+            if ngraphs:
+                ngraphs[k % S][0].replay()
+            else:
+                dist.all_gather_into_tensor(bs["ag_recv"][0], bs["ag_send"][0])
             nev[k][1].record(stream)
-            dist.reduce_scatter_tensor(rst, rs_send[0])
+            if ngraphs:
+                ngraphs[k % S][1].replay()
+            else:
+                dist.reduce_scatter_tensor(bs["rs_recv"][0], bs["rs_send"][0])
             nev[k][2].record(stream)
         barrier()
         nt = torch.tensor([sum(e[0].elapsed_time(e[2]) for e in nev), sum(e[0].elapsed_time(e[1]) for e in nev),
@@ -287,7 +341,7 @@ def run_pat(args, rank, world, local):
         nccl = {"algo": os.environ.get("NCCL_ALGO"), "ms_per_step": nt[0] / K,
                 "busbw_gbs": busbw_gbs(n, C, nt[0] / K / 1e3),
                 "ag_us": 1e3 * nt[1] / K, "rs_us": 1e3 * nt[2] / K,
-                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()), "timing": mode}
 
     # ---- roofline of the dominant kernel
     peaks, peak_src = load_peaks()
@@ -296,7 +350,7 @@ def run_pat(args, rank, world, local):
     if world == 1:
         algo_bytes = (n * n + n) * C  # local mode: read n*C + write n^2*C (AG) / read n^2*C + write n*C (RS)
         peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-        roof = {"bound": "hbm", "kernel": f"pat_kernel ({dom})", "unit": "GB/s",
+        roof = {"bound": "hbm", "kernel": ("local_rs_kernel" if dom == "reduce_scatter" else "local_ag_kernel"), "unit": "GB/s",
                 "algorithmic_bytes_per_launch": algo_bytes, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
     else:
         algo_bytes = (n - 1) * C  # per rank, received over NVLink
@@ -348,7 +402,8 @@ def run_pat(args, rank, world, local):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.rand on device)",
             "config": {"workload": "BASELINE configs[0]: PAT AG + RS(sum), 1 MiB fp32 per rank",
                        "nranks": n, "placement": placement, "chunk_bytes": C, "trees": plan_ag["trees"],
-                       "rounds": plan_ag["rounds"], "l2": "flushed (256 MiB write) before every timed step",
+                       "rounds": plan_ag["rounds"], "l2": f"inputs larger than L2: {S} rotating buffer sets, {S * step_bytes / 2**20:.0f} MiB total",
+                       "timing": "CUDA events around CUDA-graph replays of the C-ABI calls, per step",
                        "plan_allgather": plan_ag, "plan_reduce_scatter": plan_rs},
             "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K},
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
@@ -393,13 +448,18 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    # one JSON line on stdout: everything else (NCCL banners, warnings) goes to stderr
+    real_stdout = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(os.dup(2), "w")
     rank, world, local = dist_env()
     if args.impl == "reference":
         out = run_reference(args, rank, world)
     else:
         out = run_pat(args, rank, world, local)
     if rank == 0 and out is not None:
-        print(json.dumps(out), flush=True)
+        with os.fdopen(real_stdout, "w") as f:
+            f.write(json.dumps(out) + "\n")
 
 
 if __name__ == "__main__":
