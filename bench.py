@@ -106,6 +106,11 @@ def reference_time(n: int, chunk_bytes: int, seconds: float, mode: int = 1):
     return el / steps, steps, threads if mode else 1
 
 
+def dbg(msg: str) -> None:
+    if os.environ.get("BENCH_DEBUG"):
+        print(f"[bench {os.environ.get('RANK', '0')}] {msg}", file=sys.stderr, flush=True)
+
+
 def busbw_gbs(n: int, chunk_bytes: int, seconds: float) -> float:
     return 2.0 * n * (n - 1) * chunk_bytes / seconds / 1e9
 
@@ -217,11 +222,13 @@ def run_pat(args, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    dbg("warmup")
     for _ in range(args.warmup):
         for bs in sets:
             step(bs)
     barrier()
     comm.raise_async_error()
+    dbg("capture")
     # The timed loop replays CUDA graphs of the C-ABI calls (one AG and one RS graph per buffer
     # set): the launches are the library's own kernels, without Python/ctypes host overhead.
     graphs = []
@@ -236,10 +243,12 @@ def run_pat(args, rank, world, local):
                 comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
             graphs.append((ga, gr))
     stream.wait_stream(cap)
+    dbg("replay-warm")
     for ga, gr in graphs:
         ga.replay()
         gr.replay()
     barrier()
+    dbg("timed")
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     with ClockSampler(local) as clocks:
@@ -262,6 +271,25 @@ def run_pat(args, rank, world, local):
     ms_per_step = tot_ms / K
     value = busbw_gbs(n, C, ms_per_step / 1e3)
 
+    # ---- the same steps launched eagerly through the C ABI (apples-to-apples with NCCL eager)
+    KE = min(K, 100)
+    eev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(KE)]
+    barrier()
+    for k in range(KE):
+        bs = sets[k % S]
+        eev[k][0].record(stream)
+        comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
+        eev[k][1].record(stream)
+        comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
+        eev[k][2].record(stream)
+    barrier()
+    et = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in eev), sum(e[1].elapsed_time(e[2]) for e in eev)],
+                      dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    eager_us = {"all_gather": 1e3 * float(et[0]) / KE, "reduce_scatter": 1e3 * float(et[1]) / KE}
+
+    dbg("e2e")
     # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region
     h_ag_send = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(L)]
     h_rs_send = [torch.empty(n * elems, dtype=torch.float32).pin_memory() for _ in range(L)]
@@ -293,6 +321,7 @@ def run_pat(args, rank, world, local):
 
     # ---- NCCL Ring comparison (N > 1)
     nccl = None
+    dbg("nccl")
     if world > 1 and not args.no_nccl:
         for _ in range(args.warmup):
             for bs in sets:
@@ -301,7 +330,10 @@ def run_pat(args, rank, world, local):
         barrier()
         # same timing method as the PAT arm: graph replay when NCCL captures, else eager
         ngraphs, mode = [], "graph"
+        dbg("nccl-capture")
         try:
+            if not os.environ.get("BENCH_NCCL_GRAPH"):  # capturing many NCCL graphs hung on 2.28.9
+                raise RuntimeError("eager")
             cap2 = torch.cuda.Stream(dev)
             cap2.wait_stream(stream)
             with torch.cuda.stream(cap2):
@@ -405,7 +437,9 @@ def run_pat(args, rank, world, local):
                        "rounds": plan_ag["rounds"], "l2": f"inputs larger than L2: {S} rotating buffer sets, {S * step_bytes / 2**20:.0f} MiB total",
                        "timing": "CUDA events around CUDA-graph replays of the C-ABI calls, per step",
                        "plan_allgather": plan_ag, "plan_reduce_scatter": plan_rs},
-            "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K},
+            "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K,
+                           "timing": "graph replay"},
+            "latency_us_eager": dict(eager_us, timing="eager C-ABI calls, CUDA events per call"),
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host"},

@@ -43,7 +43,7 @@ constexpr size_t kFlagBytes = sizeof(uint64_t) * kMaxChannels * kFlagWords;  // 
 constexpr uint32_t kMagic = 0x50415442;                                       // "PATB"
 constexpr size_t kDefaultStepBytes = 256 << 10;  // inbox bytes per channel per pipeline step
 constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
-constexpr size_t kDefaultLL = 64 << 10;
+constexpr size_t kDefaultLL = 1 << 20;  // LL below: measured crossover 1-2 MiB at n=2 (graph mode)
 constexpr int kDefaultTimeoutMs = 20000;
 
 struct Compiled {
