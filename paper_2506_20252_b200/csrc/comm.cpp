@@ -163,7 +163,9 @@ void fill_defaults(patConfig_t* c, int n) {
   if (c->protocol == patProtoAuto && env_int("PAT_PROTOCOL", &v)) c->protocol = (int)v;
   if (c->threads <= 0) c->threads = env_int("PAT_THREADS", &v) ? (int)v : 512;
   c->threads = std::min(std::max(c->threads / 32 * 32, 64), 1024);
-  if (c->depth <= 0) c->depth = env_int("PAT_DEPTH", &v) ? (int)v : 2;
+  // one inbox buffer per PAT round of the full-aggregation schedule, plus one: the skewed
+  // sender keeps ceil(log2 n) steps in flight (kernels.cu, send_role)
+  if (c->depth <= 0) c->depth = env_int("PAT_DEPTH", &v) ? (int)v : ceil_log2(std::max(n, 2)) + 1;
   c->depth = std::min(std::max(c->depth, 1), 16);
   if (c->direct == 0 && env_int("PAT_DIRECT", &v)) c->direct = (int)v;
   if (c->fused == 0 && env_int("PAT_FUSED", &v)) c->fused = (int)v;
@@ -478,6 +480,11 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.slice_bytes = sl.slice;
     p.slot_stride = static_cast<int64_t>(comm->slot_bytes);
     p.depth = comm->cfg.depth;
+    {
+      long long sk = 1;
+      env_int("PAT_SKEW", &sk);
+      p.skew = (sk != 0 && p.proto == kProtoSimple && p.nrounds > 1 && p.depth >= p.nrounds) ? 1 : 0;
+    }
     p.chan_stride = static_cast<int64_t>(p.depth) * std::max(n - 1, 1) * p.slot_stride;
     p.send_warps = comm->cfg.send_warps;
     p.gpu_scope = single_device ? 1 : 0;

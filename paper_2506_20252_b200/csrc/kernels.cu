@@ -263,27 +263,25 @@ __device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Wait
   for (int k = 0; k < p.npeers; ++k) wait_flag(mine + 8 + (s.R + p.peers[k]) % p.n, s.g - p.depth + 1, w);
 }
 
-// SIMPLE sender role: pushes every round of step s (warps [0, send_warps)).
+// SIMPLE sender role, one PAT round of step s (warps [0, send_warps)). `waited` caches which
+// rounds' arrivals of this step were already acquired.
 template <int DT, int OP, int KIND>
-__device__ void send_step(const KPlan& p, const Step& s, Waiter& w, int tid, int nthr) {
+__device__ void send_round(const KPlan& p, const Step& s, int t, uint32_t& waited, Waiter& w, int tid, int nthr) {
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const char* snd = p.send[s.lr];
   char* out = p.recv[s.lr];
   const uint64_t* myflags = chan_flags(p, s.R, s.c);
   const bool gpu = p.gpu_scope;
-  uint32_t waited = 0;
-  auto ensure = [&](int t) {  // arrivals of round t (needed for forwarding)
-    if (!((waited >> t) & 1u)) {
-      if (tid == 0) wait_flag(myflags + t, s.g + 1, w);
+  auto ensure = [&](int tr) {  // arrivals of round tr (needed for forwarding)
+    if (!((waited >> tr) & 1u)) {
+      if (tid == 0) wait_flag(myflags + tr, s.g + 1, w);
       named_bar(1, nthr);
-      waited |= 1u << t;
+      waited |= 1u << tr;
     }
   };
-  if (tid == 0 && !p.direct) wait_credits(p, s, w);
-  named_bar(1, nthr);
   const char* srcs[kMaxArr + 1];
-  for (int t = 0; t < p.nrounds; ++t) {
+  {
     const KRound& r = p.rounds[t];
     const int P = (s.R + r.peer) % n;
     for (int pos = 0; pos < r.nchunks; ++pos) {
@@ -317,6 +315,37 @@ __device__ void send_step(const KPlan& p, const Step& s, Waiter& w, int tid, int
       st_relaxed(chan_flags(p, P, s.c) + t, s.g + 1, gpu);
     }
   }
+}
+
+// SIMPLE sender role over all steps. With p.skew, iteration k runs round t of step k - t
+// (oldest step first): a forward of round t waits for arrivals its upstream peer pushed one
+// iteration earlier, so the flag latency hides behind the next step's pushes (a wavefront
+// through the PAT tree). Needs depth > nrounds - 1 inbox buffers (host guarantees).
+template <int DT, int OP, int KIND>
+__device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, Waiter& w, int tid, int nthr,
+                          volatile uint64_t* sent_steps) {
+  const int NR = p.nrounds;
+  uint32_t waited[kMaxRounds] = {};
+  auto task = [&](int i, int t) {
+    const Step s = make_step(p, base, i, R, lr, c);
+    uint32_t& wm = waited[i % kMaxRounds];
+    if (t == 0) {  // first push of step i: the peers' buffers (g % depth) must be free
+      wm = 0;
+      if (tid == 0 && !p.direct) wait_credits(p, s, w);
+      named_bar(1, nthr);
+    }
+    send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr);
+    if (t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
+  };
+  if (p.skew) {
+    for (int k = 0; k < p.iters + NR - 1; ++k)
+      for (int t = NR - 1; t >= 0; --t)
+        if (k - t >= 0 && k - t < p.iters) task(k - t, t);
+  } else {
+    for (int i = 0; i < p.iters; ++i)
+      for (int t = 0; t < NR; ++t) task(i, t);
+  }
+  if (NR == 0 && tid == 0) *sent_steps = base + p.iters;
 }
 
 // SIMPLE receiver role: delivers (AG) or folds the output (RS) of step s, then — once the
@@ -482,11 +511,7 @@ __global__ void __launch_bounds__(1024) pat_kernel(const __grid_constant__ KPlan
   } else {
     const int nsend = p.send_warps * 32;
     if (static_cast<int>(threadIdx.x) < nsend) {
-      for (int i = 0; i < p.iters; ++i) {
-        const Step s = make_step(p, base, i, R, lr, c);
-        send_step<DT, OP, KIND>(p, s, w, threadIdx.x, nsend);
-        if (threadIdx.x == 0) s_sent = s.g + 1;  // after the group's last barrier of the step
-      }
+      send_role<DT, OP, KIND>(p, base, R, lr, c, w, threadIdx.x, nsend, &s_sent);
     } else {
       const int tid = threadIdx.x - nsend, nrecv = blockDim.x - nsend;
       for (int i = 0; i < p.iters; ++i) {

@@ -41,6 +41,7 @@ struct KPlan {
   int send_warps;   // SIMPLE: warps [0, send_warps) push, the rest deliver / fold
   int gpu_scope;    // all ranks on this device: flags and fences at .gpu scope instead of .sys
   int direct;       // AG: push straight into the peers' recvbufs (peer_recv), no inbox
+  int skew;         // SIMPLE sender runs round t of step k - t in iteration k (needs depth >= nrounds)
   int64_t chunk_bytes;   // bytes of one rank chunk (AG sendcount*esize, RS recvcount*esize)
   int64_t slice_bytes;   // payload bytes per slot per pipeline step
   int64_t slot_stride;   // inbox bytes per slot
