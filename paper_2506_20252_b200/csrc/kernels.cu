@@ -266,7 +266,8 @@ __device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Wait
 // SIMPLE sender role, one PAT round of step s (warps [0, send_warps)). `waited` caches which
 // rounds' arrivals of this step were already acquired.
 template <int DT, int OP, int KIND>
-__device__ void send_round(const KPlan& p, const Step& s, int t, uint32_t& waited, Waiter& w, int tid, int nthr) {
+__device__ void send_round(const KPlan& p, const Step& s, int t, uint32_t& waited, Waiter& w, int tid, int nthr,
+                           bool signal) {
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const char* snd = p.send[s.lr];
@@ -309,10 +310,12 @@ __device__ void send_round(const KPlan& p, const Step& s, int t, uint32_t& waite
       }
       grp_fold<DT, OP>(dst, srcs, m, s.len, p, tid, nthr);
     }
-    named_bar(1, nthr);
-    if (tid == 0) {
-      fence_acq_rel(gpu);
-      st_relaxed(chan_flags(p, P, s.c) + t, s.g + 1, gpu);
+    if (signal) {
+      named_bar(1, nthr);
+      if (tid == 0) {
+        fence_acq_rel(gpu);
+        st_relaxed(chan_flags(p, P, s.c) + t, s.g + 1, gpu);
+      }
     }
   }
 }
@@ -326,7 +329,7 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
                           volatile uint64_t* sent_steps) {
   const int NR = p.nrounds;
   uint32_t waited[kMaxRounds] = {};
-  auto task = [&](int i, int t) {
+  auto task = [&](int i, int t, bool signal) {
     const Step s = make_step(p, base, i, R, lr, c);
     uint32_t& wm = waited[i % kMaxRounds];
     if (t == 0) {  // first push of step i: the peers' buffers (g % depth) must be free
@@ -334,16 +337,28 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
       if (tid == 0 && !p.direct) wait_credits(p, s, w);
       named_bar(1, nthr);
     }
-    send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr);
-    if (t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
+    send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr, signal);
+    if (signal && t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
   };
   if (p.skew) {
-    for (int k = 0; k < p.iters + NR - 1; ++k)
+    // one fence per iteration: push every task of the wavefront, then release all its flags
+    for (int k = 0; k < p.iters + NR - 1; ++k) {
       for (int t = NR - 1; t >= 0; --t)
-        if (k - t >= 0 && k - t < p.iters) task(k - t, t);
+        if (k - t >= 0 && k - t < p.iters) task(k - t, t, false);
+      named_bar(1, nthr);
+      if (tid == 0) {
+        fence_acq_rel(p.gpu_scope);
+        for (int t = NR - 1; t >= 0; --t) {
+          const int i = k - t;
+          if (i < 0 || i >= p.iters) continue;
+          st_relaxed(chan_flags(p, (R + p.rounds[t].peer) % p.n, c) + t, base + i + 1, p.gpu_scope);
+          if (t == NR - 1) *sent_steps = base + i + 1;
+        }
+      }
+    }
   } else {
     for (int i = 0; i < p.iters; ++i)
-      for (int t = 0; t < NR; ++t) task(i, t);
+      for (int t = 0; t < NR; ++t) task(i, t, true);
   }
   if (NR == 0 && tid == 0) *sent_steps = base + p.iters;
 }

@@ -11,7 +11,7 @@ for f in sys.argv[1:]:
         t[(r["coll"], r["dtype"], r["bytes_per_rank"])][r["impl"]] = r
     for k in sorted(t):
         d = t[k]
-        p = d.get("pat")
+        p = d.get("pat") or next(v for kk, v in d.items() if kk.startswith("pat"))
         nc = next((v for kk, v in d.items() if kk.startswith("nccl")), None)
         s = f"{k[0]} {k[1]:4s} {k[2]:>11d} pat {p['us']:8.1f}us {p['busbw_gbs']:6.1f}GB/s"
         if "plan" in p:
