@@ -38,7 +38,7 @@ NVLINK_MEASURED_GBS = 770.0  # peer copy per direction (B200_PROFILING.md)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="pat", choices=["pat", "reference"])
     ap.add_argument("--chunk-bytes", type=int, default=CHUNK_BYTES)
@@ -153,7 +153,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.ok:
@@ -229,42 +229,48 @@ def run_pat(args, rank, world, local):
     barrier()
     comm.raise_async_error()
     dbg("capture")
-    # The timed loop replays CUDA graphs of the C-ABI calls (one AG and one RS graph per buffer
-    # set): the launches are the library's own kernels, without Python/ctypes host overhead.
-    graphs = []
-    cap = torch.cuda.Stream(dev)
-    cap.wait_stream(stream)
-    with torch.cuda.stream(cap):
-        for bs in sets:
-            ga, gr = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-            with torch.cuda.graph(ga, stream=cap):
-                comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
-            with torch.cuda.graph(gr, stream=cap):
-                comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
-            graphs.append((ga, gr))
-    stream.wait_stream(cap)
+    # The timed region replays ONE CUDA graph holding exactly K steps (step k = PAT all-gather +
+    # PAT reduce-scatter on buffer set k % S), captured from the C-ABI calls: the launches are
+    # the library's own kernels back to back, without Python/ctypes host gaps. Two more graphs
+    # of K all-gathers and K reduce-scatters give the per-collective latencies.
+    K = args.steps
+
+    def capture(kinds):
+        gph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(gph, stream=cap):
+                for k in range(K):
+                    bs = sets[k % S]
+                    if "ag" in kinds:
+                        comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
+                    if "rs" in kinds:
+                        comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
+        stream.wait_stream(cap)
+        return gph
+
+    g_step, g_ag, g_rs = capture(("ag", "rs")), capture(("ag",)), capture(("rs",))
     dbg("replay-warm")
-    for ga, gr in graphs:
-        ga.replay()
-        gr.replay()
+    for gph in (g_step, g_ag, g_rs):
+        gph.replay()
     barrier()
     dbg("timed")
-    K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+
+    def timed_replay(gph):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a.record(stream)
+        gph.replay()
+        b.record(stream)
+        barrier()
+        return a.elapsed_time(b)
+
     with ClockSampler(local) as clocks:
-        barrier()
-        for k in range(K):
-            ga, gr = graphs[k % S]
-            ev[k][0].record(stream)
-            ga.replay()
-            ev[k][1].record(stream)
-            gr.replay()
-            ev[k][2].record(stream)
-        barrier()
+        step_ms = timed_replay(g_step)
+    ag_ms, rs_ms = timed_replay(g_ag), timed_replay(g_rs)
     comm.raise_async_error()
-    ag_ms = sum(e[0].elapsed_time(e[1]) for e in ev)
-    rs_ms = sum(e[1].elapsed_time(e[2]) for e in ev)
-    tot = torch.tensor([ag_ms + rs_ms, ag_ms, rs_ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([step_ms, ag_ms, rs_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     tot_ms, ag_ms, rs_ms = (float(x) for x in tot.tolist())
@@ -435,10 +441,10 @@ def run_pat(args, rank, world, local):
             "config": {"workload": "BASELINE configs[0]: PAT AG + RS(sum), 1 MiB fp32 per rank",
                        "nranks": n, "placement": placement, "chunk_bytes": C, "trees": plan_ag["trees"],
                        "rounds": plan_ag["rounds"], "l2": f"inputs larger than L2: {S} rotating buffer sets, {S * step_bytes / 2**20:.0f} MiB total",
-                       "timing": "CUDA events around CUDA-graph replays of the C-ABI calls, per step",
+                       "timing": "CUDA events around one CUDA-graph replay of exactly K steps (captured C-ABI calls)",
                        "plan_allgather": plan_ag, "plan_reduce_scatter": plan_rs},
             "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K,
-                           "timing": "graph replay"},
+                           "timing": "graph of K back-to-back calls per collective"},
             "latency_us_eager": dict(eager_us, timing="eager C-ABI calls, CUDA events per call"),
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
