@@ -38,7 +38,7 @@ NVLINK_MEASURED_GBS = 770.0  # peer copy per direction (B200_PROFILING.md)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="pat", choices=["pat", "reference"])
     ap.add_argument("--chunk-bytes", type=int, default=CHUNK_BYTES)
@@ -268,7 +268,7 @@ def run_pat(args, rank, world, local):
 
     with ClockSampler(local) as clocks:
         step_ms = timed_replay(g_step)
-    ag_ms, rs_ms = timed_replay(g_ag), timed_replay(g_rs)
+        ag_ms, rs_ms = timed_replay(g_ag), timed_replay(g_rs)
     comm.raise_async_error()
     tot = torch.tensor([step_ms, ag_ms, rs_ms], dtype=torch.float64, device=dev)
     if world > 1:

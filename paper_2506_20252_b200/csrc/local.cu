@@ -64,50 +64,48 @@ __device__ __forceinline__ V tree(const V* x) {
   else return f(f(f(x[0], x[1]), f(x[3], x[2])), f(f(x[5], f(x[7], x[6])), x[4]));
 }
 
+// Grid: n groups of `bpr` blocks; group o (all-gather: origin, reduce-scatter: output rank)
+// walks its chunk in 16-byte units with U loads in flight per thread before any store.
+constexpr int kLocalThreads = 512;
+constexpr int kU = 4;
+
 // All-gather: unit u of origin o is read once and written to all n outputs.
-__global__ void __launch_bounds__(512) local_ag_kernel(const __grid_constant__ LPlan p) {
+__global__ void __launch_bounds__(kLocalThreads, 2) local_ag_kernel(const __grid_constant__ LPlan p) {
   const int n = p.n;
+  const int bpr = gridDim.x / n;
+  const int o = blockIdx.x / bpr;
+  const int b = blockIdx.x - o * bpr;
   const int64_t Cb = p.chunk_bytes;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const char* src = p.send[o];
+  const int skip = (p.recv[o] + o * Cb == src) ? o : -1;  // in place: rank o's own block is there
   if (p.vec == 16) {
     const int64_t nu = Cb >> 4;
-    const int64_t total = nu * n;
-    constexpr int U = 4;
-    int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (; i + (U - 1) * stride < total; i += U * stride) {
-      uint4 v[U];
-      int64_t o[U], u[U];
+    const int64_t step = static_cast<int64_t>(bpr) * blockDim.x;
+    int64_t u = static_cast<int64_t>(b) * blockDim.x + threadIdx.x;
+    for (; u + (kU - 1) * step < nu; u += kU * step) {
+      uint4 v[kU];
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        o[k] = (i + k * stride) / nu;
-        u[k] = (i + k * stride) - o[k] * nu;
-        v[k] = ld_nc16(p.send[o[k]] + 16 * u[k]);
-      }
-      for (int r = 0; r < n; ++r)
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          char* dst = p.recv[r] + o[k] * Cb + 16 * u[k];
-          if (dst != p.send[o[k]] + 16 * u[k]) st_cs16(dst, v[k]);
-        }
-    }
-    for (; i < total; i += stride) {
-      const int64_t o = i / nu, u = i - o * nu;
-      const uint4 v = ld_nc16(p.send[o] + 16 * u);
+      for (int k = 0; k < kU; ++k) v[k] = ld_nc16(src + 16 * (u + k * step));
       for (int r = 0; r < n; ++r) {
+        if (r == skip) continue;
         char* dst = p.recv[r] + o * Cb + 16 * u;
-        if (dst != p.send[o] + 16 * u) st_cs16(dst, v);
+#pragma unroll
+        for (int k = 0; k < kU; ++k) st_cs16(dst + 16 * k * step, v[k]);
       }
+    }
+    for (; u < nu; u += step) {
+      const uint4 v = ld_nc16(src + 16 * u);
+      for (int r = 0; r < n; ++r)
+        if (r != skip) st_cs16(p.recv[r] + o * Cb + 16 * u, v);
     }
   } else {
     const int es = p.esize;
-    const int64_t ne = Cb / es, total = ne * n;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-      const int64_t o = i / ne, e = i - o * ne;
-      const uint64_t v = ld_elem(p.send[o] + e * es, es);
-      for (int r = 0; r < n; ++r) {
-        char* dst = p.recv[r] + o * Cb + e * es;
-        if (dst != p.send[o] + e * es) st_elem(dst, v, es);
-      }
+    const int64_t ne = Cb / es;
+    for (int64_t e = static_cast<int64_t>(b) * blockDim.x + threadIdx.x; e < ne;
+         e += static_cast<int64_t>(bpr) * blockDim.x) {
+      const uint64_t v = ld_elem(src + e * es, es);
+      for (int r = 0; r < n; ++r)
+        if (r != skip) st_elem(p.recv[r] + o * Cb + e * es, v, es);
     }
   }
 }
@@ -115,35 +113,38 @@ __global__ void __launch_bounds__(512) local_ag_kernel(const __grid_constant__ L
 // Reduce-scatter: out[r] = tree(x_0..x_{n-1}), x_j = send[(r+j) % n] block r.
 template <int DT, int OP, int N>
 __device__ __forceinline__ void local_rs_body(const LPlan& p) {
+  const int bpr = gridDim.x / N;
+  const int r = blockIdx.x / bpr;
+  const int b = blockIdx.x - r * bpr;
   const int64_t Cb = p.chunk_bytes;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const char* src[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) src[j] = p.send[(r + j) % N] + r * Cb;
+  char* dst = p.recv[r];
   if (p.vec == 16) {
-    const int64_t nu = Cb >> 4, total = nu * N;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-      const int r = static_cast<int>(i / nu);
-      const int64_t u = i - static_cast<int64_t>(r) * nu;
+    const int64_t nu = Cb >> 4;
+    const int64_t step = static_cast<int64_t>(bpr) * blockDim.x;
+    for (int64_t u = static_cast<int64_t>(b) * blockDim.x + threadIdx.x; u < nu; u += step) {
       uint4 x[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) x[j] = ld_nc16(p.send[(r + j) % N] + r * Cb + 16 * u);
-      st_cs16(p.recv[r] + 16 * u, tree<DT, OP, N>(x));
+      for (int j = 0; j < N; ++j) x[j] = ld_nc16(src[j] + 16 * u);
+      st_cs16(dst + 16 * u, tree<DT, OP, N>(x));
     }
   } else {
     using S = typename DType<DT>::S;
-    const int64_t ne = Cb / static_cast<int64_t>(sizeof(S)), total = ne * N;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-      const int r = static_cast<int>(i / ne);
-      const int64_t e = i - static_cast<int64_t>(r) * ne;
+    const int64_t ne = Cb / static_cast<int64_t>(sizeof(S));
+    for (int64_t e = static_cast<int64_t>(b) * blockDim.x + threadIdx.x; e < ne;
+         e += static_cast<int64_t>(bpr) * blockDim.x) {
       S x[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j)
-        x[j] = *reinterpret_cast<const S*>(p.send[(r + j) % N] + r * Cb + e * static_cast<int64_t>(sizeof(S)));
-      *reinterpret_cast<S*>(p.recv[r] + e * static_cast<int64_t>(sizeof(S))) = tree_scalar<DT, OP, N>(x);
+      for (int j = 0; j < N; ++j) x[j] = *reinterpret_cast<const S*>(src[j] + e * static_cast<int64_t>(sizeof(S)));
+      *reinterpret_cast<S*>(dst + e * static_cast<int64_t>(sizeof(S))) = tree_scalar<DT, OP, N>(x);
     }
   }
 }
 
 template <int DT, int OP>
-__global__ void __launch_bounds__(512) local_rs_kernel(const __grid_constant__ LPlan p) {
+__global__ void __launch_bounds__(kLocalThreads, 2) local_rs_kernel(const __grid_constant__ LPlan p) {
   switch (p.n) {
     case 1: local_rs_body<DT, OP, 1>(p); break;
     case 2: local_rs_body<DT, OP, 2>(p); break;
@@ -191,12 +192,12 @@ cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize,
     p.send[r] = send_by_rank[r];
     p.recv[r] = recv_by_rank[r];
   }
-  const int threads = 512;
-  const int64_t units = vec == 16 ? (chunk_bytes >> 4) * n : (chunk_bytes / esize) * n;
-  const int64_t want = (units + threads - 1) / threads;
-  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 4LL * sm_count)));
-  if (kind == 0) local_ag_kernel<<<blocks, threads, 0, stream>>>(p);
-  else kLocalRs[dtype][op]<<<blocks, threads, 0, stream>>>(p);
+  // per rank: enough blocks for ~2 resident CTAs on every SM overall, no more than the units
+  const int64_t per_rank_units = vec == 16 ? (chunk_bytes >> 4) : (chunk_bytes / esize);
+  const int64_t want = (per_rank_units + kLocalThreads - 1) / kLocalThreads;
+  const int bpr = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (4LL * sm_count + n - 1) / n)));
+  if (kind == 0) local_ag_kernel<<<bpr * n, kLocalThreads, 0, stream>>>(p);
+  else kLocalRs[dtype][op]<<<bpr * n, kLocalThreads, 0, stream>>>(p);
   return cudaGetLastError();
 }
 
