@@ -38,7 +38,7 @@ NVLINK_MEASURED_GBS = 770.0  # peer copy per direction (B200_PROFILING.md)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=10000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="pat", choices=["pat", "reference"])
     ap.add_argument("--chunk-bytes", type=int, default=CHUNK_BYTES)
@@ -234,14 +234,15 @@ def run_pat(args, rank, world, local):
     # the library's own kernels back to back, without Python/ctypes host gaps. Two more graphs
     # of K all-gathers and K reduce-scatters give the per-collective latencies.
     K = args.steps
+    G = min(K, 1000)  # steps per graph; the timed region replays it K // G times (+ a remainder graph)
 
-    def capture(kinds):
+    def capture(kinds, count):
         gph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream(dev)
         cap.wait_stream(stream)
         with torch.cuda.stream(cap):
             with torch.cuda.graph(gph, stream=cap):
-                for k in range(K):
+                for k in range(count):
                     bs = sets[k % S]
                     if "ag" in kinds:
                         comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
@@ -250,25 +251,33 @@ def run_pat(args, rank, world, local):
         stream.wait_stream(cap)
         return gph
 
-    g_step, g_ag, g_rs = capture(("ag", "rs")), capture(("ag",)), capture(("rs",))
+    rem = K % G
+    graphs = {kinds: (capture(kinds, G), capture(kinds, rem) if rem else None)
+              for kinds in (("ag", "rs"), ("ag",), ("rs",))}
     dbg("replay-warm")
-    for gph in (g_step, g_ag, g_rs):
-        gph.replay()
+    for full, part in graphs.values():
+        full.replay()
+        if part is not None:
+            part.replay()
     barrier()
     dbg("timed")
 
-    def timed_replay(gph):
+    def timed_replay(kinds):
+        full, part = graphs[kinds]
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         a.record(stream)
-        gph.replay()
+        for _ in range(K // G):  # exactly K steps: K // G replays of G steps + the remainder
+            full.replay()
+        if part is not None:
+            part.replay()
         b.record(stream)
         barrier()
         return a.elapsed_time(b)
 
     with ClockSampler(local) as clocks:
-        step_ms = timed_replay(g_step)
-        ag_ms, rs_ms = timed_replay(g_ag), timed_replay(g_rs)
+        step_ms = timed_replay(("ag", "rs"))
+        ag_ms, rs_ms = timed_replay(("ag",)), timed_replay(("rs",))
     comm.raise_async_error()
     tot = torch.tensor([step_ms, ag_ms, rs_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -357,8 +366,9 @@ def run_pat(args, rank, world, local):
         except Exception:
             mode, ngraphs = "eager", []
         barrier()
-        nev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
-        for k in range(K):
+        KN = min(K, 1000)
+        nev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(KN)]
+        for k in range(KN):
             bs = sets[k % S]
             nev[k][0].record(stream)
             if ngraphs:
@@ -376,9 +386,9 @@ def run_pat(args, rank, world, local):
                            sum(e[1].elapsed_time(e[2]) for e in nev)], dtype=torch.float64, device=dev)
         dist.all_reduce(nt, op=dist.ReduceOp.MAX)
         nt = nt.tolist()
-        nccl = {"algo": os.environ.get("NCCL_ALGO"), "ms_per_step": nt[0] / K,
-                "busbw_gbs": busbw_gbs(n, C, nt[0] / K / 1e3),
-                "ag_us": 1e3 * nt[1] / K, "rs_us": 1e3 * nt[2] / K,
+        nccl = {"algo": os.environ.get("NCCL_ALGO"), "ms_per_step": nt[0] / KN,
+                "busbw_gbs": busbw_gbs(n, C, nt[0] / KN / 1e3),
+                "ag_us": 1e3 * nt[1] / KN, "rs_us": 1e3 * nt[2] / KN,
                 "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()), "timing": mode}
 
     # ---- roofline of the dominant kernel
@@ -441,7 +451,7 @@ def run_pat(args, rank, world, local):
             "config": {"workload": "BASELINE configs[0]: PAT AG + RS(sum), 1 MiB fp32 per rank",
                        "nranks": n, "placement": placement, "chunk_bytes": C, "trees": plan_ag["trees"],
                        "rounds": plan_ag["rounds"], "l2": f"inputs larger than L2: {S} rotating buffer sets, {S * step_bytes / 2**20:.0f} MiB total",
-                       "timing": "CUDA events around one CUDA-graph replay of exactly K steps (captured C-ABI calls)",
+                       "timing": "CUDA events around CUDA-graph replays of exactly K steps (captured C-ABI calls)",
                        "plan_allgather": plan_ag, "plan_reduce_scatter": plan_rs},
             "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K,
                            "timing": "graph of K back-to-back calls per collective"},
