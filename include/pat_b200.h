@@ -165,6 +165,12 @@ patResult_t patCommDestroy(patComm_t comm);
 patResult_t patCommCount(patComm_t comm, int* nranks);
 /* Ranks driven by this communicator, in the order the array arguments use. */
 patResult_t patCommLocalRanks(patComm_t comm, int* nlocal, int* ranks, int* devices);
+/* Device event trace of the last transport launch on device group `group` (communicators
+ * created with PAT_TRACE=<entries per CTA role> in the environment). Layout: ctas x 2 roles
+ * (push, deliver) x entries x {globaltimer ns, code}; code bits 56..63 event, 40..55 step,
+ * 32..39 round. Synchronises the device. */
+patResult_t patCommTraceRead(patComm_t comm, int group, void* host, size_t cap, size_t* out_bytes, int* ctas,
+                             int* entries);
 /* Device-reported asynchronous error (timeouts); readable without synchronising. */
 patResult_t patCommGetAsyncError(patComm_t comm, patResult_t* async_error);
 patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDataType_t dtype,

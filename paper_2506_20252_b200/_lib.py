@@ -99,7 +99,7 @@ SYMBOLS = [
     "patCommLocalRanks", "patCommGetAsyncError", "patCommPlan", "patAllGather",
     "patReduceScatter", "patAllGatherSchedule", "patReduceScatterSchedule", "patScheduleBuild",
     "patScheduleMirror", "patScheduleValidate", "patScheduleStats", "patScheduleTraceCsv",
-    "patMaxTrees", "patTreesFromBuffer", "patPatBufferSlots", "patRoundCountFormula",
+    "patMaxTrees", "patTreesFromBuffer", "patPatBufferSlots", "patRoundCountFormula", "patCommTraceRead",
 ]
 
 _lib = None
@@ -145,6 +145,7 @@ def lib() -> ctypes.CDLL:
         L.patTreesFromBuffer.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, IP]
         L.patPatBufferSlots.argtypes = [ctypes.c_int, ctypes.c_int, IP]
         L.patRoundCountFormula.argtypes = [ctypes.c_int, ctypes.c_int, IP]
+        L.patCommTraceRead.argtypes = [VP, ctypes.c_int, VP, ctypes.c_size_t, SZP, IP, IP]
         _lib = L
     return _lib
 

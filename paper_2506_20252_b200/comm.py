@@ -182,6 +182,18 @@ class PatComm:
                                 ctypes.byref(info)), "patCommPlan")
         return info.as_dict()
 
+    def trace(self, group: int = 0):
+        """Device event trace of the last transport launch (PAT_TRACE=<entries> at init).
+        Returns a numpy array [ctas, 2 roles, entries, 2] of (globaltimer ns, code)."""
+        import numpy as np
+
+        nb, ctas, ent = ctypes.c_size_t(), ctypes.c_int(), ctypes.c_int()
+        lib().patCommTraceRead(self._h, group, None, 0, ctypes.byref(nb), ctypes.byref(ctas), ctypes.byref(ent))
+        buf = np.zeros(nb.value // 8, np.uint64)
+        check(lib().patCommTraceRead(self._h, group, buf.ctypes.data, nb.value, ctypes.byref(nb),
+                                     ctypes.byref(ctas), ctypes.byref(ent)), "patCommTraceRead")
+        return buf.reshape(ctas.value, 2, ent.value, 2)
+
     def async_error(self) -> int:
         e = ctypes.c_int()
         check(lib().patCommGetAsyncError(self._h, ctypes.byref(e)), "patCommGetAsyncError")

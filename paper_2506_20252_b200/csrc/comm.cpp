@@ -58,6 +58,9 @@ struct DevGroup {
   int device = 0;
   std::vector<int> lidx;           // local indices on this device
   uint64_t* iter_state = nullptr;  // [lidx.size()][kMaxChannels]
+  uint64_t* trace = nullptr;       // PAT_TRACE: [lidx.size() * kMaxChannels][2 roles][cap][2]
+  int trace_cap = 0;
+  int trace_ctas = 0;              // CTAs of the last traced launch
   int sm_count = 0;
   std::array<char*, kMaxRanks> pool_view{};  // every rank's pool as seen from this device
 };
@@ -411,6 +414,13 @@ patResult_t setup_groups(patComm* comm) {
     const size_t bytes = sizeof(uint64_t) * kMaxChannels * g.lidx.size();
     CUDA_TRY(cudaMalloc(&g.iter_state, bytes));
     CUDA_TRY(cudaMemset(g.iter_state, 0, bytes));
+    long long tcap = 0;
+    if (env_int("PAT_TRACE", &tcap) && tcap > 0) {  // device event trace for tools/trace.py
+      g.trace_cap = static_cast<int>(std::min<long long>(tcap, 4096));
+      const size_t tb = sizeof(uint64_t) * 2 * 2 * g.trace_cap * kMaxChannels * g.lidx.size();
+      CUDA_TRY(cudaMalloc(&g.trace, tb));
+      CUDA_TRY(cudaMemset(g.trace, 0, tb));
+    }
   }
   comm->events.resize(comm->lranks.size());
   for (size_t l = 0; l < comm->lranks.size(); ++l) {
@@ -497,6 +507,13 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       for (size_t l = 0; l < comm->lranks.size(); ++l) p.peer_recv[comm->lranks[l]] = static_cast<char*>(recvbuffs[l]);
     p.timeout_ns = static_cast<uint64_t>(comm->cfg.timeout_ms) * 1000000ull;
     p.err = comm->err_dev;
+    p.trace = g.trace;
+    p.trace_cap = g.trace_cap;
+    if (g.trace) {
+      g.trace_ctas = p.nlocal * p.channels;
+      CUDA_TRY(cudaMemsetAsync(g.trace, 0, sizeof(uint64_t) * 4 * g.trace_cap * g.trace_ctas,
+                               streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr));
+    }
     for (int r = 0; r < n; ++r) {
       p.flags[r] = reinterpret_cast<uint64_t*>(g.pool_view[r]);
       p.inbox[r] = g.pool_view[r] + kFlagBytes;
@@ -700,6 +717,7 @@ patResult_t patCommDestroy(patComm_t comm) {
       for (void* p : comm->ipc_opened) cudaIpcCloseMemHandle(p);
       comm->ipc_opened.clear();
       if (g.iter_state) cudaFree(g.iter_state);
+      if (g.trace) cudaFree(g.trace);
     }
     for (size_t l = 0; l < comm->owned_pool.size(); ++l) {
       cudaSetDevice(comm->ldevs[l]);
@@ -726,6 +744,23 @@ patResult_t patCommLocalRanks(patComm_t comm, int* nlocal, int* ranks, int* devi
     if (ranks) ranks[l] = comm->lranks[l];
     if (devices) devices[l] = comm->ldevs[l];
   }
+  return patSuccess;
+}
+
+patResult_t patCommTraceRead(patComm_t comm, int group, void* host, size_t cap, size_t* out_bytes, int* ctas,
+                             int* entries) {
+  if (!comm || group < 0 || group >= static_cast<int>(comm->groups.size())) return patInvalidArgument;
+  DevGroup& g = comm->groups[group];
+  if (!g.trace) return patInvalidUsage;  // set PAT_TRACE=<entries> before creating the communicator
+  const size_t bytes = sizeof(uint64_t) * 4 * g.trace_cap * g.trace_ctas;
+  if (out_bytes) *out_bytes = bytes;
+  if (ctas) *ctas = g.trace_ctas;
+  if (entries) *entries = g.trace_cap;
+  if (!host || cap < bytes) return patCapacity;
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(g.device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(host, g.trace, bytes, cudaMemcpyDeviceToHost));
   return patSuccess;
 }
 

@@ -102,6 +102,31 @@ struct Waiter {
   bool gpu;  // flag scope
 };
 
+// ------------------------------------------------------------------------- device trace
+// Event codes (bits 56..63 event, 40..55 step, 32..39 round); one writer thread per role.
+enum TraceEv : uint64_t {
+  kEvStart = 1, kEvCredit = 2, kEvPushed = 3, kEvFenced = 4, kEvArrived = 5, kEvDelivered = 6, kEvDone = 7,
+  kEvEnd = 8, kEvWaitArr = 9
+};
+
+struct Tracer {
+  uint64_t* buf = nullptr;
+  int cap = 0, n = 0;
+  __device__ __forceinline__ void init(const KPlan& p, int role) {
+    if (p.trace) {
+      buf = p.trace + (static_cast<int64_t>(blockIdx.x) * 2 + role) * p.trace_cap * 2;
+      cap = p.trace_cap;
+    }
+  }
+  __device__ __forceinline__ void rec(uint64_t ev, uint64_t step, int round) {
+    if (buf && n < cap) {
+      buf[2 * n] = globaltimer();
+      buf[2 * n + 1] = (ev << 56) | ((step & 0xffff) << 40) | (static_cast<uint64_t>(round & 0xff) << 32);
+      ++n;
+    }
+  }
+};
+
 __device__ __noinline__ void report_timeout(Waiter& w) {
   if (!w.aborted) {
     atomicCAS_system(w.err, 0, 40 /* patTimeout */);
@@ -329,15 +354,20 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
                           volatile uint64_t* sent_steps) {
   const int NR = p.nrounds;
   uint32_t waited[kMaxRounds] = {};
+  Tracer tr;
+  if (tid == 0) tr.init(p, 0);
+  tr.rec(kEvStart, base, 0);
   auto task = [&](int i, int t, bool signal) {
     const Step s = make_step(p, base, i, R, lr, c);
     uint32_t& wm = waited[i % kMaxRounds];
     if (t == 0) {  // first push of step i: the peers' buffers (g % depth) must be free
       wm = 0;
       if (tid == 0 && !p.direct) wait_credits(p, s, w);
+      tr.rec(kEvCredit, s.g, 0);
       named_bar(1, nthr);
     }
     send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr, signal);
+    tr.rec(kEvPushed, s.g, t);
     if (signal && t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
   };
   if (p.skew) {
@@ -348,6 +378,7 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
       named_bar(1, nthr);
       if (tid == 0) {
         fence_acq_rel(p.gpu_scope);
+        tr.rec(kEvFenced, base + k, 0);
         for (int t = NR - 1; t >= 0; --t) {
           const int i = k - t;
           if (i < 0 || i >= p.iters) continue;
@@ -361,13 +392,14 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
       for (int t = 0; t < NR; ++t) task(i, t, true);
   }
   if (NR == 0 && tid == 0) *sent_steps = base + p.iters;
+  tr.rec(kEvEnd, base + p.iters, 0);
 }
 
 // SIMPLE receiver role: delivers (AG) or folds the output (RS) of step s, then — once the
 // sender role is also done with this step's inbox — publishes done(g) to every rank.
 template <int DT, int OP, int KIND>
 __device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int nthr,
-                          volatile uint64_t* sent_steps) {
+                          volatile uint64_t* sent_steps, Tracer& tr) {
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const char* snd = p.send[s.lr];
@@ -383,6 +415,7 @@ __device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int
   }
   for (int t = 0; t < p.nrounds; ++t) {
     if (tid == 0) wait_flag(myflags + t, s.g + 1, w);
+    tr.rec(kEvArrived, s.g, t);
     named_bar(2, nthr);
     if constexpr (KIND == kAG) {
       if (!p.direct) {
@@ -413,6 +446,7 @@ __device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int
       }
     }
   }
+  tr.rec(kEvDelivered, s.g, 0);
   named_bar(2, nthr);
   if (tid < n && tid != s.R) st_release(chan_flags(p, tid, s.c) + 8 + s.R, s.g + 1, gpu);
 }
@@ -529,10 +563,14 @@ __global__ void __launch_bounds__(1024) pat_kernel(const __grid_constant__ KPlan
       send_role<DT, OP, KIND>(p, base, R, lr, c, w, threadIdx.x, nsend, &s_sent);
     } else {
       const int tid = threadIdx.x - nsend, nrecv = blockDim.x - nsend;
+      Tracer tr;
+      if (tid == 0) tr.init(p, 1);
+      tr.rec(kEvStart, base, 0);
       for (int i = 0; i < p.iters; ++i) {
         const Step s = make_step(p, base, i, R, lr, c);
-        recv_step<DT, OP, KIND>(p, s, w, tid, nrecv, &s_sent);
+        recv_step<DT, OP, KIND>(p, s, w, tid, nrecv, &s_sent, tr);
       }
+      tr.rec(kEvEnd, base + p.iters, 0);
     }
   }
   __syncthreads();

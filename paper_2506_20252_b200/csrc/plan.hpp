@@ -64,6 +64,9 @@ struct KPlan {
   char* peer_recv[kMaxRanks];       // direct mode: every rank's recvbuf as seen from this device
   uint64_t* flags[kMaxRanks];       // [kMaxChannels][kFlagWords]
   int* err;                         // mapped pinned host word (first async error)
+  // optional device trace (PAT_TRACE=1): per (CTA, role) ring of {globaltimer ns, event code}
+  uint64_t* trace;
+  int trace_cap;                    // entries per (CTA, role)
 };
 
 }  // namespace pat

@@ -1,0 +1,84 @@
+"""Device event trace of one transport call per rank (diagnostics).
+
+  PAT_TRACE=64 torchrun --nproc-per-node 4 --master-addr 127.0.0.1 tools/trace_run.py --bytes 16777216 --coll ag
+
+Writes gpurun_out/trace_<coll>_<bytes>_r<rank>.npz (ctas x 2 roles x entries x {ns, code}) and
+prints, for rank 0, a timeline summary: per event type, the min / median / max time (us) from
+the kernel's first event, over CTAs.
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+EV = {1: "start", 2: "credit", 3: "pushed", 4: "fenced", 5: "arrived", 6: "delivered", 7: "done", 8: "end"}
+
+
+def summarize(tr):
+    import numpy as np
+
+    t0 = None
+    rows = {}
+    for c in range(tr.shape[0]):
+        for role in range(2):
+            for e in range(tr.shape[2]):
+                ns, code = int(tr[c, role, e, 0]), int(tr[c, role, e, 1])
+                if ns == 0:
+                    continue
+                t0 = ns if t0 is None else min(t0, ns)
+                ev, step, rnd = code >> 56, (code >> 40) & 0xFFFF, (code >> 32) & 0xFF
+                rows.setdefault((role, EV.get(ev, ev), rnd), []).append((ns, step))
+    out = []
+    for (role, ev, rnd), v in sorted(rows.items(), key=lambda kv: min(x[0] for x in kv[1])):
+        ts = np.array([x[0] - t0 for x in v]) / 1e3
+        out.append(f"{'push' if role == 0 else 'recv'} {ev:9s} r{rnd} n={len(ts):5d}  min {ts.min():8.2f}  "
+                   f"med {np.median(ts):8.2f}  max {ts.max():8.2f} us")
+    return "\n".join(out)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bytes", type=int, default=16 << 20)
+    ap.add_argument("--coll", default="ag")
+    ap.add_argument("--warmup", type=int, default=5)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_20252_b200 import FLOAT32, SUM, PatComm
+
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = PatComm.from_process_group(device=local)
+    n, elems = world, args.bytes // 4
+    if args.coll == "ag":
+        s, r = torch.ones(elems, device=dev), torch.empty(n * elems, device=dev)
+        fn = lambda: comm.all_gather([s], [r], elems, FLOAT32)
+    else:
+        s, r = torch.ones(n * elems, device=dev), torch.empty(elems, device=dev)
+        fn = lambda: comm.reduce_scatter([s], [r], elems, FLOAT32, SUM)
+    for _ in range(args.warmup):
+        fn()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    fn()
+    torch.cuda.synchronize(dev)
+    tr = comm.trace()
+    os.makedirs("gpurun_out", exist_ok=True)
+    np.savez_compressed(f"gpurun_out/trace_{args.coll}_{args.bytes}_r{rank}.npz", trace=tr,
+                        plan=str(comm.plan(0 if args.coll == "ag" else 1, elems, FLOAT32)))
+    if rank == 0:
+        print(comm.plan(0 if args.coll == "ag" else 1, elems, FLOAT32))
+        print(summarize(tr))
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
