@@ -497,7 +497,12 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     {
       long long sk = 1;
       env_int("PAT_SKEW", &sk);
-      p.skew = (sk != 0 && p.proto == kProtoSimple && p.nrounds > 1 && p.depth >= p.nrounds) ? 1 : 0;
+      // skew distance L: the sender keeps (nrounds-1)*L+1 steps in flight -> needs that many buffers
+      const int L = static_cast<int>(std::max(0LL, sk));
+      p.skew = (L > 0 && p.proto == kProtoSimple && p.nrounds > 1 && p.depth >= (p.nrounds - 1) * L + 1 &&
+                (p.nrounds - 1) * L + 1 <= kMaxRounds)
+                   ? L
+                   : 0;
     }
     p.chan_stride = static_cast<int64_t>(p.depth) * std::max(n - 1, 1) * p.slot_stride;
     p.send_warps = comm->cfg.send_warps;

@@ -371,16 +371,19 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
     if (signal && t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
   };
   if (p.skew) {
-    // one fence per iteration: push every task of the wavefront, then release all its flags
-    for (int k = 0; k < p.iters + NR - 1; ++k) {
-      for (int t = NR - 1; t >= 0; --t)
-        if (k - t >= 0 && k - t < p.iters) task(k - t, t, false);
+    // Round t of step k - t*L in iteration k (L = p.skew): the newest step's independent
+    // round 0 goes first, forwards of older steps after it, then ONE fence for the iteration
+    // and all of its flags.
+    const int L = p.skew;
+    for (int k = 0; k < p.iters + (NR - 1) * L; ++k) {
+      for (int t = 0; t < NR; ++t)
+        if (k - t * L >= 0 && k - t * L < p.iters) task(k - t * L, t, false);
       named_bar(1, nthr);
       if (tid == 0) {
         fence_acq_rel(p.gpu_scope);
         tr.rec(kEvFenced, base + k, 0);
         for (int t = NR - 1; t >= 0; --t) {
-          const int i = k - t;
+          const int i = k - t * L;
           if (i < 0 || i >= p.iters) continue;
           st_relaxed(chan_flags(p, (R + p.rounds[t].peer) % p.n, c) + t, base + i + 1, p.gpu_scope);
           if (t == NR - 1) *sent_steps = base + i + 1;
