@@ -138,7 +138,7 @@ def main():
                 rec = {"coll": coll, "impl": "pat", "n": n, "gpus": world, "dtype": dname,
                        "bytes_per_rank": elems * es, "us": us,
                        "busbw_gbs": (n - 1) * elems * es / (us * 1e-6) / 1e9,
-                       "plan": comm.plan(0 if coll == "ag" else 1, elems, pdt)}
+                       "plan": comm.plan(0 if coll == "ag" else 1, elems, pdt), "forced": args.protocol}
                 if out:
                     out.write(json.dumps(rec) + "\n")
                     out.flush()

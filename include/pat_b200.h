@@ -93,7 +93,12 @@ typedef enum { patSum = 0, patProd = 1, patMax = 2, patMin = 3, patNumOps = 4 } 
 typedef enum { patAllGatherKind = 0, patReduceScatterKind = 1 } patCollKind_t;
 typedef enum { patAlgoRing = 0, patAlgoBruckNearest = 1, patAlgoBruckFarthest = 2,
                patAlgoRecursiveDoubling = 3, patAlgoPat = 4 } patAlgorithm_t;
-typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2 } patProtocol_t;
+/* LL: flag-in-line stores for small chunks. SIMPLE: pushed slices through the peers' inbox pools.
+   PULL: receivers read the upstream's buffers (user sendbuf / recvbuf, staged RS partials);
+   needs every rank's user buffers mapped in this process (patCommInitAll, cudaMalloc memory).
+   LL128: 128-byte lines carrying 120 payload bytes and a flag word (mid-size chunks).
+   Auto: LL up to ll_threshold, LL128 up to ll128_threshold, then PULL where possible, else SIMPLE. */
+typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3, patProtoLL128 = 4 } patProtocol_t;
 
 typedef struct {
   size_t size;              /* sizeof(patConfig_t) */
@@ -113,11 +118,13 @@ typedef struct {
   int fused;                /* all ranks on one device: -1 = run the transport kernel anyway,
                                0 = fused single-device executor (one read of every input, one
                                write of every output, same fold tree as the schedule) */
+  size_t ll128_threshold;   /* per-rank chunk bytes up to which LL128 is used (above ll_threshold);
+                               0 = default */
 } patConfig_t;
 
 /* Plan the library would launch for one call (introspection / benchmarks). */
 typedef struct {
-  int protocol;             /* patProtoLL or patProtoSimple */
+  int protocol;             /* patProtoLL, patProtoLL128, patProtoSimple or patProtoPull */
   int trees;
   int rounds;               /* PAT rounds (= sync steps) */
   int channels;             /* CTAs per rank */

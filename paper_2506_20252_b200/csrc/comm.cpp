@@ -45,6 +45,9 @@ constexpr size_t kDefaultPoolBytes = 512ull << 20;  // inbox pool budget per ran
 constexpr size_t kMinSlice = 64 << 10, kMaxSlice = 256 << 10;
 constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
 constexpr size_t kDefaultLL = 1 << 20;  // LL below: measured crossover 1-2 MiB at n=2 (graph mode)
+constexpr size_t kDefaultLL128 = 1 << 20;  // LL128 for (ll_threshold, this]
+constexpr size_t kLLSlotBytes = 16 << 10;  // LL / LL128 slot: 8 KiB / 15 KiB payload per channel-step
+constexpr int64_t kLL128PayloadBytes = 120;  // per 128-byte line (transport.cuh)
 constexpr int kDefaultTimeoutMs = 20000;
 
 struct Compiled {
@@ -93,6 +96,9 @@ struct patComm {
   std::vector<DevGroup> groups;
   std::vector<void*> ipc_opened;
   size_t slot_bytes = 0, pool_bytes = 0;
+  size_t ll_slot_bytes = 0;                // LL / LL128 inbox slot (own regions, see common_init)
+  size_t region_off[5] = {};               // inbox region of each protocol within a pool
+  int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
   int channels = 0;
   int* err_host = nullptr;
   int* err_dev = nullptr;
@@ -177,6 +183,7 @@ void fill_defaults(patConfig_t* c, int n) {
     c->slice_bytes = s;
   }
   if (c->ll_threshold == 0) c->ll_threshold = env_int("PAT_LL_THRESHOLD", &v) ? (size_t)v : kDefaultLL;
+  if (c->ll128_threshold == 0) c->ll128_threshold = env_int("PAT_LL128_THRESHOLD", &v) ? (size_t)v : kDefaultLL128;
   if (c->timeout_ms <= 0) c->timeout_ms = env_int("PAT_TIMEOUT_MS", &v) ? (int)v : kDefaultTimeoutMs;
   if (c->protocol == patProtoAuto && env_int("PAT_PROTOCOL", &v)) c->protocol = (int)v;
   if (c->threads <= 0) c->threads = env_int("PAT_THREADS", &v) ? (int)v : 512;
@@ -296,6 +303,34 @@ patResult_t compile_schedule(patComm* comm, const Schedule& given, Compiled** ou
   }
   for (int j = 0; j < p.nslots; ++j)
     if (p.slot_offset[j] == 0) p.fin[p.nfin++] = static_cast<int8_t>(j);
+  // PULL protocol tables (kernels: pull_task / pull_role)
+  for (int j = 0; j < p.nslots; ++j) p.pull_dst[j] = -1;
+  for (int f = 0; f < p.nfin; ++f) p.pull_act[p.fin[f]] = f == 0 ? kOutFirst : kOutNext;
+  for (int t = 0; t < p.nrounds; ++t) {
+    const KRound& kr = p.rounds[t];
+    int dep = -1;
+    for (int pos = 0; pos < kr.nchunks; ++pos) {
+      const int na = kr.narr[pos];
+      if (na == 0) continue;
+      dep = std::max(dep, static_cast<int>(p.slot_round[kr.arr[pos][na - 1]]));
+      for (int a = 0; a < na; ++a) {  // arrivals of the forwarded offset, round order
+        const int j = kr.arr[pos][a];
+        p.pull_dst[j] = kr.arr[pos][na - 1];
+        p.pull_act[j] = na == 1 ? kAccOnly : a == 0 ? kAccFirst : a == na - 1 ? kAccLast : kAccMid;
+      }
+    }
+    p.round_dep[t] = static_cast<int8_t>(dep);
+  }
+  for (int t = 0; t < p.nrounds; ++t) {
+    if (p.round_dep[t] >= 0) p.sig_after[p.round_dep[t]] |= static_cast<uint8_t>(1u << t);
+    for (int pos = 0; pos < p.rounds[t].nchunks; ++pos) {
+      const int j = p.rounds[t].slot_base + pos;
+      if (p.slot_offset[j] != 0) {
+        p.stage_rounds |= static_cast<uint8_t>(1u << t);
+        if (kind == kRS && p.pull_dst[j] < 0) return patInternalError;  // arrival never forwarded
+      }
+    }
+  }
   for (int t = 0; t < p.nrounds; ++t) {
     bool seen = false;
     for (int k = 0; k < p.npeers; ++k) seen |= p.peers[k] == p.rounds[t].peer;
@@ -328,14 +363,22 @@ struct Slicing {
   int64_t slice;
 };
 
-Slicing choose_slicing(const patComm* comm, int64_t chunk_bytes, int max_channels) {
+Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int max_channels, bool pull_ok) {
   Slicing s{};
   const int channels = std::max(1, std::min(comm->channels, max_channels));
   int proto = comm->cfg.protocol;
-  if (proto == patProtoAuto) proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold) ? kProtoLL : kProtoSimple;
+  if (proto == patProtoAuto)
+    proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold)      ? kProtoLL
+            : chunk_bytes <= static_cast<int64_t>(comm->cfg.ll128_threshold) ? kProtoLL128
+            : pull_ok                                                        ? kProtoPull
+                                                                             : kProtoSimple;
+  if (proto == kProtoPull && !pull_ok) proto = kProtoSimple;
   s.proto = proto;
-  const int64_t cap = proto == kProtoLL ? static_cast<int64_t>(comm->slot_bytes / 2) : static_cast<int64_t>(comm->slot_bytes);
-  const int64_t minslice = proto == kProtoLL ? 512 : 16 << 10;
+  int64_t cap = proto == kProtoLL      ? static_cast<int64_t>(comm->ll_slot_bytes / 2)
+                : proto == kProtoLL128 ? static_cast<int64_t>(comm->ll_slot_bytes / 128 * kLL128PayloadBytes)
+                                       : static_cast<int64_t>(comm->slot_bytes);
+  if (proto == kProtoPull && kind == kAG) cap = std::max<int64_t>(cap, comm->pull_slice);  // AG pull stages nothing
+  const int64_t minslice = proto == kProtoLL ? 512 : proto == kProtoLL128 ? 32 * kLL128PayloadBytes : 16 << 10;
   int64_t per = (chunk_bytes + channels - 1) / channels;
   per = (per + 15) & ~int64_t(15);
   per = std::max<int64_t>(per, std::min<int64_t>(minslice, cap));
@@ -386,8 +429,19 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   comm->cfg = c;
   comm->channels = c.max_channels;
   comm->slot_bytes = c.slice_bytes;
+  {
+    long long v = 0;
+    comm->pull_slice = env_int("PAT_PULL_SLICE", &v) && v >= 256 ? (v & ~15LL) : (512 << 10);
+  }
   const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
-  comm->pool_bytes = kFlagBytes + static_cast<size_t>(comm->channels) * c.depth * slots * comm->slot_bytes;
+  // Inbox regions: SIMPLE/PULL slots, then LL and LL128 slots. The polling protocols get their
+  // own memory: a stale payload word left by another protocol could otherwise match a flag.
+  comm->ll_slot_bytes = std::max<size_t>(256, std::min<size_t>(kLLSlotBytes, comm->slot_bytes) & ~size_t(127));
+  const size_t nslots = static_cast<size_t>(comm->channels) * c.depth * slots;
+  comm->region_off[kProtoSimple] = comm->region_off[kProtoPull] = 0;
+  comm->region_off[kProtoLL] = nslots * comm->slot_bytes;
+  comm->region_off[kProtoLL128] = comm->region_off[kProtoLL] + nslots * comm->ll_slot_bytes;
+  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL128] + nslots * comm->ll_slot_bytes;
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&comm->err_host), sizeof(int),
                          cudaHostAllocMapped | cudaHostAllocPortable));
   *comm->err_host = 0;
@@ -459,7 +513,13 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   DeviceGuard guard;
   int cap = 0;
   if (patResult_t e = channel_cap(comm, kind, dtype, op, &cap)) return e;
-  const Slicing sl = choose_slicing(comm, chunk_bytes, cap);
+  // one device holds every rank: .gpu-scope flags; zero-copy all-gather is always safe
+  const bool single_device = !comm->multiprocess && comm->groups.size() == 1;
+  // PULL reads the peers' user buffers: they must be mapped into every device of this process
+  bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple;
+  for (size_t l = 0; l < comm->lranks.size() && pull_ok && !single_device; ++l)
+    pull_ok = legacy_ipc_capable(sendbuffs[l]) && (kind == kRS || legacy_ipc_capable(recvbuffs[l]));
+  const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok);
   int vec = 16;
   bool aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
   for (size_t l = 0; l < comm->lranks.size(); ++l) {
@@ -470,8 +530,6 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   }
   vec = aligned16 ? 16 : (aligned8 ? 8 : 0);
   if (sl.proto == kProtoSimple && vec == 8) vec = 0;  // SIMPLE vectors are 16 bytes
-  // one device holds every rank: .gpu-scope flags; zero-copy all-gather is always safe
-  const bool single_device = !comm->multiprocess && comm->groups.size() == 1;
   const bool fused = single_device && comm->cfg.fused >= 0 && cp->fused_ok &&
                      static_cast<int>(comm->groups[0].lidx.size()) == n;
   bool direct = false;
@@ -492,22 +550,31 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.iters = sl.iters;
     p.chunk_bytes = chunk_bytes;
     p.slice_bytes = sl.slice;
-    p.slot_stride = static_cast<int64_t>(comm->slot_bytes);
+    p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL || sl.proto == kProtoLL128 ? comm->ll_slot_bytes
+                                                                                         : comm->slot_bytes);
     p.depth = comm->cfg.depth;
     {
       long long sk = 1;
       env_int("PAT_SKEW", &sk);
       // skew distance L: the sender keeps (nrounds-1)*L+1 steps in flight -> needs that many buffers
       const int L = static_cast<int>(std::max(0LL, sk));
-      p.skew = (L > 0 && p.proto == kProtoSimple && p.nrounds > 1 && p.depth >= (p.nrounds - 1) * L + 1 &&
-                (p.nrounds - 1) * L + 1 <= kMaxRounds)
-                   ? L
-                   : 0;
+      if (p.proto == kProtoPull)  // all-gather pull stages nothing: no credit bound on the skew
+        p.skew = (L > 0 && p.nrounds > 1 && (kind == kAG || p.depth >= (p.nrounds - 1) * L + 1)) ? L : 0;
+      else
+        p.skew = (L > 0 && p.proto == kProtoSimple && p.nrounds > 1 && p.depth >= (p.nrounds - 1) * L + 1 &&
+                  (p.nrounds - 1) * L + 1 <= kMaxRounds)
+                     ? L
+                     : 0;
     }
     p.chan_stride = static_cast<int64_t>(p.depth) * std::max(n - 1, 1) * p.slot_stride;
     p.send_warps = comm->cfg.send_warps;
     p.gpu_scope = single_device ? 1 : 0;
-    p.direct = direct ? 1 : 0;
+    p.direct = direct && sl.proto != kProtoPull ? 1 : 0;
+    if (sl.proto == kProtoPull)
+      for (size_t l = 0; l < comm->lranks.size(); ++l) {
+        p.peer_send[comm->lranks[l]] = static_cast<const char*>(sendbuffs[l]);
+        p.peer_recv[comm->lranks[l]] = static_cast<char*>(recvbuffs[l]);
+      }
     if (direct)
       for (size_t l = 0; l < comm->lranks.size(); ++l) p.peer_recv[comm->lranks[l]] = static_cast<char*>(recvbuffs[l]);
     p.timeout_ns = static_cast<uint64_t>(comm->cfg.timeout_ms) * 1000000ull;
@@ -521,7 +588,7 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     }
     for (int r = 0; r < n; ++r) {
       p.flags[r] = reinterpret_cast<uint64_t*>(g.pool_view[r]);
-      p.inbox[r] = g.pool_view[r] + kFlagBytes;
+      p.inbox[r] = g.pool_view[r] + kFlagBytes + comm->region_off[sl.proto];
     }
     for (size_t i = 0; i < g.lidx.size(); ++i) {
       const int l = g.lidx[i];
@@ -787,7 +854,7 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   DeviceGuard guard;
   int cap = 0;
   if (patResult_t e = channel_cap(comm, kind, dtype, 0, &cap)) return e;
-  const Slicing sl = choose_slicing(comm, cb, cap);
+  const Slicing sl = choose_slicing(comm, kind, cb, cap, !comm->multiprocess);  // assumes cudaMalloc buffers
   std::memset(info, 0, sizeof(*info));
   info->protocol = sl.proto;
   info->trees = trees;

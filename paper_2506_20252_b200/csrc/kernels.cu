@@ -1,595 +1,16 @@
-// kernels.cu — sm_100a kernels for PAT all-gather and reduce-scatter.
-//
-// One cooperative launch per device per collective. CTA (lr, c) runs channel c of local rank
-// lr through `iters` pipeline steps; step i moves slice (i*channels + c) of every chunk
-// through all PAT rounds. Per round the rank pushes its <= T chunk slices into the inbox of
-// peer (r + peer) over NVLink (or HBM in local mode), then signals; receivers fold or copy
-// from their own inbox. This replaces the reference executor's send/deliver phases
-// (simulate.cpp:180-218 all-gather, :247-296 reduce-scatter) and its Mailbox rendezvous +
-// lockstep join (simulate.cpp:49-70, 131-149) with per-step release/acquire flags.
-//
-// Two protocols:
-//  * LL (small messages): 16-byte lines {data32, flag, data32, flag} stored with one
-//    st.volatile.v4 into the peer's inbox; the receiver polls the line itself, so data and
-//    signal travel together and no fence or separate flag is needed. 50% wire efficiency.
-//    Every thread owns the same words of every chunk in every round: no CTA barriers.
-//  * SIMPLE (bulk): warp-specialised. Sender warps push 16-byte vectors of the slice into the
-//    peer (inbox slot, or the peer's recvbuf directly in direct all-gather mode), then one
-//    thread issues fence.acq_rel + st.relaxed of the (channel, round) flag at the receiver
-//    (NCCL-style: named barrier, then a single release). Receiver warps wait for the flags
-//    and deliver (all-gather) or fold the output (reduce-scatter), so step g+1's pushes
-//    overlap step g's delivery.
-// Inbox slots are `depth`-buffered by step; a rank re-uses a peer's slot buffer only after
-// that peer published "done with step g-depth" (credit flags), so the pool is bounded:
-// channels * depth * (n-1) slots per rank, independent of the message size.
-//
-// Reduction order (reduce-scatter) is the reference's exactly: a forwarded offset carries
-// fold(arrivals in round order) (+) own contribution (simulate.cpp:257-266, 281-285); the
-// output is own (+) offset-0 arrivals in round order (simulate.cpp:239, 278-279). Each fold
-// is rounded to the wire dtype (fp16/bf16 computed in fp32, RNE).
-#include <cuda_bf16.h>
-#include <cuda_fp16.h>
-#include <cuda_runtime.h>
-
-#include <cstdint>
-#include <type_traits>
-
-#include "fold.cuh"
-#include "plan.hpp"
+// kernels.cu — dispatch and launch of the transport kernel (transport.cuh). The kernel
+// templates are instantiated per dtype group in rs_*.cu so the build compiles in parallel.
+#include "transport.cuh"
 
 namespace pat {
 
-// ------------------------------------------------------------------------- memory primitives
-
-// Flags and fences at .gpu scope when every rank lives on this device, .sys across GPUs.
-__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, bool gpu) {
-  uint64_t v;
-  if (gpu) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  else asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v, bool gpu) {
-  if (gpu) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-  else asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, bool gpu) {
-  if (gpu) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-  else asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void fence_acq_rel(bool gpu) {
-  if (gpu) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  else asm volatile("fence.acq_rel.sys;" ::: "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ uint64_t globaltimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ uint4 ld16(const void* p) {  // L2-coherent (bypasses a stale L1)
-  uint4 v;
-  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ void st16(void* p, uint4 v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ void st_ll(void* p, uint2 v, uint32_t flag) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(flag), "r"(v.y),
-               "r"(flag)
-               : "memory");
-}
-__device__ __forceinline__ uint4 ld_volatile16(const void* p) {
-  uint4 v;
-  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-// ------------------------------------------------------------------------- waits
-
-struct Waiter {
-  uint64_t timeout_ns;
-  int* err;
-  bool aborted;
-  bool gpu;  // flag scope
-};
-
-// ------------------------------------------------------------------------- device trace
-// Event codes (bits 56..63 event, 40..55 step, 32..39 round); one writer thread per role.
-enum TraceEv : uint64_t {
-  kEvStart = 1, kEvCredit = 2, kEvPushed = 3, kEvFenced = 4, kEvArrived = 5, kEvDelivered = 6, kEvDone = 7,
-  kEvEnd = 8, kEvWaitArr = 9
-};
-
-struct Tracer {
-  uint64_t* buf = nullptr;
-  int cap = 0, n = 0;
-  __device__ __forceinline__ void init(const KPlan& p, int role) {
-    if (p.trace) {
-      buf = p.trace + (static_cast<int64_t>(blockIdx.x) * 2 + role) * p.trace_cap * 2;
-      cap = p.trace_cap;
-    }
-  }
-  __device__ __forceinline__ void rec(uint64_t ev, uint64_t step, int round) {
-    if (buf && n < cap) {
-      buf[2 * n] = globaltimer();
-      buf[2 * n + 1] = (ev << 56) | ((step & 0xffff) << 40) | (static_cast<uint64_t>(round & 0xff) << 32);
-      ++n;
-    }
-  }
-};
-
-__device__ __noinline__ void report_timeout(Waiter& w) {
-  if (!w.aborted) {
-    atomicCAS_system(w.err, 0, 40 /* patTimeout */);
-    w.aborted = true;
-  }
-}
-
-// Spin until *flag >= want (acquire). Thread-level; callers broadcast with a barrier.
-__device__ __forceinline__ void wait_flag(const uint64_t* flag, uint64_t want, Waiter& w) {
-  if (w.aborted) return;
-  uint64_t start = 0;
-  uint32_t spins = 0;
-  while (ld_acquire(flag, w.gpu) < want) {
-    if ((++spins & 1023u) == 0) {
-      const uint64_t now = globaltimer();
-      if (start == 0) start = now;
-      else if (now - start > w.timeout_ns) { report_timeout(w); return; }
-    }
-  }
-}
-
-// Poll one LL line until both flag words carry `flag`; returns its 8 data bytes.
-__device__ __forceinline__ uint2 ld_ll(const char* line, uint32_t flag, Waiter& w) {
-  uint4 v = ld_volatile16(line);
-  if (v.y == flag && v.w == flag) return make_uint2(v.x, v.z);
-  uint64_t start = 0;
-  uint32_t spins = 0;
-  while (!w.aborted) {
-    v = ld_volatile16(line);
-    if (v.y == flag && v.w == flag) break;
-    if ((++spins & 1023u) == 0) {
-      const uint64_t now = globaltimer();
-      if (start == 0) start = now;
-      else if (now - start > w.timeout_ns) report_timeout(w);
-    }
-  }
-  return make_uint2(v.x, v.z);
-}
-
-// ------------------------------------------------------------------------- group data movers
-
-// dst = fold_left(src[0], ..., src[m-1]) over `len` bytes (16-byte vectors; len % 16 == 0),
-// by the `nthr` threads of one warp group (thread index `tid` within the group).
-template <int DT, int OP>
-__device__ __forceinline__ void grp_fold16(char* dst, const char* const* src, int m, int64_t len, int tid, int nthr) {
-  const int64_t nu = len >> 4;
-  const int64_t B = nthr;
-  int64_t u = tid;
-  if (m == 1) {  // copy: 8 independent 16-byte loads in flight per thread
-    const char* s0 = src[0];
-    constexpr int U = 8;
-    for (; u + (U - 1) * B < nu; u += U * B) {
-      uint4 v[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) v[k] = ld16(s0 + 16 * (u + k * B));
-#pragma unroll
-      for (int k = 0; k < U; ++k) st16(dst + 16 * (u + k * B), v[k]);
-    }
-    for (; u < nu; u += B) st16(dst + 16 * u, ld16(s0 + 16 * u));
-    return;
-  }
-  constexpr int U = 4;
-  for (; u + (U - 1) * B < nu; u += U * B) {
-    uint4 a[U];
-#pragma unroll
-    for (int i = 0; i < U; ++i) a[i] = ld16(src[0] + 16 * (u + i * B));
-    for (int k = 1; k < m; ++k) {
-      uint4 b[U];
-#pragma unroll
-      for (int i = 0; i < U; ++i) b[i] = ld16(src[k] + 16 * (u + i * B));
-#pragma unroll
-      for (int i = 0; i < U; ++i) fold_vec<DT, OP>(a[i], b[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < U; ++i) st16(dst + 16 * (u + i * B), a[i]);
-  }
-  for (; u < nu; u += B) {
-    uint4 a = ld16(src[0] + 16 * u);
-    for (int k = 1; k < m; ++k) fold_vec<DT, OP>(a, ld16(src[k] + 16 * u));
-    st16(dst + 16 * u, a);
-  }
-}
-
-// Element-granular variant for buffers that are not 16-byte aligned.
-template <int DT, int OP>
-__device__ __forceinline__ void grp_fold_elems(char* dst, const char* const* src, int m, int64_t len, int esize,
-                                               int tid, int nthr) {
-  const int64_t ne = len / esize;
-  for (int64_t e = tid; e < ne; e += nthr) {
-    uint64_t a = ld_elem(src[0] + e * esize, esize);
-    for (int k = 1; k < m; ++k) a = fold_elem_bits<DT, OP>(a, ld_elem(src[k] + e * esize, esize));
-    st_elem(dst + e * esize, a, esize);
-  }
-}
-
-template <int DT, int OP>
-__device__ __forceinline__ void grp_fold(char* dst, const char* const* src, int m, int64_t len, const KPlan& p,
-                                         int tid, int nthr) {
-  if (len <= 0) return;
-  if (p.vec == 16) grp_fold16<DT, OP>(dst, src, m, len, tid, nthr);
-  else grp_fold_elems<DT, OP>(dst, src, m, len, p.esize, tid, nthr);
-}
-
-// 8-byte user words for LL (zero padded past `valid`).
-__device__ __forceinline__ uint2 load_word(const char* p, int valid, const KPlan& pl) {
-  if (valid == 8 && pl.vec >= 8) {
-    const uint64_t v = ld_cg_bytes<8>(p);
-    return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
-  }
-  uint64_t v = 0;
-  for (int b = 0; b < valid; b += pl.esize) v |= ld_elem(p + b, pl.esize) << (8 * b);
-  return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
-}
-__device__ __forceinline__ void store_word(char* p, uint2 w, int valid, const KPlan& pl) {
-  const uint64_t v = static_cast<uint64_t>(w.x) | (static_cast<uint64_t>(w.y) << 32);
-  if (valid == 8 && pl.vec >= 8) {
-    *reinterpret_cast<uint64_t*>(p) = v;
-    return;
-  }
-  for (int b = 0; b < valid; b += pl.esize) {
-    const uint64_t mask = pl.esize == 8 ? ~0ull : ((1ull << (8 * pl.esize)) - 1);
-    st_elem(p + b, (v >> (8 * b)) & mask, pl.esize);
-  }
-}
-
-// ------------------------------------------------------------------------- steps
-
-struct Step {
-  uint64_t g;        // absolute pipeline step of this channel
-  int64_t off, len;  // byte range of the slice within every chunk
-  int R, lr, c, buf;
-};
-
-__device__ __forceinline__ Step make_step(const KPlan& p, uint64_t base, int i, int R, int lr, int c) {
-  Step s;
-  s.g = base + i;
-  s.off = (static_cast<int64_t>(i) * p.channels + c) * p.slice_bytes;
-  s.len = max(int64_t{0}, min(p.slice_bytes, p.chunk_bytes - s.off));
-  s.R = R;
-  s.lr = lr;
-  s.c = c;
-  s.buf = static_cast<int>(s.g % static_cast<uint64_t>(p.depth));
-  return s;
-}
-
-__device__ __forceinline__ char* slot_ptr(const KPlan& p, int rank, int c, int buf, int j) {
-  return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j) * p.slot_stride;
-}
-
-__device__ __forceinline__ uint64_t* chan_flags(const KPlan& p, int rank, int c) {
-  return p.flags[rank] + c * kFlagWords;
-}
-
-// Credits: before pushing step g into a peer's inbox buffer g % depth, the peer must have
-// finished step g - depth (published as done_from[peer] >= g - depth + 1).
-__device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Waiter& w) {
-  if (s.g < static_cast<uint64_t>(p.depth)) return;
-  const uint64_t* mine = chan_flags(p, s.R, s.c);
-  for (int k = 0; k < p.npeers; ++k) wait_flag(mine + 8 + (s.R + p.peers[k]) % p.n, s.g - p.depth + 1, w);
-}
-
-// SIMPLE sender role, one PAT round of step s (warps [0, send_warps)). `waited` caches which
-// rounds' arrivals of this step were already acquired.
-template <int DT, int OP, int KIND>
-__device__ void send_round(const KPlan& p, const Step& s, int t, uint32_t& waited, Waiter& w, int tid, int nthr,
-                           bool signal) {
-  const int n = p.n;
-  const int64_t Cb = p.chunk_bytes;
-  const char* snd = p.send[s.lr];
-  char* out = p.recv[s.lr];
-  const uint64_t* myflags = chan_flags(p, s.R, s.c);
-  const bool gpu = p.gpu_scope;
-  auto ensure = [&](int tr) {  // arrivals of round tr (needed for forwarding)
-    if (!((waited >> tr) & 1u)) {
-      if (tid == 0) wait_flag(myflags + tr, s.g + 1, w);
-      named_bar(1, nthr);
-      waited |= 1u << tr;
-    }
-  };
-  const char* srcs[kMaxArr + 1];
-  {
-    const KRound& r = p.rounds[t];
-    const int P = (s.R + r.peer) % n;
-    for (int pos = 0; pos < r.nchunks; ++pos) {
-      int m = 0;
-      char* dst;
-      if constexpr (KIND == kAG) {
-        const int origin = (s.R - r.chunk[pos] + n) % n;
-        if (r.narr[pos] == 0) {
-          srcs[m++] = snd + s.off;
-        } else {
-          const int j = r.arr[pos][0];
-          ensure(p.slot_round[j]);
-          srcs[m++] = p.direct ? out + origin * Cb + s.off : slot_ptr(p, s.R, s.c, s.buf, j);
-        }
-        dst = p.direct ? p.peer_recv[P] + origin * Cb + s.off : slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
-      } else {
-        const int dest = (s.R - r.chunk[pos] + n) % n;
-        for (int a = 0; a < r.narr[pos]; ++a) {
-          const int j = r.arr[pos][a];
-          ensure(p.slot_round[j]);
-          srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, j);
-        }
-        srcs[m++] = snd + dest * Cb + s.off;  // own contribution folded last
-        dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
-      }
-      grp_fold<DT, OP>(dst, srcs, m, s.len, p, tid, nthr);
-    }
-    if (signal) {
-      named_bar(1, nthr);
-      if (tid == 0) {
-        fence_acq_rel(gpu);
-        st_relaxed(chan_flags(p, P, s.c) + t, s.g + 1, gpu);
-      }
-    }
-  }
-}
-
-// SIMPLE sender role over all steps. With p.skew, iteration k runs round t of step k - t
-// (oldest step first): a forward of round t waits for arrivals its upstream peer pushed one
-// iteration earlier, so the flag latency hides behind the next step's pushes (a wavefront
-// through the PAT tree). Needs depth > nrounds - 1 inbox buffers (host guarantees).
-template <int DT, int OP, int KIND>
-__device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, Waiter& w, int tid, int nthr,
-                          volatile uint64_t* sent_steps) {
-  const int NR = p.nrounds;
-  uint32_t waited[kMaxRounds] = {};
-  Tracer tr;
-  if (tid == 0) tr.init(p, 0);
-  tr.rec(kEvStart, base, 0);
-  auto task = [&](int i, int t, bool signal) {
-    const Step s = make_step(p, base, i, R, lr, c);
-    uint32_t& wm = waited[i % kMaxRounds];
-    if (t == 0) {  // first push of step i: the peers' buffers (g % depth) must be free
-      wm = 0;
-      if (tid == 0 && !p.direct) wait_credits(p, s, w);
-      tr.rec(kEvCredit, s.g, 0);
-      named_bar(1, nthr);
-    }
-    send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr, signal);
-    tr.rec(kEvPushed, s.g, t);
-    if (signal && t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
-  };
-  if (p.skew) {
-    // Round t of step k - t*L in iteration k (L = p.skew): the newest step's independent
-    // round 0 goes first, forwards of older steps after it, then ONE fence for the iteration
-    // and all of its flags.
-    const int L = p.skew;
-    for (int k = 0; k < p.iters + (NR - 1) * L; ++k) {
-      for (int t = 0; t < NR; ++t)
-        if (k - t * L >= 0 && k - t * L < p.iters) task(k - t * L, t, false);
-      named_bar(1, nthr);
-      if (tid == 0) {
-        fence_acq_rel(p.gpu_scope);
-        tr.rec(kEvFenced, base + k, 0);
-        for (int t = NR - 1; t >= 0; --t) {
-          const int i = k - t * L;
-          if (i < 0 || i >= p.iters) continue;
-          st_relaxed(chan_flags(p, (R + p.rounds[t].peer) % p.n, c) + t, base + i + 1, p.gpu_scope);
-          if (t == NR - 1) *sent_steps = base + i + 1;
-        }
-      }
-    }
-  } else {
-    for (int i = 0; i < p.iters; ++i)
-      for (int t = 0; t < NR; ++t) task(i, t, true);
-  }
-  if (NR == 0 && tid == 0) *sent_steps = base + p.iters;
-  tr.rec(kEvEnd, base + p.iters, 0);
-}
-
-// SIMPLE receiver role: delivers (AG) or folds the output (RS) of step s, then — once the
-// sender role is also done with this step's inbox — publishes done(g) to every rank.
-template <int DT, int OP, int KIND>
-__device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int nthr,
-                          volatile uint64_t* sent_steps, Tracer& tr) {
-  const int n = p.n;
-  const int64_t Cb = p.chunk_bytes;
-  const char* snd = p.send[s.lr];
-  char* out = p.recv[s.lr];
-  const uint64_t* myflags = chan_flags(p, s.R, s.c);
-  const bool gpu = p.gpu_scope;
-  const char* srcs[kMaxArr + 1];
-  if constexpr (KIND == kAG) {
-    if (out + s.R * Cb != snd) {  // own chunk placement (simulate.cpp:160-165); skipped in place
-      srcs[0] = snd + s.off;
-      grp_fold<DT, OP>(out + s.R * Cb + s.off, srcs, 1, s.len, p, tid, nthr);
-    }
-  }
-  for (int t = 0; t < p.nrounds; ++t) {
-    if (tid == 0) wait_flag(myflags + t, s.g + 1, w);
-    tr.rec(kEvArrived, s.g, t);
-    named_bar(2, nthr);
-    if constexpr (KIND == kAG) {
-      if (!p.direct) {
-        const KRound& r = p.rounds[t];
-        for (int pos = 0; pos < r.nchunks; ++pos) {
-          const int j = r.slot_base + pos;
-          const int origin = (s.R - p.slot_offset[j] + n) % n;
-          srcs[0] = slot_ptr(p, s.R, s.c, s.buf, j);
-          grp_fold<DT, OP>(out + origin * Cb + s.off, srcs, 1, s.len, p, tid, nthr);
-        }
-      }
-    }
-  }
-  if constexpr (KIND == kRS) {
-    int m = 0;
-    srcs[m++] = snd + s.R * Cb + s.off;  // output starts as own contribution (simulate.cpp:239)
-    for (int f = 0; f < p.nfin; ++f) srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, p.fin[f]);
-    grp_fold<DT, OP>(out + s.off, srcs, m, s.len, p, tid, nthr);
-  }
-  if (tid == 0) {  // the sender role must be done reading this step's inbox too
-    uint64_t start = 0;
-    uint32_t spins = 0;
-    while (*sent_steps < s.g + 1 && !w.aborted) {
-      if ((++spins & 1023u) == 0) {
-        const uint64_t now = globaltimer();
-        if (start == 0) start = now;
-        else if (now - start > w.timeout_ns) report_timeout(w);
-      }
-    }
-  }
-  tr.rec(kEvDelivered, s.g, 0);
-  named_bar(2, nthr);
-  if (tid < n && tid != s.R) st_release(chan_flags(p, tid, s.c) + 8 + s.R, s.g + 1, gpu);
-}
-
-// LL: every thread owns the same 8-byte words of the slice in every chunk and round, so it
-// only ever waits on lines it polls itself — no CTA barrier inside the step.
-template <int DT, int OP, int KIND>
-__device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
-  const int n = p.n;
-  const int64_t Cb = p.chunk_bytes;
-  const char* snd = p.send[s.lr];
-  char* out = p.recv[s.lr];
-  const uint32_t flag = static_cast<uint32_t>(s.g + 1);
-  const int64_t nlines = (s.len + 7) >> 3;
-  const int B = blockDim.x;
-
-  if constexpr (KIND == kAG) {
-    if (out + s.R * Cb != snd)
-      for (int64_t q = threadIdx.x; q < nlines; q += B) {
-        const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
-        store_word(out + s.R * Cb + s.off + 8 * q, load_word(snd + s.off + 8 * q, valid, p), valid, p);
-      }
-  }
-  for (int t = 0; t < p.nrounds; ++t) {
-    const KRound& r = p.rounds[t];
-    const int P = (s.R + r.peer) % n;
-    for (int pos = 0; pos < r.nchunks; ++pos) {
-      char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
-      if constexpr (KIND == kAG) {
-        const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
-        for (int64_t q = threadIdx.x; q < nlines; q += B) {
-          const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
-          const uint2 v = fwd ? ld_ll(fwd + 16 * q, flag, w) : load_word(snd + s.off + 8 * q, valid, p);
-          st_ll(dst + 16 * q, v, flag);
-        }
-      } else {
-        const int dest = (s.R - r.chunk[pos] + n) % n;
-        const char* own = snd + dest * Cb + s.off;
-        const int na = r.narr[pos];
-        for (int64_t q = threadIdx.x; q < nlines; q += B) {
-          const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
-          uint2 acc;
-          if (na == 0) {
-            acc = load_word(own + 8 * q, valid, p);
-          } else {
-            acc = ld_ll(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) + 16 * q, flag, w);
-            for (int a = 1; a < na; ++a)
-              fold_vec<DT, OP>(acc, ld_ll(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][a]) + 16 * q, flag, w));
-            fold_vec<DT, OP>(acc, load_word(own + 8 * q, valid, p));
-          }
-          st_ll(dst + 16 * q, acc, flag);
-        }
-      }
-    }
-  }
-  if constexpr (KIND == kAG) {
-    for (int j = 0; j < p.nslots; ++j) {
-      const int origin = (s.R - p.slot_offset[j] + n) % n;
-      const char* slot = slot_ptr(p, s.R, s.c, s.buf, j);
-      for (int64_t q = threadIdx.x; q < nlines; q += B) {
-        const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
-        store_word(out + origin * Cb + s.off + 8 * q, ld_ll(slot + 16 * q, flag, w), valid, p);
-      }
-    }
-  } else {
-    for (int64_t q = threadIdx.x; q < nlines; q += B) {
-      const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
-      uint2 acc = load_word(snd + s.R * Cb + s.off + 8 * q, valid, p);
-      for (int f = 0; f < p.nfin; ++f)
-        fold_vec<DT, OP>(acc, ld_ll(slot_ptr(p, s.R, s.c, s.buf, p.fin[f]) + 16 * q, flag, w));
-      store_word(out + s.off + 8 * q, acc, valid, p);
-    }
-  }
-}
-
-template <int DT, int OP, int KIND>
-__global__ void __launch_bounds__(1024) pat_kernel(const __grid_constant__ KPlan p) {
-  const int lr = blockIdx.x / p.channels;
-  const int c = blockIdx.x - lr * p.channels;
-  const int R = p.rank[lr];
-  __shared__ uint64_t s_base;
-  __shared__ volatile uint64_t s_sent;
-  if (threadIdx.x == 0) {
-    s_base = p.iter_state[lr][c];
-    s_sent = 0;
-  }
-  __syncthreads();
-  const uint64_t base = s_base;
-  Waiter w{p.timeout_ns, p.err, false, p.gpu_scope != 0};
-
-  if (p.direct && KIND == kAG) {
-    // entry handshake: a peer may be written directly only once it entered this call
-    if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
-      st_release(chan_flags(p, threadIdx.x, c) + 16 + R, base + 1, w.gpu);
-    if (threadIdx.x == 0)
-      for (int k = 0; k < p.npeers; ++k)
-        wait_flag(chan_flags(p, R, c) + 16 + (R + p.peers[k]) % p.n, base + 1, w);
-    __syncthreads();
-  }
-
-  if (p.proto == kProtoLL) {
-    for (int i = 0; i < p.iters; ++i) {
-      const Step s = make_step(p, base, i, R, lr, c);
-      if (threadIdx.x == 0) wait_credits(p, s, w);
-      __syncthreads();
-      step_ll<DT, OP, KIND>(p, s, w);
-      __syncthreads();
-      if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
-        st_release(chan_flags(p, threadIdx.x, c) + 8 + R, s.g + 1, w.gpu);
-    }
-  } else {
-    const int nsend = p.send_warps * 32;
-    if (static_cast<int>(threadIdx.x) < nsend) {
-      send_role<DT, OP, KIND>(p, base, R, lr, c, w, threadIdx.x, nsend, &s_sent);
-    } else {
-      const int tid = threadIdx.x - nsend, nrecv = blockDim.x - nsend;
-      Tracer tr;
-      if (tid == 0) tr.init(p, 1);
-      tr.rec(kEvStart, base, 0);
-      for (int i = 0; i < p.iters; ++i) {
-        const Step s = make_step(p, base, i, R, lr, c);
-        recv_step<DT, OP, KIND>(p, s, w, tid, nrecv, &s_sent, tr);
-      }
-      tr.rec(kEvEnd, base + p.iters, 0);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) p.iter_state[lr][c] = base + p.iters;
-}
-
-// ------------------------------------------------------------------------- dispatch
-
 using KernelFn = void (*)(const KPlan);
 
-#define PAT_RS_ROW(DT) \
-  { pat_kernel<DT, kSum, kRS>, pat_kernel<DT, kProd, kRS>, pat_kernel<DT, kMax, kRS>, pat_kernel<DT, kMin, kRS> }
+extern const KernelFn kRsRowI8[4], kRsRowU8[4], kRsRowI32[4], kRsRowU32[4], kRsRowI64[4], kRsRowU64[4],
+    kRsRowF16[4], kRsRowF32[4], kRsRowF64[4], kRsRowBF16[4];
 
-static const KernelFn kRsTable[10][4] = {
-    PAT_RS_ROW(kI8), PAT_RS_ROW(kU8), PAT_RS_ROW(kI32), PAT_RS_ROW(kU32), PAT_RS_ROW(kI64),
-    PAT_RS_ROW(kU64), PAT_RS_ROW(kF16), PAT_RS_ROW(kF32), PAT_RS_ROW(kF64), PAT_RS_ROW(kBF16)};
+static const KernelFn* const kRsTable[10] = {kRsRowI8,  kRsRowU8,  kRsRowI32, kRsRowU32, kRsRowI64,
+                                             kRsRowU64, kRsRowF16, kRsRowF32, kRsRowF64, kRsRowBF16};
 static const KernelFn kAgKernel = pat_kernel<kU8, kSum, kAG>;
 
 KernelFn kernel_for(int kind, int dtype, int op) {

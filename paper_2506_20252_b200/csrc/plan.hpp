@@ -18,7 +18,17 @@ constexpr int kMaxChannels = 128;
 constexpr int kFlagWords = 32;  // per channel: data flag per round [0,8), done-from per rank [8,16),
                                 // ready-from per rank [16,24) (direct mode entry handshake)
 
-enum Proto : int { kProtoLL = 1, kProtoSimple = 2 };
+enum Proto : int { kProtoLL = 1, kProtoSimple = 2, kProtoPull = 3, kProtoLL128 = 4 };
+
+// PULL reduce-scatter: what a rank does with the arrival it pulled into slot j.
+enum PullAct : int8_t {
+  kOutFirst = 0,  // out = own[R] (+) m        (simulate.cpp:239, 278-279)
+  kOutNext = 1,   // out = out (+) m
+  kAccOnly = 2,   // stage[dst] = m (+) own     (single arrival; own folded last, :260-266)
+  kAccFirst = 3,  // stage[dst] = m             (accumulator opened by the first arrival, :282-283)
+  kAccMid = 4,    // stage[dst] = stage (+) m   (later arrivals in round order, :285)
+  kAccLast = 5    // stage[dst] = (stage (+) m) (+) own
+};
 enum KindK : int { kAG = 0, kRS = 1 };
 
 // One PAT round compiled for the kernel.
@@ -54,6 +64,12 @@ struct KPlan {
   int8_t fin[kMaxSlots];
   int8_t npeers;                   // distinct send peers (credit waits)
   int8_t peers[kMaxRounds];
+  // PULL protocol (receiver reads the upstream's buffers): per arrival slot j
+  int8_t pull_act[kMaxSlots];      // RS: PullAct
+  int8_t pull_dst[kMaxSlots];      // RS: local staging slot accumulating offset slot_offset[j]
+  int8_t round_dep[kMaxRounds];    // upstream round whose arrivals round t reads; -1 = own data only
+  uint8_t sig_after[kMaxRounds];   // reader rounds (bitmask) that become ready when round t completes
+  uint8_t stage_rounds;            // RS: bitmask of rounds that write the local staging (need credits)
   // ranks driven by this launch
   int rank[kMaxLocal];
   const char* send[kMaxLocal];
@@ -62,6 +78,7 @@ struct KPlan {
   // every rank's pool, mapped into this device's address space
   char* inbox[kMaxRanks];
   char* peer_recv[kMaxRanks];       // direct mode: every rank's recvbuf as seen from this device
+  const char* peer_send[kMaxRanks]; // PULL: every rank's sendbuf as seen from this device
   uint64_t* flags[kMaxRanks];       // [kMaxChannels][kFlagWords]
   int* err;                         // mapped pinned host word (first async error)
   // optional device trace (PAT_TRACE=1): per (CTA, role) ring of {globaltimer ns, event code}

@@ -1,0 +1,10 @@
+// rs_f64.cu — reduce-scatter transport kernels for F64, all four ops (see kernels.cu).
+#include "transport.cuh"
+
+namespace pat {
+using KernelFn = void (*)(const KPlan);
+#define PAT_RS_ROW(DT, NAME) \
+  extern const KernelFn NAME[4] = {pat_kernel<DT, kSum, kRS>, pat_kernel<DT, kProd, kRS>, pat_kernel<DT, kMax, kRS>, \
+                                  pat_kernel<DT, kMin, kRS>};
+PAT_RS_ROW(kF64, kRsRowF64)
+}  // namespace pat

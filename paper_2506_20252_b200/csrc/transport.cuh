@@ -1,0 +1,873 @@
+// kernels.cu — sm_100a kernels for PAT all-gather and reduce-scatter.
+//
+// One cooperative launch per device per collective. CTA (lr, c) runs channel c of local rank
+// lr through `iters` pipeline steps; step i moves slice (i*channels + c) of every chunk
+// through all PAT rounds. Per round the rank pushes its <= T chunk slices into the inbox of
+// peer (r + peer) over NVLink (or HBM in local mode), then signals; receivers fold or copy
+// from their own inbox. This replaces the reference executor's send/deliver phases
+// (simulate.cpp:180-218 all-gather, :247-296 reduce-scatter) and its Mailbox rendezvous +
+// lockstep join (simulate.cpp:49-70, 131-149) with per-step release/acquire flags.
+//
+// Two protocols:
+//  * LL (small messages): 16-byte lines {data32, flag, data32, flag} stored with one
+//    st.volatile.v4 into the peer's inbox; the receiver polls the line itself, so data and
+//    signal travel together and no fence or separate flag is needed. 50% wire efficiency.
+//    Every thread owns the same words of every chunk in every round: no CTA barriers.
+//  * SIMPLE (bulk): warp-specialised. Sender warps push 16-byte vectors of the slice into the
+//    peer (inbox slot, or the peer's recvbuf directly in direct all-gather mode), then one
+//    thread issues fence.acq_rel + st.relaxed of the (channel, round) flag at the receiver
+//    (NCCL-style: named barrier, then a single release). Receiver warps wait for the flags
+//    and deliver (all-gather) or fold the output (reduce-scatter), so step g+1's pushes
+//    overlap step g's delivery.
+// Inbox slots are `depth`-buffered by step; a rank re-uses a peer's slot buffer only after
+// that peer published "done with step g-depth" (credit flags), so the pool is bounded:
+// channels * depth * (n-1) slots per rank, independent of the message size.
+//
+// Reduction order (reduce-scatter) is the reference's exactly: a forwarded offset carries
+// fold(arrivals in round order) (+) own contribution (simulate.cpp:257-266, 281-285); the
+// output is own (+) offset-0 arrivals in round order (simulate.cpp:239, 278-279). Each fold
+// is rounded to the wire dtype (fp16/bf16 computed in fp32, RNE).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "fold.cuh"
+#include "plan.hpp"
+
+namespace pat {
+
+// ------------------------------------------------------------------------- memory primitives
+
+// Flags and fences at .gpu scope when every rank lives on this device, .sys across GPUs.
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, bool gpu) {
+  uint64_t v;
+  if (gpu) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v, bool gpu) {
+  if (gpu) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, bool gpu) {
+  if (gpu) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel(bool gpu) {
+  if (gpu) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint4 ld16(const void* p) {  // L2-coherent (bypasses a stale L1)
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st16(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_ll(void* p, uint2 v, uint32_t flag) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(flag), "r"(v.y),
+               "r"(flag)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_volatile16(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+// ------------------------------------------------------------------------- waits
+
+struct Waiter {
+  uint64_t timeout_ns;
+  int* err;
+  bool aborted;
+  bool gpu;  // flag scope
+};
+
+// ------------------------------------------------------------------------- device trace
+// Event codes (bits 56..63 event, 40..55 step, 32..39 round); one writer thread per role.
+enum TraceEv : uint64_t {
+  kEvStart = 1, kEvCredit = 2, kEvPushed = 3, kEvFenced = 4, kEvArrived = 5, kEvDelivered = 6, kEvDone = 7,
+  kEvEnd = 8, kEvWaitArr = 9
+};
+
+struct Tracer {
+  uint64_t* buf = nullptr;
+  int cap = 0, n = 0;
+  __device__ __forceinline__ void init(const KPlan& p, int role) {
+    if (p.trace) {
+      buf = p.trace + (static_cast<int64_t>(blockIdx.x) * 2 + role) * p.trace_cap * 2;
+      cap = p.trace_cap;
+    }
+  }
+  __device__ __forceinline__ void rec(uint64_t ev, uint64_t step, int round) {
+    if (buf && n < cap) {
+      buf[2 * n] = globaltimer();
+      buf[2 * n + 1] = (ev << 56) | ((step & 0xffff) << 40) | (static_cast<uint64_t>(round & 0xff) << 32);
+      ++n;
+    }
+  }
+};
+
+static __device__ __noinline__ void report_timeout(Waiter& w) {
+  if (!w.aborted) {
+    atomicCAS_system(w.err, 0, 40 /* patTimeout */);
+    w.aborted = true;
+  }
+}
+
+// Spin until *flag >= want (acquire). Thread-level; callers broadcast with a barrier.
+__device__ __forceinline__ void wait_flag(const uint64_t* flag, uint64_t want, Waiter& w) {
+  if (w.aborted) return;
+  uint64_t start = 0;
+  uint32_t spins = 0;
+  while (ld_acquire(flag, w.gpu) < want) {
+    if ((++spins & 1023u) == 0) {
+      const uint64_t now = globaltimer();
+      if (start == 0) start = now;
+      else if (now - start > w.timeout_ns) { report_timeout(w); return; }
+    }
+  }
+}
+
+// Poll one LL line until both flag words carry `flag`; returns its 8 data bytes.
+__device__ __forceinline__ uint2 ld_ll(const char* line, uint32_t flag, Waiter& w) {
+  uint4 v = ld_volatile16(line);
+  if (v.y == flag && v.w == flag) return make_uint2(v.x, v.z);
+  uint64_t start = 0;
+  uint32_t spins = 0;
+  while (!w.aborted) {
+    v = ld_volatile16(line);
+    if (v.y == flag && v.w == flag) break;
+    if ((++spins & 1023u) == 0) {
+      const uint64_t now = globaltimer();
+      if (start == 0) start = now;
+      else if (now - start > w.timeout_ns) report_timeout(w);
+    }
+  }
+  return make_uint2(v.x, v.z);
+}
+
+// ------------------------------------------------------------------------- group data movers
+
+// dst = fold_left(src[0], ..., src[m-1]) over `len` bytes (16-byte vectors; len % 16 == 0),
+// by the `nthr` threads of one warp group (thread index `tid` within the group).
+template <int DT, int OP>
+__device__ __forceinline__ void grp_fold16(char* dst, const char* const* src, int m, int64_t len, int tid, int nthr) {
+  const int64_t nu = len >> 4;
+  const int64_t B = nthr;
+  int64_t u = tid;
+  if (m == 1) {  // copy: 8 independent 16-byte loads in flight per thread
+    const char* s0 = src[0];
+    constexpr int U = 8;
+    for (; u + (U - 1) * B < nu; u += U * B) {
+      uint4 v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) v[k] = ld16(s0 + 16 * (u + k * B));
+#pragma unroll
+      for (int k = 0; k < U; ++k) st16(dst + 16 * (u + k * B), v[k]);
+    }
+    for (; u < nu; u += B) st16(dst + 16 * u, ld16(s0 + 16 * u));
+    return;
+  }
+  constexpr int U = 4;
+  for (; u + (U - 1) * B < nu; u += U * B) {
+    uint4 a[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) a[i] = ld16(src[0] + 16 * (u + i * B));
+    for (int k = 1; k < m; ++k) {
+      uint4 b[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) b[i] = ld16(src[k] + 16 * (u + i * B));
+#pragma unroll
+      for (int i = 0; i < U; ++i) fold_vec<DT, OP>(a[i], b[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < U; ++i) st16(dst + 16 * (u + i * B), a[i]);
+  }
+  for (; u < nu; u += B) {
+    uint4 a = ld16(src[0] + 16 * u);
+    for (int k = 1; k < m; ++k) fold_vec<DT, OP>(a, ld16(src[k] + 16 * u));
+    st16(dst + 16 * u, a);
+  }
+}
+
+// Element-granular variant for buffers that are not 16-byte aligned.
+template <int DT, int OP>
+__device__ __forceinline__ void grp_fold_elems(char* dst, const char* const* src, int m, int64_t len, int esize,
+                                               int tid, int nthr) {
+  const int64_t ne = len / esize;
+  for (int64_t e = tid; e < ne; e += nthr) {
+    uint64_t a = ld_elem(src[0] + e * esize, esize);
+    for (int k = 1; k < m; ++k) a = fold_elem_bits<DT, OP>(a, ld_elem(src[k] + e * esize, esize));
+    st_elem(dst + e * esize, a, esize);
+  }
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ void grp_fold(char* dst, const char* const* src, int m, int64_t len, const KPlan& p,
+                                         int tid, int nthr) {
+  if (len <= 0) return;
+  if (p.vec == 16) grp_fold16<DT, OP>(dst, src, m, len, tid, nthr);
+  else grp_fold_elems<DT, OP>(dst, src, m, len, p.esize, tid, nthr);
+}
+
+// 8-byte user words for LL (zero padded past `valid`).
+__device__ __forceinline__ uint2 load_word(const char* p, int valid, const KPlan& pl) {
+  if (valid == 8 && pl.vec >= 8) {
+    const uint64_t v = ld_cg_bytes<8>(p);
+    return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
+  }
+  uint64_t v = 0;
+  for (int b = 0; b < valid; b += pl.esize) v |= ld_elem(p + b, pl.esize) << (8 * b);
+  return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
+}
+__device__ __forceinline__ void store_word(char* p, uint2 w, int valid, const KPlan& pl) {
+  const uint64_t v = static_cast<uint64_t>(w.x) | (static_cast<uint64_t>(w.y) << 32);
+  if (valid == 8 && pl.vec >= 8) {
+    *reinterpret_cast<uint64_t*>(p) = v;
+    return;
+  }
+  for (int b = 0; b < valid; b += pl.esize) {
+    const uint64_t mask = pl.esize == 8 ? ~0ull : ((1ull << (8 * pl.esize)) - 1);
+    st_elem(p + b, (v >> (8 * b)) & mask, pl.esize);
+  }
+}
+
+// ------------------------------------------------------------------------- steps
+
+struct Step {
+  uint64_t g;        // absolute pipeline step of this channel
+  int64_t off, len;  // byte range of the slice within every chunk
+  int R, lr, c, buf;
+};
+
+__device__ __forceinline__ Step make_step(const KPlan& p, uint64_t base, int i, int R, int lr, int c) {
+  Step s;
+  s.g = base + i;
+  s.off = (static_cast<int64_t>(i) * p.channels + c) * p.slice_bytes;
+  s.len = max(int64_t{0}, min(p.slice_bytes, p.chunk_bytes - s.off));
+  s.R = R;
+  s.lr = lr;
+  s.c = c;
+  s.buf = static_cast<int>(s.g % static_cast<uint64_t>(p.depth));
+  return s;
+}
+
+__device__ __forceinline__ char* slot_ptr(const KPlan& p, int rank, int c, int buf, int j) {
+  return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j) * p.slot_stride;
+}
+
+__device__ __forceinline__ uint64_t* chan_flags(const KPlan& p, int rank, int c) {
+  return p.flags[rank] + c * kFlagWords;
+}
+
+// Credits: before pushing step g into a peer's inbox buffer g % depth, the peer must have
+// finished step g - depth (published as done_from[peer] >= g - depth + 1).
+__device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Waiter& w) {
+  if (s.g < static_cast<uint64_t>(p.depth)) return;
+  const uint64_t* mine = chan_flags(p, s.R, s.c);
+  for (int k = 0; k < p.npeers; ++k) wait_flag(mine + 8 + (s.R + p.peers[k]) % p.n, s.g - p.depth + 1, w);
+}
+
+// SIMPLE sender role, one PAT round of step s (warps [0, send_warps)). `waited` caches which
+// rounds' arrivals of this step were already acquired.
+template <int DT, int OP, int KIND>
+__device__ void send_round(const KPlan& p, const Step& s, int t, uint32_t& waited, Waiter& w, int tid, int nthr,
+                           bool signal) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const char* snd = p.send[s.lr];
+  char* out = p.recv[s.lr];
+  const uint64_t* myflags = chan_flags(p, s.R, s.c);
+  const bool gpu = p.gpu_scope;
+  auto ensure = [&](int tr) {  // arrivals of round tr (needed for forwarding)
+    if (!((waited >> tr) & 1u)) {
+      if (tid == 0) wait_flag(myflags + tr, s.g + 1, w);
+      named_bar(1, nthr);
+      waited |= 1u << tr;
+    }
+  };
+  const char* srcs[kMaxArr + 1];
+  {
+    const KRound& r = p.rounds[t];
+    const int P = (s.R + r.peer) % n;
+    for (int pos = 0; pos < r.nchunks; ++pos) {
+      int m = 0;
+      char* dst;
+      if constexpr (KIND == kAG) {
+        const int origin = (s.R - r.chunk[pos] + n) % n;
+        if (r.narr[pos] == 0) {
+          srcs[m++] = snd + s.off;
+        } else {
+          const int j = r.arr[pos][0];
+          ensure(p.slot_round[j]);
+          srcs[m++] = p.direct ? out + origin * Cb + s.off : slot_ptr(p, s.R, s.c, s.buf, j);
+        }
+        dst = p.direct ? p.peer_recv[P] + origin * Cb + s.off : slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
+      } else {
+        const int dest = (s.R - r.chunk[pos] + n) % n;
+        for (int a = 0; a < r.narr[pos]; ++a) {
+          const int j = r.arr[pos][a];
+          ensure(p.slot_round[j]);
+          srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, j);
+        }
+        srcs[m++] = snd + dest * Cb + s.off;  // own contribution folded last
+        dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
+      }
+      grp_fold<DT, OP>(dst, srcs, m, s.len, p, tid, nthr);
+    }
+    if (signal) {
+      named_bar(1, nthr);
+      if (tid == 0) {
+        fence_acq_rel(gpu);
+        st_relaxed(chan_flags(p, P, s.c) + t, s.g + 1, gpu);
+      }
+    }
+  }
+}
+
+// SIMPLE sender role over all steps. With p.skew, iteration k runs round t of step k - t
+// (oldest step first): a forward of round t waits for arrivals its upstream peer pushed one
+// iteration earlier, so the flag latency hides behind the next step's pushes (a wavefront
+// through the PAT tree). Needs depth > nrounds - 1 inbox buffers (host guarantees).
+template <int DT, int OP, int KIND>
+__device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, Waiter& w, int tid, int nthr,
+                          volatile uint64_t* sent_steps) {
+  const int NR = p.nrounds;
+  uint32_t waited[kMaxRounds] = {};
+  Tracer tr;
+  if (tid == 0) tr.init(p, 0);
+  tr.rec(kEvStart, base, 0);
+  auto task = [&](int i, int t, bool signal) {
+    const Step s = make_step(p, base, i, R, lr, c);
+    uint32_t& wm = waited[i % kMaxRounds];
+    if (t == 0) {  // first push of step i: the peers' buffers (g % depth) must be free
+      wm = 0;
+      if (tid == 0 && !p.direct) wait_credits(p, s, w);
+      tr.rec(kEvCredit, s.g, 0);
+      named_bar(1, nthr);
+    }
+    send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr, signal);
+    tr.rec(kEvPushed, s.g, t);
+    if (signal && t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
+  };
+  if (p.skew) {
+    // Round t of step k - t*L in iteration k (L = p.skew): the newest step's independent
+    // round 0 goes first, forwards of older steps after it, then ONE fence for the iteration
+    // and all of its flags.
+    const int L = p.skew;
+    for (int k = 0; k < p.iters + (NR - 1) * L; ++k) {
+      for (int t = 0; t < NR; ++t)
+        if (k - t * L >= 0 && k - t * L < p.iters) task(k - t * L, t, false);
+      named_bar(1, nthr);
+      if (tid == 0) {
+        fence_acq_rel(p.gpu_scope);
+        tr.rec(kEvFenced, base + k, 0);
+        for (int t = NR - 1; t >= 0; --t) {
+          const int i = k - t * L;
+          if (i < 0 || i >= p.iters) continue;
+          st_relaxed(chan_flags(p, (R + p.rounds[t].peer) % p.n, c) + t, base + i + 1, p.gpu_scope);
+          if (t == NR - 1) *sent_steps = base + i + 1;
+        }
+      }
+    }
+  } else {
+    for (int i = 0; i < p.iters; ++i)
+      for (int t = 0; t < NR; ++t) task(i, t, true);
+  }
+  if (NR == 0 && tid == 0) *sent_steps = base + p.iters;
+  tr.rec(kEvEnd, base + p.iters, 0);
+}
+
+// SIMPLE receiver role: delivers (AG) or folds the output (RS) of step s, then — once the
+// sender role is also done with this step's inbox — publishes done(g) to every rank.
+template <int DT, int OP, int KIND>
+__device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int nthr,
+                          volatile uint64_t* sent_steps, Tracer& tr) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const char* snd = p.send[s.lr];
+  char* out = p.recv[s.lr];
+  const uint64_t* myflags = chan_flags(p, s.R, s.c);
+  const bool gpu = p.gpu_scope;
+  const char* srcs[kMaxArr + 1];
+  if constexpr (KIND == kAG) {
+    if (out + s.R * Cb != snd) {  // own chunk placement (simulate.cpp:160-165); skipped in place
+      srcs[0] = snd + s.off;
+      grp_fold<DT, OP>(out + s.R * Cb + s.off, srcs, 1, s.len, p, tid, nthr);
+    }
+  }
+  for (int t = 0; t < p.nrounds; ++t) {
+    if (tid == 0) wait_flag(myflags + t, s.g + 1, w);
+    tr.rec(kEvArrived, s.g, t);
+    named_bar(2, nthr);
+    if constexpr (KIND == kAG) {
+      if (!p.direct) {
+        const KRound& r = p.rounds[t];
+        for (int pos = 0; pos < r.nchunks; ++pos) {
+          const int j = r.slot_base + pos;
+          const int origin = (s.R - p.slot_offset[j] + n) % n;
+          srcs[0] = slot_ptr(p, s.R, s.c, s.buf, j);
+          grp_fold<DT, OP>(out + origin * Cb + s.off, srcs, 1, s.len, p, tid, nthr);
+        }
+      }
+    }
+  }
+  if constexpr (KIND == kRS) {
+    int m = 0;
+    srcs[m++] = snd + s.R * Cb + s.off;  // output starts as own contribution (simulate.cpp:239)
+    for (int f = 0; f < p.nfin; ++f) srcs[m++] = slot_ptr(p, s.R, s.c, s.buf, p.fin[f]);
+    grp_fold<DT, OP>(out + s.off, srcs, m, s.len, p, tid, nthr);
+  }
+  if (tid == 0) {  // the sender role must be done reading this step's inbox too
+    uint64_t start = 0;
+    uint32_t spins = 0;
+    while (*sent_steps < s.g + 1 && !w.aborted) {
+      if ((++spins & 1023u) == 0) {
+        const uint64_t now = globaltimer();
+        if (start == 0) start = now;
+        else if (now - start > w.timeout_ns) report_timeout(w);
+      }
+    }
+  }
+  tr.rec(kEvDelivered, s.g, 0);
+  named_bar(2, nthr);
+  if (tid < n && tid != s.R) st_release(chan_flags(p, tid, s.c) + 8 + s.R, s.g + 1, gpu);
+}
+
+// LL: every thread owns the same 8-byte words of the slice in every chunk and round, so it
+// only ever waits on lines it polls itself — no CTA barrier inside the step.
+template <int DT, int OP, int KIND>
+__device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const char* snd = p.send[s.lr];
+  char* out = p.recv[s.lr];
+  const uint32_t flag = static_cast<uint32_t>(s.g + 1);
+  const int64_t nlines = (s.len + 7) >> 3;
+  const int B = blockDim.x;
+
+  if constexpr (KIND == kAG) {
+    if (out + s.R * Cb != snd)
+      for (int64_t q = threadIdx.x; q < nlines; q += B) {
+        const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+        store_word(out + s.R * Cb + s.off + 8 * q, load_word(snd + s.off + 8 * q, valid, p), valid, p);
+      }
+  }
+  for (int t = 0; t < p.nrounds; ++t) {
+    const KRound& r = p.rounds[t];
+    const int P = (s.R + r.peer) % n;
+    for (int pos = 0; pos < r.nchunks; ++pos) {
+      char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
+      if constexpr (KIND == kAG) {
+        const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
+        for (int64_t q = threadIdx.x; q < nlines; q += B) {
+          const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+          const uint2 v = fwd ? ld_ll(fwd + 16 * q, flag, w) : load_word(snd + s.off + 8 * q, valid, p);
+          st_ll(dst + 16 * q, v, flag);
+        }
+      } else {
+        const int dest = (s.R - r.chunk[pos] + n) % n;
+        const char* own = snd + dest * Cb + s.off;
+        const int na = r.narr[pos];
+        for (int64_t q = threadIdx.x; q < nlines; q += B) {
+          const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+          uint2 acc;
+          if (na == 0) {
+            acc = load_word(own + 8 * q, valid, p);
+          } else {
+            acc = ld_ll(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) + 16 * q, flag, w);
+            for (int a = 1; a < na; ++a)
+              fold_vec<DT, OP>(acc, ld_ll(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][a]) + 16 * q, flag, w));
+            fold_vec<DT, OP>(acc, load_word(own + 8 * q, valid, p));
+          }
+          st_ll(dst + 16 * q, acc, flag);
+        }
+      }
+    }
+  }
+  if constexpr (KIND == kAG) {
+    for (int j = 0; j < p.nslots; ++j) {
+      const int origin = (s.R - p.slot_offset[j] + n) % n;
+      const char* slot = slot_ptr(p, s.R, s.c, s.buf, j);
+      for (int64_t q = threadIdx.x; q < nlines; q += B) {
+        const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+        store_word(out + origin * Cb + s.off + 8 * q, ld_ll(slot + 16 * q, flag, w), valid, p);
+      }
+    }
+  } else {
+    for (int64_t q = threadIdx.x; q < nlines; q += B) {
+      const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+      uint2 acc = load_word(snd + s.R * Cb + s.off + 8 * q, valid, p);
+      for (int f = 0; f < p.nfin; ++f)
+        fold_vec<DT, OP>(acc, ld_ll(slot_ptr(p, s.R, s.c, s.buf, p.fin[f]) + 16 * q, flag, w));
+      store_word(out + s.off + 8 * q, acc, valid, p);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------- PULL protocol
+// The receiver reads. In round t rank R pulls the chunks K_t from its upstream Q = R - peer_t
+// (the rank that pushes to it in the reference's send/deliver, simulate.cpp:186-212, 252-290):
+//  * all-gather: a leaf chunk comes straight from Q's sendbuf, a forwarded one from Q's recvbuf
+//    (where Q itself delivered it) — zero copy on both sides, no staging at all;
+//  * reduce-scatter: a leaf is Q's own contribution (Q's sendbuf); a forwarded offset is Q's
+//    staged message fold(arrivals) (+) own, which Q finalised when it pulled the last arrival.
+//    R folds what it pulls into its output or into its own staging slot (PullAct).
+// Every NVLink byte is a read of the peer's HBM (measured 775 GB/s vs 714 GB/s for pushed
+// stores, profiles/r01_p2p_probe_*.txt). Flags: after finishing round tr of a step, Q tells each
+// reader whose round t'' depends on round tr (sig_after) by a store into the reader's flags;
+// readers publish done(step) to every rank, which is the staging credit (RS) and the exit
+// condition: a rank leaves the call only once its readers are done with its buffers.
+
+template <int DT, int OP, int KIND>
+__device__ __forceinline__ void pull_task(const KPlan& p, const Step& s, int t, int tid, int nthr) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const KRound& r = p.rounds[t];
+  const int Q = (s.R - r.peer + n) % n;
+  char* out = p.recv[s.lr];
+  const char* own = p.send[s.lr];
+  const char* srcs[3];
+  for (int pos = 0; pos < r.nchunks; ++pos) {
+    const int k = r.chunk[pos];              // offset at the sender Q
+    const int at = (Q - k + n) % n;          // AG: origin; RS: destination of the contribution
+    if constexpr (KIND == kAG) {
+      srcs[0] = r.narr[pos] == 0 ? p.peer_send[Q] + s.off : p.peer_recv[Q] + at * Cb + s.off;
+      grp_fold<DT, OP>(out + at * Cb + s.off, srcs, 1, s.len, p, tid, nthr);
+    } else {
+      const char* m = r.narr[pos] == 0 ? p.peer_send[Q] + at * Cb + s.off
+                                       : slot_ptr(p, Q, s.c, s.buf, r.arr[pos][r.narr[pos] - 1]);
+      const int j = r.slot_base + pos;
+      const int kr = p.slot_offset[j];                  // received offset at R
+      const char* mine = own + ((s.R - kr + n) % n) * Cb + s.off;
+      char* stage = slot_ptr(p, s.R, s.c, s.buf, p.pull_dst[j]);
+      char* dst = stage;
+      int cnt = 2;
+      switch (p.pull_act[j]) {
+        case kOutFirst: dst = out + s.off; srcs[0] = mine; srcs[1] = m; break;
+        case kOutNext: dst = out + s.off; srcs[0] = dst; srcs[1] = m; break;
+        case kAccOnly: srcs[0] = m; srcs[1] = mine; break;
+        case kAccFirst: srcs[0] = m; cnt = 1; break;
+        case kAccMid: srcs[0] = stage; srcs[1] = m; break;
+        default: srcs[0] = stage; srcs[1] = m; srcs[2] = mine; cnt = 3; break;  // kAccLast
+      }
+      grp_fold<DT, OP>(dst, srcs, cnt, s.len, p, tid, nthr);
+    }
+  }
+}
+
+template <int DT, int OP, int KIND>
+__device__ void pull_role(const KPlan& p, uint64_t base, int R, int lr, int c, Waiter& w) {
+  const int n = p.n, NR = p.nrounds, L = p.skew;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const bool gpu = p.gpu_scope != 0;
+  uint64_t* myflags = chan_flags(p, R, c);
+  // entry: my sendbuf (and, for AG, recvbuf) are final once this stream reached the call
+  if (tid < n && tid != R) st_release(chan_flags(p, tid, c) + 16 + R, base + 1, gpu);
+  if (tid == 0)
+    for (int t = 0; t < NR; ++t) wait_flag(myflags + 16 + (R - p.rounds[t].peer + n) % n, base + 1, w);
+  __syncthreads();
+  auto task = [&](int i, int t) {
+    const Step s = make_step(p, base, i, R, lr, c);
+    if (tid == 0) {
+      // RS: staging buffer s.buf is free once every reader finished step g - depth
+      if (KIND == kRS && ((p.stage_rounds >> t) & 1) && s.g >= static_cast<uint64_t>(p.depth))
+        for (int q = 0; q < n; ++q)
+          if (q != R) wait_flag(myflags + 8 + q, s.g - p.depth + 1, w);
+      if (p.round_dep[t] >= 0) wait_flag(myflags + t, s.g + 1, w);
+    }
+    if constexpr (KIND == kAG) {  // own chunk placement (simulate.cpp:160-165), skipped in place
+      if (t == 0 && p.recv[lr] + R * p.chunk_bytes != p.send[lr]) {
+        const char* src[1] = {p.send[lr] + s.off};
+        grp_fold<DT, OP>(p.recv[lr] + R * p.chunk_bytes + s.off, src, 1, s.len, p, tid, nthr);
+      }
+    }
+    __syncthreads();
+    pull_task<DT, OP, KIND>(p, s, t, tid, nthr);
+  };
+  // after the fence: readers of round t (sig_after) and, after the last round, done(step)
+  auto signal = [&](int i, int t) {
+    const uint64_t g1 = base + i + 1;
+    for (int t2 = 0; t2 < NR; ++t2)
+      if ((p.sig_after[t] >> t2) & 1) st_relaxed(chan_flags(p, (R + p.rounds[t2].peer) % n, c) + t2, g1, gpu);
+    if (t == NR - 1)
+      for (int q = 0; q < n; ++q)
+        if (q != R) st_relaxed(chan_flags(p, q, c) + 8 + R, g1, gpu);
+  };
+  if (L > 0) {  // skewed: round t of step k - t*L in iteration k, one fence per iteration
+    for (int k = 0; k < p.iters + (NR - 1) * L; ++k) {
+      for (int t = 0; t < NR; ++t)
+        if (k - t * L >= 0 && k - t * L < p.iters) task(k - t * L, t);
+      __syncthreads();
+      if (tid == 0) {
+        fence_acq_rel(gpu);
+        for (int t = NR - 1; t >= 0; --t)
+          if (k - t * L >= 0 && k - t * L < p.iters) signal(k - t * L, t);
+      }
+    }
+  } else {
+    for (int i = 0; i < p.iters; ++i)
+      for (int t = 0; t < NR; ++t) {
+        task(i, t);
+        __syncthreads();
+        if (tid == 0) {
+          fence_acq_rel(gpu);
+          signal(i, t);
+        }
+      }
+  }
+  // exit: every reader is done with my buffers (sendbuf, recvbuf, staging) for this call
+  if (tid < n && tid != R) wait_flag(myflags + 8 + tid, base + p.iters, w);
+}
+
+// ------------------------------------------------------------------------- LL128
+// 128-byte lines of 16 words; word 15 is the flag, words 0..14 carry 120 payload bytes (94%
+// wire efficiency against LL's 50%). A warp stores 4 whole lines with ONE st.volatile.v2.u64
+// (lane j of an 8-lane group writes words 2j, 2j+1); NVLink delivers each 128-byte line of a
+// warp store as a unit, so a reader that sees the flag word sees the line (the property NCCL's
+// LL128 protocol rests on). Readers load the line with one warp load and re-poll until the flag
+// lane of every group matches. Lines are forwarded as they are, with the new step's flag.
+constexpr int kLL128Payload = 120;
+
+__device__ __forceinline__ void st_ll128(char* p, uint64_t a, uint64_t b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_ll128(const char* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+// Poll this lane's 16 bytes of line `line` (nullptr lanes are idle) until all four lines of the
+// warp carry `flag` in their word 15.
+__device__ __forceinline__ void poll_ll128(const char* line, int j, uint64_t flag, uint64_t& a, uint64_t& b,
+                                           Waiter& w) {
+  uint64_t start = 0;
+  uint32_t spins = 0;
+  while (true) {
+    bool ok = true;
+    if (line) {
+      ld_ll128(line + 16 * j, a, b);
+      ok = j != 7 || b == flag;
+    }
+    ok = __shfl_sync(0xffffffffu, ok, (threadIdx.x & 31) | 7);
+    if (__all_sync(0xffffffffu, ok) || w.aborted) return;
+    if ((++spins & 1023u) == 0) {
+      const uint64_t now = globaltimer();
+      if (start == 0) start = now;
+      else if (now - start > w.timeout_ns) report_timeout(w);
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t u64of(uint2 v) { return static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32); }
+__device__ __forceinline__ uint2 u2of(uint64_t v) { return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32)); }
+
+template <int DT, int OP>
+__device__ __forceinline__ uint64_t fold64(uint64_t a, uint64_t b) {
+  uint2 x = u2of(a);
+  fold_vec<DT, OP>(x, u2of(b));
+  return u64of(x);
+}
+
+// Payload words of lane j in line L of a slice of `len` bytes starting at `p` (user memory).
+struct LaneWords {
+  int64_t off;   // byte offset of word 0 within the slice
+  int v0, v1;    // valid bytes of word 0 / word 1 (0 = none)
+};
+__device__ __forceinline__ LaneWords lane_words(int64_t L, int j, int64_t len) {
+  LaneWords x;
+  x.off = L * kLL128Payload + 16 * j;
+  x.v0 = static_cast<int>(max(int64_t{0}, min(int64_t{8}, len - x.off)));
+  x.v1 = j == 7 ? 0 : static_cast<int>(max(int64_t{0}, min(int64_t{8}, len - x.off - 8)));
+  return x;
+}
+__device__ __forceinline__ void load_lane(const char* base, const LaneWords& x, const KPlan& p, uint64_t& a,
+                                          uint64_t& b) {
+  a = x.v0 ? u64of(load_word(base + x.off, x.v0, p)) : 0;
+  b = x.v1 ? u64of(load_word(base + x.off + 8, x.v1, p)) : 0;
+}
+__device__ __forceinline__ void store_lane(char* base, const LaneWords& x, const KPlan& p, uint64_t a, uint64_t b) {
+  if (x.v0) store_word(base + x.off, u2of(a), x.v0, p);
+  if (x.v1) store_word(base + x.off + 8, u2of(b), x.v1, p);
+}
+
+template <int DT, int OP, int KIND>
+__device__ void step_ll128(const KPlan& p, const Step& s, Waiter& w) {
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const char* snd = p.send[s.lr];
+  char* out = p.recv[s.lr];
+  const uint64_t flag = s.g + 1;
+  const int64_t nlines = (s.len + kLL128Payload - 1) / kLL128Payload;
+  const int lane = threadIdx.x & 31, j = lane & 7;
+  const int64_t warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // warp-uniform walk over groups of 4 lines; L < 0 marks an idle lane
+  auto for_lines = [&](auto&& body) {
+    for (int64_t l0 = warp * 4; l0 < nlines; l0 += nwarps * 4) {
+      const int64_t L = l0 + (lane >> 3);
+      body(L < nlines ? L : -1);
+    }
+  };
+
+  if constexpr (KIND == kAG) {
+    if (out + s.R * Cb != snd)
+      for_lines([&](int64_t L) {
+        if (L < 0) return;
+        const LaneWords x = lane_words(L, j, s.len);
+        uint64_t a, b;
+        load_lane(snd + s.off, x, p, a, b);
+        store_lane(out + s.R * Cb + s.off, x, p, a, b);
+      });
+  }
+  for (int t = 0; t < p.nrounds; ++t) {
+    const KRound& r = p.rounds[t];
+    const int P = (s.R + r.peer) % n;
+    for (int pos = 0; pos < r.nchunks; ++pos) {
+      char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
+      if constexpr (KIND == kAG) {
+        const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
+        for_lines([&](int64_t L) {
+          uint64_t a = 0, b = 0;
+          if (fwd) {
+            poll_ll128(L >= 0 ? fwd + 128 * L : nullptr, j, flag, a, b, w);
+          } else if (L >= 0) {
+            load_lane(snd + s.off, lane_words(L, j, s.len), p, a, b);
+          }
+          if (L >= 0) st_ll128(dst + 128 * L + 16 * j, a, j == 7 ? flag : b);
+        });
+      } else {
+        const int dest = (s.R - r.chunk[pos] + n) % n;
+        const char* own = snd + dest * Cb + s.off;
+        const int na = r.narr[pos];
+        for_lines([&](int64_t L) {
+          uint64_t a = 0, b = 0;
+          if (na == 0) {
+            if (L >= 0) load_lane(own, lane_words(L, j, s.len), p, a, b);
+          } else {
+            poll_ll128(L >= 0 ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) + 128 * L : nullptr, j, flag, a, b, w);
+            for (int q = 1; q < na; ++q) {
+              uint64_t a2 = 0, b2 = 0;
+              poll_ll128(L >= 0 ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][q]) + 128 * L : nullptr, j, flag, a2, b2, w);
+              a = fold64<DT, OP>(a, a2);
+              b = fold64<DT, OP>(b, b2);
+            }
+            if (L >= 0) {
+              uint64_t a2, b2;
+              load_lane(own, lane_words(L, j, s.len), p, a2, b2);
+              a = fold64<DT, OP>(a, a2);
+              b = fold64<DT, OP>(b, b2);
+            }
+          }
+          if (L >= 0) st_ll128(dst + 128 * L + 16 * j, a, j == 7 ? flag : b);
+        });
+      }
+    }
+  }
+  if constexpr (KIND == kAG) {
+    for (int q = 0; q < p.nslots; ++q) {
+      const int origin = (s.R - p.slot_offset[q] + n) % n;
+      const char* slot = slot_ptr(p, s.R, s.c, s.buf, q);
+      for_lines([&](int64_t L) {
+        uint64_t a = 0, b = 0;
+        poll_ll128(L >= 0 ? slot + 128 * L : nullptr, j, flag, a, b, w);
+        if (L >= 0) store_lane(out + origin * Cb + s.off, lane_words(L, j, s.len), p, a, b);
+      });
+    }
+  } else {
+    for_lines([&](int64_t L) {
+      uint64_t a = 0, b = 0;
+      const LaneWords x = lane_words(L < 0 ? 0 : L, j, s.len);
+      if (L >= 0) load_lane(snd + s.R * Cb + s.off, x, p, a, b);
+      for (int f = 0; f < p.nfin; ++f) {
+        uint64_t a2 = 0, b2 = 0;
+        poll_ll128(L >= 0 ? slot_ptr(p, s.R, s.c, s.buf, p.fin[f]) + 128 * L : nullptr, j, flag, a2, b2, w);
+        a = fold64<DT, OP>(a, a2);
+        b = fold64<DT, OP>(b, b2);
+      }
+      if (L >= 0) store_lane(out + s.off, x, p, a, b);
+    });
+  }
+}
+
+template <int DT, int OP, int KIND>
+__global__ void __launch_bounds__(1024) pat_kernel(const __grid_constant__ KPlan p) {
+  const int lr = blockIdx.x / p.channels;
+  const int c = blockIdx.x - lr * p.channels;
+  const int R = p.rank[lr];
+  __shared__ uint64_t s_base;
+  __shared__ volatile uint64_t s_sent;
+  if (threadIdx.x == 0) {
+    s_base = p.iter_state[lr][c];
+    s_sent = 0;
+  }
+  __syncthreads();
+  const uint64_t base = s_base;
+  Waiter w{p.timeout_ns, p.err, false, p.gpu_scope != 0};
+
+  if (p.direct && KIND == kAG) {
+    // entry handshake: a peer may be written directly only once it entered this call
+    if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
+      st_release(chan_flags(p, threadIdx.x, c) + 16 + R, base + 1, w.gpu);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < p.npeers; ++k)
+        wait_flag(chan_flags(p, R, c) + 16 + (R + p.peers[k]) % p.n, base + 1, w);
+    __syncthreads();
+  }
+
+  if (p.proto == kProtoPull) {
+    pull_role<DT, OP, KIND>(p, base, R, lr, c, w);
+  } else if (p.proto == kProtoLL || p.proto == kProtoLL128) {
+    for (int i = 0; i < p.iters; ++i) {
+      const Step s = make_step(p, base, i, R, lr, c);
+      if (threadIdx.x == 0) wait_credits(p, s, w);
+      __syncthreads();
+      if (p.proto == kProtoLL) step_ll<DT, OP, KIND>(p, s, w);
+      else step_ll128<DT, OP, KIND>(p, s, w);
+      __syncthreads();
+      // done(step): every load of this step's inbox has returned (its value was consumed before
+      // the barrier), so a relaxed store suffices to hand the buffers back
+      if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
+        st_relaxed(chan_flags(p, threadIdx.x, c) + 8 + R, s.g + 1, w.gpu);
+    }
+  } else {
+    const int nsend = p.send_warps * 32;
+    if (static_cast<int>(threadIdx.x) < nsend) {
+      send_role<DT, OP, KIND>(p, base, R, lr, c, w, threadIdx.x, nsend, &s_sent);
+    } else {
+      const int tid = threadIdx.x - nsend, nrecv = blockDim.x - nsend;
+      Tracer tr;
+      if (tid == 0) tr.init(p, 1);
+      tr.rec(kEvStart, base, 0);
+      for (int i = 0; i < p.iters; ++i) {
+        const Step s = make_step(p, base, i, R, lr, c);
+        recv_step<DT, OP, KIND>(p, s, w, tid, nrecv, &s_sent, tr);
+      }
+      tr.rec(kEvEnd, base + p.iters, 0);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) p.iter_state[lr][c] = base + p.iters;
+}
+
+}  // namespace pat

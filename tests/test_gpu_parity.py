@@ -198,7 +198,7 @@ def test_reduce_scatter_ops(op, dt, executor):
             assert same(got[r], want[r]), (op, dt, n, r)
 
 
-@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_SIMPLE])
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
 def test_protocols_forced(proto):
     for n in (2, 5, 8):
         comm = comm_for(n, protocol=proto, fused=-1)
@@ -367,3 +367,61 @@ def test_multi_gpu_parity(n):
 def test_no_async_error_left():
     for c in _COMMS.values():
         assert c.async_error() == 0
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
+@pytest.mark.parametrize("n", [2, 3, 4, 6, 8])
+def test_multi_gpu_bulk_protocols(n, proto):
+    """SIMPLE (pushed slices through the inboxes) and PULL (receivers read the peers' buffers)
+    across NVLink, with a small pool so reduce-scatter staging credits cycle many times."""
+    devices = list(range(n)) if n <= NGPU else [r % NGPU for r in range(n)]
+    comm = comm_for(n, devices, protocol=proto, staging_bytes=n * 256 * 1024, channels=8)
+    for elems in (3, 70001, 600000):
+        p = O.random_payload(O.FLOAT32, n, elems, elems + n)
+        got = gpu_allgather(comm, devices, p, elems, O.FLOAT32)
+        want = oracle_ag(n, O.max_trees(n), O.FLOAT32, p, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (n, elems)
+        for dt, op in ((O.BFLOAT16, O.SUM), (O.FLOAT32, O.SUM), (O.INT32, O.MAX)):
+            q = O.random_payload(dt, n * n, elems, elems + 5)
+            got = gpu_reduce_scatter(comm, devices, q, elems, dt, op)
+            want = oracle_rs(n, O.max_trees(n), dt, op, q, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (n, elems, dt, op)
+
+
+@pytest.mark.parametrize("trees", [1, 2])
+def test_pull_single_tree_schedules(trees):
+    """PULL with T < max_trees: more rounds than pipeline buffers (no skew), same results."""
+    n = 8
+    comm = comm_for(n, protocol=_lib.PROTO_PULL, fused=-1, trees=trees, staging_bytes=n * 128 * 1024, channels=4)
+    for elems in (5, 100003):
+        p = O.random_payload(O.INT32, n, elems, 21)
+        got = gpu_allgather(comm, [0] * n, p, elems, O.INT32)
+        want = oracle_ag(n, trees, O.INT32, p, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (trees, elems)
+        q = O.random_payload(O.FLOAT32, n * n, elems, 22)
+        got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.FLOAT32, O.SUM)
+        want = oracle_rs(n, trees, O.FLOAT32, O.SUM, q, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (trees, elems)
+
+
+def test_protocol_switches_share_no_inbox_state():
+    """One communicator whose calls alternate LL / LL128 / bulk by size: the polling protocols
+    have their own inbox regions, so payload words a bulk protocol left behind can never pass
+    for a flag. The int32 payload holds small step-counter-like values to make a collision
+    likely if the regions were shared."""
+    n = 4
+    comm = comm_for(n, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=4096,
+                    ll128_threshold=40000)
+    for it in range(16):
+        elems = [200, 5000, 60000, 3000][it % 4]  # LL, LL128, bulk, LL128 (4-byte elements)
+        p = (np.arange(n * elems, dtype=np.int64) % 64 + 1 + it).astype(np.int32)
+        got = gpu_allgather(comm, [0] * n, p, elems, O.INT32)
+        want = oracle_ag(n, O.max_trees(n), O.INT32, p, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (it, elems)
+        q = (np.arange(n * n * elems, dtype=np.int64) % 64 + it).astype(np.int32)
+        got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.INT32, O.SUM)
+        want = oracle_rs(n, O.max_trees(n), O.INT32, O.SUM, q, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (it, elems)
+    plans = [comm.plan(0, e, O.INT32)["protocol"] for e in (200, 5000, 60000)]
+    assert plans == [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_PULL], plans

@@ -1,0 +1,149 @@
+// bidir_probe.cu — NVLink ceilings under the traffic pattern of a collective: every GPU sends
+// and receives at the same time. Not part of the product; it sets the roofline the PAT
+// transport is judged against.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/bidir_probe.cu -o tools/bidir_probe
+//   tools/bidir_probe [ngpus]
+//
+// Patterns (G GPUs, one process, peer access, 1 GiB per GPU, all GPUs launched together):
+//   ring-push  GPU i stores into GPU i+1      (every GPU sends 1 GiB and receives 1 GiB)
+//   ring-pull  GPU i loads from GPU i-1
+//   spread-push GPU i stores 1/(G-1) of its buffer into each peer
+//   ce-ring    cudaMemcpyPeerAsync i -> i+1 (copy engines)
+//   uni-push / uni-pull  only GPU 0 -> GPU 1 (the one-directional reference numbers)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e = (x);                                                                   \
+    if (e != cudaSuccess) {                                                                \
+      std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      std::exit(1);                                                                        \
+    }                                                                                      \
+  } while (0)
+
+template <int U>
+__global__ void __launch_bounds__(512) copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                   size_t n16) {
+  size_t B = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * B < n16; i += U * B) {
+    uint4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) v[k] = src[i + k * B];
+#pragma unroll
+    for (int k = 0; k < U; ++k) dst[i + k * B] = v[k];
+  }
+  for (; i < n16; i += B) dst[i] = src[i];
+}
+
+// Contiguous per-CTA ranges (the transport's slice layout) instead of a grid-stride.
+template <int U>
+__global__ void __launch_bounds__(512) copy_blocked(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                    size_t n16) {
+  const size_t per = (n16 + gridDim.x - 1) / gridDim.x;
+  const size_t beg = per * blockIdx.x, end = beg + per < n16 ? beg + per : n16;
+  const size_t B = blockDim.x;
+  size_t i = beg + threadIdx.x;
+  for (; i + (U - 1) * B < end; i += U * B) {
+    uint4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) v[k] = src[i + k * B];
+#pragma unroll
+    for (int k = 0; k < U; ++k) dst[i + k * B] = v[k];
+  }
+  for (; i < end; i += B) dst[i] = src[i];
+}
+
+int main(int argc, char** argv) {
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  const int G = argc > 1 ? std::atoi(argv[1]) : ndev;
+  if (G < 2 || G > ndev) {
+    std::printf("need >= 2 GPUs (have %d)\n", ndev);
+    return 0;
+  }
+  const size_t bytes = 1ull << 30, n16 = bytes / 16;
+  std::vector<char*> src(G), dst(G);
+  std::vector<cudaStream_t> st(G);
+  std::vector<cudaEvent_t> e0(G), e1(G);
+  for (int d = 0; d < G; ++d) {
+    CK(cudaSetDevice(d));
+    for (int p = 0; p < G; ++p)
+      if (p != d) CK(cudaDeviceEnablePeerAccess(p, 0));
+    CK(cudaMalloc(&src[d], bytes));
+    CK(cudaMalloc(&dst[d], bytes));
+    CK(cudaMemset(src[d], d + 1, bytes));
+    CK(cudaStreamCreateWithFlags(&st[d], cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e0[d]));
+    CK(cudaEventCreate(&e1[d]));
+  }
+  // run fn(d) on every active device, timed per device; returns GB/s received per GPU (min over GPUs)
+  auto run = [&](const char* name, int active, auto fn, size_t per_gpu_bytes) {
+    for (int rep = 0; rep < 2; ++rep) {  // rep 0 = warm-up
+      for (int d = 0; d < G; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaDeviceSynchronize());
+      }
+      for (int d = 0; d < active; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaEventRecord(e0[d], st[d]));
+        for (int r = 0; r < 3; ++r) fn(d);
+        CK(cudaEventRecord(e1[d], st[d]));
+      }
+      if (rep == 0) continue;
+      double worst = 1e30;
+      for (int d = 0; d < active; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaEventSynchronize(e1[d]));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0[d], e1[d]));
+        const double gbs = 3.0 * per_gpu_bytes / (ms / 1e3) / 1e9;
+        worst = gbs < worst ? gbs : worst;
+      }
+      std::printf("%-34s G=%d: %7.1f GB/s per GPU per direction\n", name, active, worst);
+      std::fflush(stdout);
+    }
+  };
+  for (int grid : {128, 148, 296}) {
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "uni-push grid %d", grid);
+    run(nm, 1, [&](int d) { copy_kernel<8><<<grid, 512, 0, st[d]>>>((const uint4*)src[0], (uint4*)dst[1], n16); }, bytes);
+    std::snprintf(nm, sizeof nm, "uni-pull grid %d", grid);
+    run(nm, 1, [&](int d) { copy_kernel<8><<<grid, 512, 0, st[d]>>>((const uint4*)src[1], (uint4*)dst[0], n16); }, bytes);
+    std::snprintf(nm, sizeof nm, "ring-push grid %d", grid);
+    run(nm, G, [&](int d) {
+      copy_kernel<8><<<grid, 512, 0, st[d]>>>((const uint4*)src[d], (uint4*)dst[(d + 1) % G], n16);
+    }, bytes);
+    std::snprintf(nm, sizeof nm, "ring-push-blocked grid %d", grid);
+    run(nm, G, [&](int d) {
+      copy_blocked<8><<<grid, 512, 0, st[d]>>>((const uint4*)src[d], (uint4*)dst[(d + 1) % G], n16);
+    }, bytes);
+    std::snprintf(nm, sizeof nm, "ring-pull grid %d", grid);
+    run(nm, G, [&](int d) {
+      copy_kernel<8><<<grid, 512, 0, st[d]>>>((const uint4*)src[(d + G - 1) % G], (uint4*)dst[d], n16);
+    }, bytes);
+    if (G > 2) {
+      std::snprintf(nm, sizeof nm, "spread-push grid %d", grid);
+      const size_t part = (n16 / (G - 1)) & ~size_t(15);
+      run(nm, G, [&](int d) {
+        for (int k = 1; k < G; ++k)
+          copy_kernel<8><<<grid / (G - 1), 512, 0, st[d]>>>((const uint4*)src[d] + (k - 1) * part,
+                                                            (uint4*)dst[(d + k) % G] + (k - 1) * part, part);
+      }, part * 16 * (G - 1));
+    }
+  }
+  for (int d = 0; d < G; ++d) {  // copy engines
+    CK(cudaSetDevice(d));
+  }
+  run("ce-uni", 1, [&](int d) { CK(cudaMemcpyPeerAsync(dst[1], 1, src[0], 0, bytes, st[d])); }, bytes);
+  run("ce-ring", G, [&](int d) { CK(cudaMemcpyPeerAsync(dst[(d + 1) % G], (d + 1) % G, src[d], d, bytes, st[d])); },
+      bytes);
+  std::printf("done\n");
+  return 0;
+}

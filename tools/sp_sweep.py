@@ -19,14 +19,17 @@ def main():
     ap.add_argument("--max-bytes", type=int, default=1 << 30)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--direct", type=int, default=0)
+    ap.add_argument("--protocol", type=int, default=0, help="0 auto, 1 LL, 2 SIMPLE, 3 PULL")
+    ap.add_argument("--gpus", type=int, default=0, help="ranks = first N GPUs (default all)")
+    ap.add_argument("--tag", default="")
     args = ap.parse_args()
     import torch
 
     from paper_2506_20252_b200 import FLOAT32, SUM, PatComm
 
-    n = torch.cuda.device_count()
-    comm = PatComm.init_all(n, list(range(n)), direct=args.direct)
-    out = open(args.out, "w")
+    n = args.gpus or torch.cuda.device_count()
+    comm = PatComm.init_all(n, list(range(n)), direct=args.direct, protocol=args.protocol)
+    out = open(args.out, "a")
     C = args.min_bytes
     while C <= args.max_bytes:
         elems = C // 4
@@ -57,7 +60,7 @@ def main():
             us = max(a.elapsed_time(b) for a, b in ev) * 1e3 / args.iters
             rec = {"coll": coll, "impl": "pat-sp", "n": n, "dtype": "f32", "bytes_per_rank": C, "us": us,
                    "busbw_gbs": (n - 1) * C / (us * 1e-6) / 1e9, "plan": comm.plan(0 if coll == "ag" else 1, elems, FLOAT32),
-                   "direct": args.direct}
+                   "direct": args.direct, "protocol": args.protocol, "tag": args.tag}
             out.write(json.dumps(rec) + "\n")
             out.flush()
             del s, r
