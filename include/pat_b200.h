@@ -97,13 +97,9 @@ typedef enum { patAlgoRing = 0, patAlgoBruckNearest = 1, patAlgoBruckFarthest = 
    PULL: receivers read the upstream's buffers (user sendbuf / recvbuf, staged RS partials);
    needs every rank's user buffers mapped in this process (patCommInitAll, cudaMalloc memory).
    LL128: 128-byte lines carrying 120 payload bytes and a flag word (mid-size chunks).
-   CE: the copy engines move the slices (cudaMemcpyAsync between peers), SM kernels fold; events
-   order the rounds. Single-process communicators with one rank per device only.
-   Auto: LL up to ll_threshold, LL128 up to ll128_threshold, CE from ce_threshold where possible,
-   then PULL where possible, else SIMPLE. */
-typedef enum {
-  patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3, patProtoLL128 = 4, patProtoCE = 5
-} patProtocol_t;
+   Auto: LL up to ll_threshold, LL128 up to ll128_threshold, then SIMPLE — except reduce-scatter
+   below 128 MiB, which PULLs where possible (measured, profiles/r01_sp_simple_vs_pull.jsonl). */
+typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3, patProtoLL128 = 4 } patProtocol_t;
 
 typedef struct {
   size_t size;              /* sizeof(patConfig_t) */
@@ -125,8 +121,6 @@ typedef struct {
                                write of every output, same fold tree as the schedule) */
   size_t ll128_threshold;   /* per-rank chunk bytes up to which LL128 is used (above ll_threshold);
                                0 = default */
-  size_t ce_threshold;      /* per-rank chunk bytes from which CE is used; 0 = default,
-                               SIZE_MAX = never */
 } patConfig_t;
 
 /* Plan the library would launch for one call (introspection / benchmarks). */

@@ -22,7 +22,6 @@
 #include <vector>
 
 #include "../../include/pat_b200.h"
-#include "ce.hpp"
 #include "plan.hpp"
 #include "schedule.hpp"
 
@@ -46,13 +45,13 @@ constexpr size_t kDefaultPoolBytes = 512ull << 20;  // inbox pool budget per ran
 constexpr size_t kMinSlice = 64 << 10, kMaxSlice = 256 << 10;
 constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
 // Protocol crossovers measured on B200 (profiles/r01_ll128_*.jsonl, graph mode, n = 2 and 4):
-// LL wins to 256 KiB, LL128 to 4 MiB, then the bulk protocols; CE from 64 MiB (single process).
+// LL wins to 256 KiB, LL128 to 4 MiB, then the bulk protocols (SIMPLE; PULL for mid-size RS).
 constexpr size_t kDefaultLL = 256 << 10;
 constexpr size_t kDefaultLL128 = 4 << 20;
-constexpr size_t kDefaultCE = 64 << 20;
+constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
 constexpr size_t kLLSlotBytes = 16 << 10;     // LL slot: 8 KiB payload per channel-step
 constexpr size_t kLL128SlotBytes = 32 << 10;  // LL128 slot: 30 KiB payload per channel-step
-constexpr int64_t kCeSliceMin = 8 << 20, kCeSliceMaxAG = 64 << 20, kCeSliceMaxRS = 16 << 20;
+
 constexpr int64_t kLL128PayloadBytes = 120;  // per 128-byte line (transport.cuh)
 constexpr int kDefaultTimeoutMs = 20000;
 
@@ -104,9 +103,7 @@ struct patComm {
   size_t slot_bytes = 0, pool_bytes = 0;
   size_t ll_slot_bytes = 0, ll128_slot_bytes = 0;  // LL / LL128 inbox slots (own regions, common_init)
   size_t region_off[5] = {};               // inbox region of each protocol within a pool
-  std::unique_ptr<CeState> ce;             // copy-engine executor (single process, created on first use)
   int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
-  int64_t ce_slice = 0;    // copy-engine slice override (PAT_CE_SLICE; 0 = automatic)
   int channels = 0;
   int* err_host = nullptr;
   int* err_dev = nullptr;
@@ -192,7 +189,6 @@ void fill_defaults(patConfig_t* c, int n) {
   }
   if (c->ll_threshold == 0) c->ll_threshold = env_int("PAT_LL_THRESHOLD", &v) ? (size_t)v : kDefaultLL;
   if (c->ll128_threshold == 0) c->ll128_threshold = env_int("PAT_LL128_THRESHOLD", &v) ? (size_t)v : kDefaultLL128;
-  if (c->ce_threshold == 0) c->ce_threshold = env_int("PAT_CE_THRESHOLD", &v) ? (size_t)v : kDefaultCE;
   if (c->timeout_ms <= 0) c->timeout_ms = env_int("PAT_TIMEOUT_MS", &v) ? (int)v : kDefaultTimeoutMs;
   if (c->protocol == patProtoAuto && env_int("PAT_PROTOCOL", &v)) c->protocol = (int)v;
   if (c->threads <= 0) c->threads = env_int("PAT_THREADS", &v) ? (int)v : 512;
@@ -372,34 +368,20 @@ struct Slicing {
   int64_t slice;
 };
 
-// The copy-engine executor needs one process that owns every rank, each on its own device.
-bool ce_capable(const patComm* comm) {
-  return !comm->multiprocess && static_cast<int>(comm->groups.size()) == comm->n && comm->n > 1;
-}
-
 Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int max_channels, bool pull_ok) {
   Slicing s{};
   const int channels = std::max(1, std::min(comm->channels, max_channels));
   int proto = comm->cfg.protocol;
-  const bool ce_ok = ce_capable(comm);
   if (proto == patProtoAuto)
     proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold)      ? kProtoLL
             : chunk_bytes <= static_cast<int64_t>(comm->cfg.ll128_threshold) ? kProtoLL128
-            : ce_ok && chunk_bytes >= static_cast<int64_t>(comm->cfg.ce_threshold) ? kProtoCE
-            : pull_ok                                                        ? kProtoPull
+            // reduce-scatter reads faster than it pushes between 4 and 128 MiB (the receiver
+            // folds what it pulls, no inbox round trip); beyond that, and for all-gather,
+            // pushed stores win (profiles/r01_sp_simple_vs_pull.jsonl)
+            : pull_ok && kind == kRS && chunk_bytes < kPullMaxRS             ? kProtoPull
                                                                              : kProtoSimple;
   if (proto == kProtoPull && !pull_ok) proto = kProtoSimple;
-  if (proto == kProtoCE && !ce_ok) proto = pull_ok ? kProtoPull : kProtoSimple;
   s.proto = proto;
-  if (proto == kProtoCE) {  // ~16 slices through the PAT rounds, each a large copy
-    const int64_t hi = kind == kAG ? kCeSliceMaxAG : kCeSliceMaxRS;
-    int64_t sl = comm->ce_slice ? comm->ce_slice : std::min(hi, std::max(kCeSliceMin, (chunk_bytes + 15) / 16));
-    sl = (sl + 255) & ~int64_t(255);
-    s.slice = std::min<int64_t>(sl, (chunk_bytes + 255) & ~int64_t(255));
-    s.channels = 1;
-    s.iters = static_cast<int>((chunk_bytes + s.slice - 1) / s.slice);
-    return s;
-  }
   int64_t cap = proto == kProtoLL      ? static_cast<int64_t>(comm->ll_slot_bytes / 2)
                 : proto == kProtoLL128 ? static_cast<int64_t>(comm->ll128_slot_bytes / 128 * kLL128PayloadBytes)
                                        : static_cast<int64_t>(comm->slot_bytes);
@@ -458,7 +440,6 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   {
     long long v = 0;
     comm->pull_slice = env_int("PAT_PULL_SLICE", &v) && v >= 256 ? (v & ~15LL) : (512 << 10);
-    comm->ce_slice = env_int("PAT_CE_SLICE", &v) && v >= 256 ? (v & ~255LL) : 0;
   }
   const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
   // Inbox regions: SIMPLE/PULL slots, then LL and LL128 slots. The polling protocols get their
@@ -567,34 +548,6 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       direct = true;
       for (size_t l = 0; l < comm->lranks.size() && direct; ++l) direct = legacy_ipc_capable(recvbuffs[l]);
     }
-  }
-  if (sl.proto == kProtoCE) {
-    if (!comm->ce) {
-      comm->ce = std::make_unique<CeState>();
-      std::vector<int> devs(n);
-      for (size_t l = 0; l < comm->lranks.size(); ++l) devs[comm->lranks[l]] = comm->ldevs[l];
-      if (int e = ce_init(*comm->ce, n, devs.data(), kMaxRounds)) {
-        std::fprintf(stderr, "pat_b200: copy-engine executor init failed: %s\n",
-                     cudaGetErrorString(static_cast<cudaError_t>(e)));
-        comm->ce.reset();
-        return patUnhandledCudaError;
-      }
-    }
-    const char* sb[kMaxRanks];
-    char* rb[kMaxRanks];
-    cudaStream_t ss[kMaxRanks];
-    for (size_t l = 0; l < comm->lranks.size(); ++l) {
-      const int r = comm->lranks[l];
-      sb[r] = static_cast<const char*>(sendbuffs[l]);
-      rb[r] = static_cast<char*>(recvbuffs[l]);
-      ss[r] = streams ? reinterpret_cast<cudaStream_t>(streams[l]) : nullptr;
-    }
-    CeCall call{kind, dtype, op, aligned16 ? 16 : 0, static_cast<int>(es), chunk_bytes, sl.slice, &cp->proto, sb, rb, ss};
-    if (int e = ce_run(*comm->ce, call)) {
-      std::fprintf(stderr, "pat_b200: copy-engine executor: %s\n", cudaGetErrorString(static_cast<cudaError_t>(e)));
-      return patUnhandledCudaError;
-    }
-    return patSuccess;
   }
   for (DevGroup& g : comm->groups) {
     KPlan p = cp->proto;
@@ -841,7 +794,6 @@ patResult_t patCommDestroy(patComm_t comm) {
       cudaSetDevice(comm->ldevs[l]);
       cudaDeviceSynchronize();
     }
-    if (comm->ce) ce_destroy(*comm->ce);
     for (DevGroup& g : comm->groups) {
       cudaSetDevice(g.device);
       for (void* p : comm->ipc_opened) cudaIpcCloseMemHandle(p);

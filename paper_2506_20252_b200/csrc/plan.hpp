@@ -18,7 +18,7 @@ constexpr int kMaxChannels = 128;
 constexpr int kFlagWords = 32;  // per channel: data flag per round [0,8), done-from per rank [8,16),
                                 // ready-from per rank [16,24) (direct mode entry handshake)
 
-enum Proto : int { kProtoLL = 1, kProtoSimple = 2, kProtoPull = 3, kProtoLL128 = 4, kProtoCE = 5 };
+enum Proto : int { kProtoLL = 1, kProtoSimple = 2, kProtoPull = 3, kProtoLL128 = 4 };
 
 // PULL reduce-scatter: what a rank does with the arrival it pulled into slot j.
 enum PullAct : int8_t {

@@ -651,11 +651,25 @@ __device__ void pull_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
 // lane of every group matches. Lines are forwarded as they are, with the new step's flag.
 constexpr int kLL128Payload = 120;
 
-__device__ __forceinline__ void st_ll128(char* p, uint64_t a, uint64_t b) {
-  asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+// The line's 16 bytes per lane must leave (and be read) in ONE warp-wide instruction: a warp
+// that diverged before the store would write the flag lane's word separately from the data
+// lanes' words (a torn line: measured on B200 with element-granular loads before the store).
+// So every LL128 access is issued convergent (__syncwarp) by all 32 lanes, idle lanes masked
+// by a predicate inside the instruction.
+__device__ __forceinline__ void st_ll128(char* p, uint64_t a, uint64_t b, bool active) {
+  __syncwarp();
+  asm volatile(
+      "{ .reg .pred q; setp.ne.u32 q, %3, 0; @q st.volatile.global.v2.u64 [%0], {%1,%2}; }" ::"l"(p), "l"(a),
+      "l"(b), "r"(static_cast<uint32_t>(active))
+      : "memory");
 }
-__device__ __forceinline__ void ld_ll128(const char* p, uint64_t& a, uint64_t& b) {
-  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+__device__ __forceinline__ void ld_ll128(const char* p, uint64_t& a, uint64_t& b, bool active) {
+  __syncwarp();
+  asm volatile(
+      "{ .reg .pred q; setp.ne.u32 q, %3, 0; mov.u64 %0, 0; mov.u64 %1, 0; @q ld.volatile.global.v2.u64 {%0,%1}, [%2]; }"
+      : "=l"(a), "=l"(b)
+      : "l"(p), "r"(static_cast<uint32_t>(active))
+      : "memory");
 }
 
 // Poll this lane's 16 bytes of line `line` (nullptr lanes are idle) until all four lines of the
@@ -665,13 +679,10 @@ __device__ __forceinline__ void poll_ll128(const char* line, int j, uint64_t fla
   uint64_t start = 0;
   uint32_t spins = 0;
   while (true) {
-    bool ok = true;
-    if (line) {
-      ld_ll128(line + 16 * j, a, b);
-      ok = j != 7 || b == flag;
-    }
-    ok = __shfl_sync(0xffffffffu, ok, (threadIdx.x & 31) | 7);
-    if (__all_sync(0xffffffffu, ok) || w.aborted) return;
+    ld_ll128(line ? line + 16 * j : nullptr, a, b, line != nullptr);
+    const bool ok = !line || j != 7 || b == flag;
+    const bool ready = __shfl_sync(0xffffffffu, ok, (threadIdx.x & 31) | 7);
+    if (__all_sync(0xffffffffu, ready) || __any_sync(0xffffffffu, w.aborted)) return;  // warp-uniform exit
     if ((++spins & 1023u) == 0) {
       const uint64_t now = globaltimer();
       if (start == 0) start = now;
@@ -754,7 +765,7 @@ __device__ void step_ll128(const KPlan& p, const Step& s, Waiter& w) {
           } else if (L >= 0) {
             load_lane(snd + s.off, lane_words(L, j, s.len), p, a, b);
           }
-          if (L >= 0) st_ll128(dst + 128 * L + 16 * j, a, j == 7 ? flag : b);
+          st_ll128(dst + 128 * (L < 0 ? 0 : L) + 16 * j, a, j == 7 ? flag : b, L >= 0);
         });
       } else {
         const int dest = (s.R - r.chunk[pos] + n) % n;
@@ -779,7 +790,7 @@ __device__ void step_ll128(const KPlan& p, const Step& s, Waiter& w) {
               b = fold64<DT, OP>(b, b2);
             }
           }
-          if (L >= 0) st_ll128(dst + 128 * L + 16 * j, a, j == 7 ? flag : b);
+          st_ll128(dst + 128 * (L < 0 ? 0 : L) + 16 * j, a, j == 7 ? flag : b, L >= 0);
         });
       }
     }

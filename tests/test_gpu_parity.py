@@ -102,6 +102,17 @@ def gpu_reduce_scatter(comm, devices, payload, elems, dtype, op, pad=0, schedule
     return [keep[2 * r + 1].cpu().numpy()[pad:pad + elems * es].view(payload.dtype) for r in range(n)]
 
 
+def mismatch(got, want, elems):
+    """Where outputs differ: [(rank, first bad element, count, (block, offset) of the first)]."""
+    out = []
+    for r, (g, w) in enumerate(zip(got, want)):
+        d = np.nonzero(g.view(np.uint8) != w.view(np.uint8))[0] // g.itemsize
+        if d.size:
+            out.append((r, int(d[0]), int(np.unique(d).size), divmod(int(d[0]), elems), g[d[:4]].tolist(),
+                        w[d[:4]].tolist()))
+    return out
+
+
 def oracle_ag(n, trees, dtype, payload, elems):
     out, _ = O.run_allgather(O.pat_allgather(n, trees), dtype, payload, elems)
     return out
@@ -378,7 +389,7 @@ def test_no_async_error_left():
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE, _lib.PROTO_PULL, _lib.PROTO_CE])
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
 @pytest.mark.parametrize("n", [2, 3, 4, 6, 8])
 def test_multi_gpu_bulk_protocols(n, proto):
     """SIMPLE (pushed slices through the inboxes) and PULL (receivers read the peers' buffers)
@@ -426,45 +437,11 @@ def test_protocol_switches_share_no_inbox_state():
         p = (np.arange(n * elems, dtype=np.int64) % 64 + 1 + it).astype(np.int32)
         got = gpu_allgather(comm, [0] * n, p, elems, O.INT32)
         want = oracle_ag(n, O.max_trees(n), O.INT32, p, elems)
-        assert all(same(got[r], want[r]) for r in range(n)), (it, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (it, elems, mismatch(got, want, elems))
         q = (np.arange(n * n * elems, dtype=np.int64) % 64 + it).astype(np.int32)
         got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.INT32, O.SUM)
         want = oracle_rs(n, O.max_trees(n), O.INT32, O.SUM, q, elems)
         assert all(same(got[r], want[r]) for r in range(n)), (it, elems)
-    plans = [comm.plan(0, e, O.INT32)["protocol"] for e in (200, 5000, 60000)]
-    assert plans == [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_PULL], plans
-
-
-@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("n", [2, 3, 4])
-def test_copy_engine_many_slices(n, monkeypatch):
-    """CE executor with small slices: many slices in flight through the skewed event pipeline,
-    inbox/staging reuse across slices and across calls, every dtype class and op."""
-    if n > NGPU:
-        pytest.skip("needs one GPU per rank")
-    monkeypatch.setenv("PAT_CE_SLICE", str(64 * 1024))
-    devices = list(range(n))
-    comm = PatComm.init_all(n, devices, protocol=_lib.PROTO_CE)
-    try:
-        assert comm.plan(1, 300000, O.FLOAT32)["protocol"] == _lib.PROTO_CE
-        for rep in range(2):
-            for elems in (1, 4097, 300000):
-                p = O.random_payload(O.FLOAT32, n, elems, elems + rep)
-                got = gpu_allgather(comm, devices, p, elems, O.FLOAT32)
-                want = oracle_ag(n, O.max_trees(n), O.FLOAT32, p, elems)
-                assert all(same(got[r], want[r]) for r in range(n)), (n, elems)
-                got = gpu_allgather(comm, devices, p, elems, O.FLOAT32, inplace=True)
-                assert all(same(got[r], want[r]) for r in range(n)), (n, elems, "inplace")
-                for dt, op in ((O.BFLOAT16, O.SUM), (O.FLOAT32, O.SUM), (O.INT32, O.MAX), (O.FLOAT16, O.MIN)):
-                    q = O.random_payload(dt, n * n, elems, elems + 9 + rep)
-                    got = gpu_reduce_scatter(comm, devices, q, elems, dt, op)
-                    want = oracle_rs(n, O.max_trees(n), dt, op, q, elems)
-                    assert all(same(got[r], want[r]) for r in range(n)), (n, elems, dt, op)
-        for dt in (O.FLOAT16, O.INT8):  # not 16-byte aligned: element-granular folds
-            q = O.random_payload(dt, n * n, 1001, 5)
-            got = gpu_reduce_scatter(comm, devices, q, 1001, dt, O.SUM, pad=2 if dt == O.FLOAT16 else 1)
-            want = oracle_rs(n, O.max_trees(n), dt, O.SUM, q, 1001)
-            assert all(same(got[r], want[r]) for r in range(n)), (n, dt)
-        assert comm.async_error() == 0
-    finally:
-        comm.destroy()
+    plans = [comm.plan(k, e, O.INT32)["protocol"] for k in (0, 1) for e in (200, 5000, 60000)]
+    assert plans == [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE,
+                     _lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_PULL], plans

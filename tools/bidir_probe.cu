@@ -2,7 +2,7 @@
 // and receives at the same time. Not part of the product; it sets the roofline the PAT
 // transport is judged against.
 //
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/bidir_probe.cu -o tools/bidir_probe
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/bidir_probe.cu -o tools/bidir_probe -lcuda
 //   tools/bidir_probe [ngpus]
 //
 // Patterns (G GPUs, one process, peer access, 1 GiB per GPU, all GPUs launched together):
@@ -11,6 +11,7 @@
 //   spread-push GPU i stores 1/(G-1) of its buffer into each peer
 //   ce-ring    cudaMemcpyPeerAsync i -> i+1 (copy engines)
 //   uni-push / uni-pull  only GPU 0 -> GPU 1 (the one-directional reference numbers)
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -140,6 +141,52 @@ int main(int argc, char** argv) {
   }
   for (int d = 0; d < G; ++d) {  // copy engines
     CK(cudaSetDevice(d));
+  }
+  // the copy-engine executor's shapes: 16 slices per call, cudaMemcpyAsync(Default) vs Peer,
+  // on the legacy default stream vs a non-blocking stream
+  const size_t sl = bytes / 16;
+  run("ce-ring-16slices-peer", G, [&](int d) {
+    for (int s = 0; s < 16; ++s)
+      CK(cudaMemcpyPeerAsync(dst[(d + 1) % G] + s * sl, (d + 1) % G, src[d] + s * sl, d, sl, st[d]));
+  }, bytes);
+  run("ce-ring-16slices-default", G, [&](int d) {
+    for (int s = 0; s < 16; ++s)
+      CK(cudaMemcpyAsync(dst[(d + 1) % G] + s * sl, src[d] + s * sl, sl, cudaMemcpyDefault, st[d]));
+  }, bytes);
+  {
+    std::vector<cudaEvent_t> ev(G * 16);
+    for (int d = 0; d < G; ++d) {
+      CK(cudaSetDevice(d));
+      for (int s = 0; s < 16; ++s) CK(cudaEventCreateWithFlags(&ev[d * 16 + s], cudaEventDisableTiming));
+    }
+    run("ce-ring-16slices-events", G, [&](int d) {
+      for (int s = 0; s < 16; ++s) {
+        CK(cudaMemcpyAsync(dst[(d + 1) % G] + s * sl, src[d] + s * sl, sl, cudaMemcpyDefault, st[d]));
+        CK(cudaEventRecord(ev[d * 16 + s], st[d]));
+        if (s > 0) CK(cudaStreamWaitEvent(st[d], ev[((d + G - 1) % G) * 16 + s - 1], 0));
+      }
+    }, bytes);
+  }
+  {  // the same dependency chain through stream memory operations on peer-mapped flags
+    std::vector<uint32_t*> flag(G);
+    for (int d = 0; d < G; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaMalloc(&flag[d], 4096));
+      CK(cudaMemset(flag[d], 0, 4096));
+    }
+    std::vector<uint32_t> calls(G, 0);
+    run("ce-ring-16slices-streamvalue", G, [&](int d) {
+      const uint32_t epoch = ++calls[d];  // the k-th call of every device pairs with its upstream's k-th
+      for (int s = 0; s < 16; ++s) {
+        CK(cudaMemcpyAsync(dst[(d + 1) % G] + s * sl, src[d] + s * sl, sl, cudaMemcpyDefault, st[d]));
+        // tell the downstream GPU slice s landed; wait until my upstream's slice s-1 landed
+        if (cuStreamWriteValue32(st[d], (CUdeviceptr)(flag[(d + 1) % G]), epoch * 16 + s + 1, 0) != CUDA_SUCCESS)
+          std::printf("writevalue failed\n");
+        if (s > 0 &&
+            cuStreamWaitValue32(st[d], (CUdeviceptr)(flag[d]), epoch * 16 + s, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+          std::printf("waitvalue failed\n");
+      }
+    }, bytes);
   }
   run("ce-uni", 1, [&](int d) { CK(cudaMemcpyPeerAsync(dst[1], 1, src[0], 0, bytes, st[d])); }, bytes);
   run("ce-ring", G, [&](int d) { CK(cudaMemcpyPeerAsync(dst[(d + 1) % G], (d + 1) % G, src[d], d, bytes, st[d])); },
