@@ -447,9 +447,12 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   comm->ll_slot_bytes = std::max<size_t>(256, std::min<size_t>(kLLSlotBytes, comm->slot_bytes) & ~size_t(127));
   comm->ll128_slot_bytes = std::max<size_t>(256, std::min<size_t>(kLL128SlotBytes, comm->slot_bytes) & ~size_t(127));
   const size_t nslots = static_cast<size_t>(comm->channels) * c.depth * slots;
+  // Regions start 4 KiB aligned: an LL128 line must sit in one 128-byte memory line, or the
+  // warp's store is split and the flag can land before the data (measured: torn lines).
+  auto align = [](size_t x) { return (x + 4095) & ~size_t(4095); };
   comm->region_off[kProtoSimple] = comm->region_off[kProtoPull] = 0;
-  comm->region_off[kProtoLL] = nslots * comm->slot_bytes;
-  comm->region_off[kProtoLL128] = comm->region_off[kProtoLL] + nslots * comm->ll_slot_bytes;
+  comm->region_off[kProtoLL] = align(nslots * comm->slot_bytes);
+  comm->region_off[kProtoLL128] = align(comm->region_off[kProtoLL] + nslots * comm->ll_slot_bytes);
   comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL128] + nslots * comm->ll128_slot_bytes;
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&comm->err_host), sizeof(int),
                          cudaHostAllocMapped | cudaHostAllocPortable));

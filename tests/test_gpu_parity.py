@@ -424,24 +424,30 @@ def test_pull_single_tree_schedules(trees):
         assert all(same(got[r], want[r]) for r in range(n)), (trees, elems)
 
 
-def test_protocol_switches_share_no_inbox_state():
+@pytest.mark.parametrize("spread", [False, True])
+def test_protocol_switches_share_no_inbox_state(spread):
     """One communicator whose calls alternate LL / LL128 / bulk by size: the polling protocols
     have their own inbox regions, so payload words a bulk protocol left behind can never pass
     for a flag. The int32 payload holds small step-counter-like values to make a collision
     likely if the regions were shared."""
     n = 4
-    comm = comm_for(n, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=4096,
+    devices = [r % max(NGPU, 1) for r in range(n)] if spread else [0] * n
+    if spread and NGPU < 2:
+        pytest.skip("needs >= 2 GPUs")
+    # a staging budget whose slot size is not a multiple of 128 bytes: the LL128 region must
+    # still start line-aligned (a misaligned line is torn over NVLink)
+    comm = comm_for(n, devices, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=4096,
                     ll128_threshold=40000)
-    for it in range(16):
+    for it in range(24):
         elems = [200, 5000, 60000, 3000][it % 4]  # LL, LL128, bulk, LL128 (4-byte elements)
         p = (np.arange(n * elems, dtype=np.int64) % 64 + 1 + it).astype(np.int32)
-        got = gpu_allgather(comm, [0] * n, p, elems, O.INT32)
+        got = gpu_allgather(comm, devices, p, elems, O.INT32)
         want = oracle_ag(n, O.max_trees(n), O.INT32, p, elems)
         assert all(same(got[r], want[r]) for r in range(n)), (it, elems, mismatch(got, want, elems))
         q = (np.arange(n * n * elems, dtype=np.int64) % 64 + it).astype(np.int32)
-        got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.INT32, O.SUM)
+        got = gpu_reduce_scatter(comm, devices, q, elems, O.INT32, O.SUM)
         want = oracle_rs(n, O.max_trees(n), O.INT32, O.SUM, q, elems)
-        assert all(same(got[r], want[r]) for r in range(n)), (it, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (it, elems, mismatch(got, want, elems))
     plans = [comm.plan(k, e, O.INT32)["protocol"] for k in (0, 1) for e in (200, 5000, 60000)]
     assert plans == [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE,
                      _lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_PULL], plans
