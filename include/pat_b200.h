@@ -103,7 +103,8 @@ typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPul
 
 typedef struct {
   size_t size;              /* sizeof(patConfig_t) */
-  size_t staging_bytes;     /* per-rank inbox pool; 0 = default (channels*2*(n-1)*slice) */
+  size_t staging_bytes;     /* cap on the per-rank inbox pool (all protocol regions, flags aside);
+                               0 = default (512 MiB of SIMPLE slots + the LL / LL128 regions) */
   size_t slice_bytes;       /* SIMPLE bytes per slot per pipeline step; 0 = default 128 KiB */
   size_t ll_threshold;      /* per-rank chunk bytes up to which LL is used; 0 = default */
   int trees;                /* PAT tree count T; 0 = max_trees(n) (full aggregation) */
@@ -134,7 +135,7 @@ typedef struct {
   int launches;             /* kernel launches (one per device) */
   int slots_per_step;       /* inbox slots per pipeline step (n-1) */
   size_t slice_bytes;       /* payload bytes per slot per step */
-  size_t pool_bytes;        /* inbox pool bytes per rank actually addressed */
+  size_t pool_bytes;        /* the whole per-rank inbox pool (flags + every protocol region) */
   int64_t bytes_sent_per_rank;   /* (n-1) * chunk bytes */
   int peak_intermediate_slots;   /* reference accounting (simulate.hpp:50) */
 } patPlanInfo_t;

@@ -176,6 +176,25 @@ class PatComm:
             check(lib().patReduceScatter(self._h, sb, rb, count, dt, int(op), self._streams(streams)),
                   "patReduceScatter")
 
+    # ---- torch.distributed-shaped forms for one rank per process (ZeRO-3 style callers)
+    def all_gather_into_tensor(self, output, input, stream=None):
+        """output (n * input.numel(), rank-ordered) <- every rank's input, like
+        torch.distributed.all_gather_into_tensor; on `stream` (default: the current stream)."""
+        if len(self.local_ranks) != 1:
+            raise PatError(5, "all_gather_into_tensor needs a one-rank-per-process communicator")
+        if output.numel() != self.nranks * input.numel() or output.dtype != input.dtype:
+            raise PatError(31, "all_gather_into_tensor: output must hold nranks * input.numel() of input's dtype")
+        self.all_gather([input], [output], input.numel(), None, None if stream is None else [stream])
+
+    def reduce_scatter_tensor(self, output, input, op: int = _lib.SUM, stream=None):
+        """output (input.numel() / n) <- fold of block `rank` of every rank's input, like
+        torch.distributed.reduce_scatter_tensor, in the PAT tree order."""
+        if len(self.local_ranks) != 1:
+            raise PatError(5, "reduce_scatter_tensor needs a one-rank-per-process communicator")
+        if input.numel() != self.nranks * output.numel() or output.dtype != input.dtype:
+            raise PatError(31, "reduce_scatter_tensor: input must hold nranks * output.numel() of output's dtype")
+        self.reduce_scatter([input], [output], output.numel(), None, op, None if stream is None else [stream])
+
     def plan(self, kind: int, count: int, dtype) -> dict:
         info = PlanInfo()
         check(lib().patCommPlan(self._h, int(kind), count, _dtype(dtype, None) if dtype is not None else 7,

@@ -182,8 +182,13 @@ void fill_defaults(patConfig_t* c, int n) {
                          : std::min(kMaxSlice, std::max(kMinSlice, kDefaultPoolBytes / slots));
   }
   c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(15));
-  if (c->staging_bytes != 0) {  // explicit budget: channels * depth * (n-1) slots of one slice
-    size_t s = (c->staging_bytes / slots) & ~size_t(15);
+  if (c->staging_bytes != 0) {
+    // explicit budget for the whole pool (flags aside): channels * depth * (n-1) slot triples,
+    // one SIMPLE/PULL slot plus the LL (<= 16 KiB) and LL128 (<= 32 KiB) slots
+    const size_t b = c->staging_bytes > 8192 ? (c->staging_bytes - 8192) / slots : 0;
+    const size_t ll_max = kLLSlotBytes + kLL128SlotBytes;
+    size_t s = b >= ll_max + kLL128SlotBytes ? b - ll_max : b / 3;
+    s &= ~size_t(127);
     if (s < 256) s = 256;
     c->slice_bytes = s;
   }
@@ -878,7 +883,7 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   info->launches = static_cast<int>(comm->groups.size());
   info->slots_per_step = cp->proto.nslots;
   info->slice_bytes = static_cast<size_t>(sl.slice);
-  info->pool_bytes = static_cast<size_t>(sl.channels) * comm->cfg.depth * cp->proto.nslots * comm->slot_bytes + kFlagBytes;
+  info->pool_bytes = comm->pool_bytes;  // the whole per-rank pool: flags + every protocol region
   info->bytes_sent_per_rank = static_cast<int64_t>(comm->n - 1) * cb;
   info->peak_intermediate_slots = cp->peak_slots;
   return patSuccess;

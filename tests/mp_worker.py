@@ -22,7 +22,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     n = world
     fails = 0
-    for proto in (0, 1, 2):
+    for proto in (0, 1, 2, 4):  # auto, LL, SIMPLE, LL128 (PULL needs one process for all ranks)
         comm = PatComm.from_process_group(device=local, protocol=proto)
         for trees in O.valid_tree_counts(n):
             for elems in (1, 37, 4096, 65537, 1 << 20):
@@ -61,6 +61,29 @@ def main():
                         print(f"rank {rank} RS mismatch proto={proto} T={trees} elems={elems} dt={dt}", flush=True)
         comm.raise_async_error()
         comm.destroy()
+    # torch.distributed-shaped forms (ZeRO-3 callers): all-gather equals NCCL's bit for bit,
+    # reduce-scatter equals the PAT-order oracle
+    comm = PatComm.from_process_group(device=local)
+    for elems in (4099, 3 << 20):
+        x = torch.randn(elems, device=dev).to(torch.bfloat16)
+        out, ref = torch.empty(n * elems, dtype=torch.bfloat16, device=dev), torch.empty(n * elems, dtype=torch.bfloat16, device=dev)
+        comm.all_gather_into_tensor(out, x)
+        dist.all_gather_into_tensor(ref, x)
+        torch.cuda.synchronize(dev)
+        if not torch.equal(out, ref):
+            fails += 1
+            print(f"rank {rank} all_gather_into_tensor differs from NCCL elems={elems}", flush=True)
+        q = O.random_payload(O.BFLOAT16, n * n, elems, elems + 17)
+        g = torch.from_numpy(q[rank * n * elems:(rank + 1) * n * elems].copy().view(np.int16)).to(dev).view(torch.bfloat16)
+        shard = torch.empty(elems, dtype=torch.bfloat16, device=dev)
+        comm.reduce_scatter_tensor(shard, g)
+        torch.cuda.synchronize(dev)
+        want, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, O.max_trees(n)), O.BFLOAT16, O.SUM, q, elems)
+        if shard.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() != want[rank].tobytes():
+            fails += 1
+            print(f"rank {rank} reduce_scatter_tensor differs from the oracle elems={elems}", flush=True)
+    comm.raise_async_error()
+    comm.destroy()
     t = torch.tensor([fails], device=dev)
     dist.all_reduce(t)
     if rank == 0:

@@ -268,6 +268,7 @@ def test_small_slots_many_pipeline_steps():
         assert all(same(got[r], want[r]) for r in range(n))
     plan = comm.plan(1, 300001, O.FLOAT32)
     assert plan["iterations"] > 1 and plan["channels"] == 4
+    assert plan["pool_bytes"] <= n * 64 * 1024 + 32 * 1024, plan  # the cap holds for the whole pool (+ flags)
 
 
 @pytest.mark.parametrize("executor", EXECUTORS)
