@@ -50,7 +50,8 @@ constexpr size_t kDefaultLL = 256 << 10;
 constexpr size_t kDefaultLL128 = 4 << 20;
 constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
 constexpr size_t kLLSlotBytes = 16 << 10;     // LL slot: 8 KiB payload per channel-step
-constexpr size_t kLL128SlotBytes = 32 << 10;  // LL128 slot: 30 KiB payload per channel-step
+constexpr size_t kLL128SlotBytes = 36 << 10;  // LL128 slot: 33.75 KiB payload per channel-step:
+                                              // a 4 MiB chunk over 128 channels in one step
 
 constexpr int64_t kLL128PayloadBytes = 120;  // per 128-byte line (transport.cuh)
 constexpr int kDefaultTimeoutMs = 20000;
