@@ -96,15 +96,14 @@ typedef enum { patAlgoRing = 0, patAlgoBruckNearest = 1, patAlgoBruckFarthest = 
 /* LL: flag-in-line stores for small chunks. SIMPLE: pushed slices through the peers' inbox pools.
    PULL: receivers read the upstream's buffers (user sendbuf / recvbuf, staged RS partials);
    needs every rank's user buffers mapped in this process (patCommInitAll, cudaMalloc memory).
-   LL128: 128-byte lines carrying 120 payload bytes and a flag word (mid-size chunks).
-   Auto: LL up to ll_threshold, LL128 up to ll128_threshold, then SIMPLE — except reduce-scatter
+   Auto: LL up to ll_threshold, then SIMPLE — except reduce-scatter
    below 128 MiB, which PULLs where possible (measured, profiles/r01_sp_simple_vs_pull.jsonl). */
-typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3, patProtoLL128 = 4 } patProtocol_t;
+typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3 } patProtocol_t;
 
 typedef struct {
   size_t size;              /* sizeof(patConfig_t) */
   size_t staging_bytes;     /* cap on the per-rank inbox pool (all protocol regions, flags aside);
-                               0 = default (512 MiB of SIMPLE slots + the LL / LL128 regions) */
+                               0 = default (512 MiB of SIMPLE slots + the LL region) */
   size_t slice_bytes;       /* SIMPLE bytes per slot per pipeline step; 0 = default 128 KiB */
   size_t ll_threshold;      /* per-rank chunk bytes up to which LL is used; 0 = default */
   int trees;                /* PAT tree count T; 0 = max_trees(n) (full aggregation) */
@@ -120,8 +119,6 @@ typedef struct {
   int fused;                /* all ranks on one device: -1 = run the transport kernel anyway,
                                0 = fused single-device executor (one read of every input, one
                                write of every output, same fold tree as the schedule) */
-  size_t ll128_threshold;   /* per-rank chunk bytes up to which LL128 is used (above ll_threshold);
-                               0 = default */
 } patConfig_t;
 
 /* Plan the library would launch for one call (introspection / benchmarks). */

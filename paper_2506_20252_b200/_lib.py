@@ -27,7 +27,7 @@ RESULTS = {
 # datatypes (ncclDataType_t numbering) and ops (ncclRedOp_t numbering)
 INT8, UINT8, INT32, UINT32, INT64, UINT64, FLOAT16, FLOAT32, FLOAT64, BFLOAT16 = range(10)
 SUM, PROD, MAX, MIN = range(4)
-PROTO_AUTO, PROTO_LL, PROTO_SIMPLE, PROTO_PULL, PROTO_LL128 = 0, 1, 2, 3, 4
+PROTO_AUTO, PROTO_LL, PROTO_SIMPLE, PROTO_PULL = 0, 1, 2, 3
 DTYPE_SIZE = {INT8: 1, UINT8: 1, INT32: 4, UINT32: 4, INT64: 8, UINT64: 8, FLOAT16: 2,
               FLOAT32: 4, FLOAT64: 8, BFLOAT16: 2}
 
@@ -57,7 +57,6 @@ class Config(ctypes.Structure):
         ("direct", ctypes.c_int),
         ("send_warps", ctypes.c_int),
         ("fused", ctypes.c_int),
-        ("ll128_threshold", ctypes.c_size_t),
     ]
 
 

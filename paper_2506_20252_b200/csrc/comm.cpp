@@ -44,16 +44,11 @@ constexpr uint32_t kMagic = 0x50415442;                                       //
 constexpr size_t kDefaultPoolBytes = 512ull << 20;  // inbox pool budget per rank (all channels)
 constexpr size_t kMinSlice = 64 << 10, kMaxSlice = 256 << 10;
 constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
-// Protocol crossovers measured on B200 (profiles/r01_ll128_*.jsonl, graph mode, n = 2 and 4):
-// LL wins to 256 KiB, LL128 to 4 MiB, then the bulk protocols (SIMPLE; PULL for mid-size RS).
-constexpr size_t kDefaultLL = 256 << 10;
-constexpr size_t kDefaultLL128 = 4 << 20;
+// Protocol crossovers measured on B200 (profiles/r01_ll128_n*_p{1,2}.jsonl, graph mode, n = 2
+// and 4): LL wins to 2 MiB, then the bulk protocols (SIMPLE; PULL for mid-size RS).
+constexpr size_t kDefaultLL = 2 << 20;
 constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
-constexpr size_t kLLSlotBytes = 16 << 10;     // LL slot: 8 KiB payload per channel-step
-constexpr size_t kLL128SlotBytes = 36 << 10;  // LL128 slot: 33.75 KiB payload per channel-step:
-                                              // a 4 MiB chunk over 128 channels in one step
-
-constexpr int64_t kLL128PayloadBytes = 120;  // per 128-byte line (transport.cuh)
+constexpr size_t kLLSlotBytes = 32 << 10;  // LL slot: 16 KiB payload per channel-step (2 MiB per step)
 constexpr int kDefaultTimeoutMs = 20000;
 
 struct Compiled {
@@ -102,8 +97,8 @@ struct patComm {
   std::vector<DevGroup> groups;
   std::vector<void*> ipc_opened;
   size_t slot_bytes = 0, pool_bytes = 0;
-  size_t ll_slot_bytes = 0, ll128_slot_bytes = 0;  // LL / LL128 inbox slots (own regions, common_init)
-  size_t region_off[5] = {};               // inbox region of each protocol within a pool
+  size_t ll_slot_bytes = 0;                // LL inbox slot (own region, common_init)
+  size_t region_off[4] = {};               // inbox region of each protocol within a pool
   int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
   int channels = 0;
   int* err_host = nullptr;
@@ -185,20 +180,18 @@ void fill_defaults(patConfig_t* c, int n) {
   c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(15));
   if (c->staging_bytes != 0) {
     // explicit budget for the whole pool (flags aside): channels * depth * (n-1) slot triples,
-    // one SIMPLE/PULL slot plus the LL (<= 16 KiB) and LL128 (<= 32 KiB) slots
+    // one SIMPLE/PULL slot plus the LL slot (<= 32 KiB)
     const size_t b = c->staging_bytes > 8192 ? (c->staging_bytes - 8192) / slots : 0;
-    const size_t ll_max = kLLSlotBytes + kLL128SlotBytes;
-    size_t s = b >= ll_max + kLL128SlotBytes ? b - ll_max : b / 3;
+    size_t s = b >= 2 * kLLSlotBytes ? b - kLLSlotBytes : b / 2;
     s &= ~size_t(127);
     if (s < 256) s = 256;
     c->slice_bytes = s;
   }
   if (c->ll_threshold == 0) c->ll_threshold = env_int("PAT_LL_THRESHOLD", &v) ? (size_t)v : kDefaultLL;
-  if (c->ll128_threshold == 0) c->ll128_threshold = env_int("PAT_LL128_THRESHOLD", &v) ? (size_t)v : kDefaultLL128;
   if (c->timeout_ms <= 0) c->timeout_ms = env_int("PAT_TIMEOUT_MS", &v) ? (int)v : kDefaultTimeoutMs;
   if (c->protocol == patProtoAuto && env_int("PAT_PROTOCOL", &v)) c->protocol = (int)v;
   if (c->threads <= 0) c->threads = env_int("PAT_THREADS", &v) ? (int)v : 512;
-  c->threads = std::min(std::max(c->threads / 32 * 32, 64), 1024);
+  c->threads = std::min(std::max(c->threads / 32 * 32, 64), kMaxThreads);
   if (c->direct == 0 && env_int("PAT_DIRECT", &v)) c->direct = (int)v;
   if (c->fused == 0 && env_int("PAT_FUSED", &v)) c->fused = (int)v;
   if (c->send_warps <= 0) c->send_warps = env_int("PAT_SEND_WARPS", &v) ? (int)v : c->threads / 64;
@@ -380,7 +373,6 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
   int proto = comm->cfg.protocol;
   if (proto == patProtoAuto)
     proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold)      ? kProtoLL
-            : chunk_bytes <= static_cast<int64_t>(comm->cfg.ll128_threshold) ? kProtoLL128
             // reduce-scatter reads faster than it pushes between 4 and 128 MiB (the receiver
             // folds what it pulls, no inbox round trip); beyond that, and for all-gather,
             // pushed stores win (profiles/r01_sp_simple_vs_pull.jsonl)
@@ -389,10 +381,9 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
   if (proto == kProtoPull && !pull_ok) proto = kProtoSimple;
   s.proto = proto;
   int64_t cap = proto == kProtoLL      ? static_cast<int64_t>(comm->ll_slot_bytes / 2)
-                : proto == kProtoLL128 ? static_cast<int64_t>(comm->ll128_slot_bytes / 128 * kLL128PayloadBytes)
                                        : static_cast<int64_t>(comm->slot_bytes);
   if (proto == kProtoPull && kind == kAG) cap = std::max<int64_t>(cap, comm->pull_slice);  // AG pull stages nothing
-  const int64_t minslice = proto == kProtoLL ? 512 : proto == kProtoLL128 ? 32 * kLL128PayloadBytes : 16 << 10;
+  const int64_t minslice = proto == kProtoLL ? 512 : 16 << 10;
   int64_t per = (chunk_bytes + channels - 1) / channels;
   per = (per + 15) & ~int64_t(15);
   per = std::max<int64_t>(per, std::min<int64_t>(minslice, cap));
@@ -448,18 +439,14 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
     comm->pull_slice = env_int("PAT_PULL_SLICE", &v) && v >= 256 ? (v & ~15LL) : (512 << 10);
   }
   const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
-  // Inbox regions: SIMPLE/PULL slots, then LL and LL128 slots. The polling protocols get their
-  // own memory: a stale payload word left by another protocol could otherwise match a flag.
+  // Inbox regions: SIMPLE/PULL slots, then LL slots. LL polls its lines, so it gets its own
+  // memory: a stale payload word left by a bulk protocol could otherwise pass for a flag.
   comm->ll_slot_bytes = std::max<size_t>(256, std::min<size_t>(kLLSlotBytes, comm->slot_bytes) & ~size_t(127));
-  comm->ll128_slot_bytes = std::max<size_t>(256, std::min<size_t>(kLL128SlotBytes, comm->slot_bytes) & ~size_t(127));
   const size_t nslots = static_cast<size_t>(comm->channels) * c.depth * slots;
-  // Regions start 4 KiB aligned: an LL128 line must sit in one 128-byte memory line, or the
-  // warp's store is split and the flag can land before the data (measured: torn lines).
   auto align = [](size_t x) { return (x + 4095) & ~size_t(4095); };
   comm->region_off[kProtoSimple] = comm->region_off[kProtoPull] = 0;
   comm->region_off[kProtoLL] = align(nslots * comm->slot_bytes);
-  comm->region_off[kProtoLL128] = align(comm->region_off[kProtoLL] + nslots * comm->ll_slot_bytes);
-  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL128] + nslots * comm->ll128_slot_bytes;
+  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL] + nslots * comm->ll_slot_bytes;
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&comm->err_host), sizeof(int),
                          cudaHostAllocMapped | cudaHostAllocPortable));
   *comm->err_host = 0;
@@ -568,9 +555,7 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.iters = sl.iters;
     p.chunk_bytes = chunk_bytes;
     p.slice_bytes = sl.slice;
-    p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL      ? comm->ll_slot_bytes
-                                         : sl.proto == kProtoLL128 ? comm->ll128_slot_bytes
-                                                                   : comm->slot_bytes);
+    p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL ? comm->ll_slot_bytes : comm->slot_bytes);
     p.depth = comm->cfg.depth;
     {
       long long sk = 1;

@@ -15,10 +15,13 @@ constexpr int kMaxSlots = 8;    // inbox slots per pipeline step (= n-1 arrivals
 constexpr int kMaxArr = 8;      // arrivals folded into one forwarded offset
 constexpr int kMaxLocal = 8;    // ranks driven by one kernel (local mode)
 constexpr int kMaxChannels = 128;
+constexpr int kMaxThreads = 512;  // per CTA: 128 registers per thread for the unrolled SIMPLE loops
 constexpr int kFlagWords = 32;  // per channel: data flag per round [0,8), done-from per rank [8,16),
                                 // ready-from per rank [16,24) (direct mode entry handshake)
 
-enum Proto : int { kProtoLL = 1, kProtoSimple = 2, kProtoPull = 3, kProtoLL128 = 4 };
+// (4 is retired: LL128, 128-byte lines with one flag word, was measured to tear over NVLink —
+// a line's flag sector can land before its data sectors — and was removed.)
+enum Proto : int { kProtoLL = 1, kProtoSimple = 2, kProtoPull = 3 };
 
 // PULL reduce-scatter: what a rank does with the arrival it pulled into slot j.
 enum PullAct : int8_t {

@@ -642,187 +642,8 @@ __device__ void pull_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
   if (tid < n && tid != R) wait_flag(myflags + 8 + tid, base + p.iters, w);
 }
 
-// ------------------------------------------------------------------------- LL128
-// 128-byte lines of 16 words; word 15 is the flag, words 0..14 carry 120 payload bytes (94%
-// wire efficiency against LL's 50%). A warp stores 4 whole lines with ONE st.volatile.v2.u64
-// (lane j of an 8-lane group writes words 2j, 2j+1); NVLink delivers each 128-byte line of a
-// warp store as a unit, so a reader that sees the flag word sees the line (the property NCCL's
-// LL128 protocol rests on). Readers load the line with one warp load and re-poll until the flag
-// lane of every group matches. Lines are forwarded as they are, with the new step's flag.
-constexpr int kLL128Payload = 120;
-
-// The line's 16 bytes per lane must leave (and be read) in ONE warp-wide instruction: a warp
-// that diverged before the store would write the flag lane's word separately from the data
-// lanes' words (a torn line: measured on B200 with element-granular loads before the store).
-// So every LL128 access is issued convergent (__syncwarp) by all 32 lanes, idle lanes masked
-// by a predicate inside the instruction.
-__device__ __forceinline__ void st_ll128(char* p, uint64_t a, uint64_t b, bool active) {
-  __syncwarp();
-  asm volatile(
-      "{ .reg .pred q; setp.ne.u32 q, %3, 0; @q st.volatile.global.v2.u64 [%0], {%1,%2}; }" ::"l"(p), "l"(a),
-      "l"(b), "r"(static_cast<uint32_t>(active))
-      : "memory");
-}
-__device__ __forceinline__ void ld_ll128(const char* p, uint64_t& a, uint64_t& b, bool active) {
-  __syncwarp();
-  asm volatile(
-      "{ .reg .pred q; setp.ne.u32 q, %3, 0; mov.u64 %0, 0; mov.u64 %1, 0; @q ld.volatile.global.v2.u64 {%0,%1}, [%2]; }"
-      : "=l"(a), "=l"(b)
-      : "l"(p), "r"(static_cast<uint32_t>(active))
-      : "memory");
-}
-
-// Poll this lane's 16 bytes of line `line` (nullptr lanes are idle) until all four lines of the
-// warp carry `flag` in their word 15.
-__device__ __forceinline__ void poll_ll128(const char* line, int j, uint64_t flag, uint64_t& a, uint64_t& b,
-                                           Waiter& w) {
-  uint64_t start = 0;
-  uint32_t spins = 0;
-  while (true) {
-    ld_ll128(line ? line + 16 * j : nullptr, a, b, line != nullptr);
-    const bool ok = !line || j != 7 || b == flag;
-    const bool ready = __shfl_sync(0xffffffffu, ok, (threadIdx.x & 31) | 7);
-    if (__all_sync(0xffffffffu, ready) || __any_sync(0xffffffffu, w.aborted)) return;  // warp-uniform exit
-    if ((++spins & 1023u) == 0) {
-      const uint64_t now = globaltimer();
-      if (start == 0) start = now;
-      else if (now - start > w.timeout_ns) report_timeout(w);
-    }
-  }
-}
-
-__device__ __forceinline__ uint64_t u64of(uint2 v) { return static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32); }
-__device__ __forceinline__ uint2 u2of(uint64_t v) { return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32)); }
-
-template <int DT, int OP>
-__device__ __forceinline__ uint64_t fold64(uint64_t a, uint64_t b) {
-  uint2 x = u2of(a);
-  fold_vec<DT, OP>(x, u2of(b));
-  return u64of(x);
-}
-
-// Payload words of lane j in line L of a slice of `len` bytes starting at `p` (user memory).
-struct LaneWords {
-  int64_t off;   // byte offset of word 0 within the slice
-  int v0, v1;    // valid bytes of word 0 / word 1 (0 = none)
-};
-__device__ __forceinline__ LaneWords lane_words(int64_t L, int j, int64_t len) {
-  LaneWords x;
-  x.off = L * kLL128Payload + 16 * j;
-  x.v0 = static_cast<int>(max(int64_t{0}, min(int64_t{8}, len - x.off)));
-  x.v1 = j == 7 ? 0 : static_cast<int>(max(int64_t{0}, min(int64_t{8}, len - x.off - 8)));
-  return x;
-}
-__device__ __forceinline__ void load_lane(const char* base, const LaneWords& x, const KPlan& p, uint64_t& a,
-                                          uint64_t& b) {
-  a = x.v0 ? u64of(load_word(base + x.off, x.v0, p)) : 0;
-  b = x.v1 ? u64of(load_word(base + x.off + 8, x.v1, p)) : 0;
-}
-__device__ __forceinline__ void store_lane(char* base, const LaneWords& x, const KPlan& p, uint64_t a, uint64_t b) {
-  if (x.v0) store_word(base + x.off, u2of(a), x.v0, p);
-  if (x.v1) store_word(base + x.off + 8, u2of(b), x.v1, p);
-}
-
 template <int DT, int OP, int KIND>
-__device__ void step_ll128(const KPlan& p, const Step& s, Waiter& w) {
-  const int n = p.n;
-  const int64_t Cb = p.chunk_bytes;
-  const char* snd = p.send[s.lr];
-  char* out = p.recv[s.lr];
-  const uint64_t flag = s.g + 1;
-  const int64_t nlines = (s.len + kLL128Payload - 1) / kLL128Payload;
-  const int lane = threadIdx.x & 31, j = lane & 7;
-  const int64_t warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  // warp-uniform walk over groups of 4 lines; L < 0 marks an idle lane
-  auto for_lines = [&](auto&& body) {
-    for (int64_t l0 = warp * 4; l0 < nlines; l0 += nwarps * 4) {
-      const int64_t L = l0 + (lane >> 3);
-      body(L < nlines ? L : -1);
-    }
-  };
-
-  if constexpr (KIND == kAG) {
-    if (out + s.R * Cb != snd)
-      for_lines([&](int64_t L) {
-        if (L < 0) return;
-        const LaneWords x = lane_words(L, j, s.len);
-        uint64_t a, b;
-        load_lane(snd + s.off, x, p, a, b);
-        store_lane(out + s.R * Cb + s.off, x, p, a, b);
-      });
-  }
-  for (int t = 0; t < p.nrounds; ++t) {
-    const KRound& r = p.rounds[t];
-    const int P = (s.R + r.peer) % n;
-    for (int pos = 0; pos < r.nchunks; ++pos) {
-      char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
-      if constexpr (KIND == kAG) {
-        const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
-        for_lines([&](int64_t L) {
-          uint64_t a = 0, b = 0;
-          if (fwd) {
-            poll_ll128(L >= 0 ? fwd + 128 * L : nullptr, j, flag, a, b, w);
-          } else if (L >= 0) {
-            load_lane(snd + s.off, lane_words(L, j, s.len), p, a, b);
-          }
-          st_ll128(dst + 128 * (L < 0 ? 0 : L) + 16 * j, a, j == 7 ? flag : b, L >= 0);
-        });
-      } else {
-        const int dest = (s.R - r.chunk[pos] + n) % n;
-        const char* own = snd + dest * Cb + s.off;
-        const int na = r.narr[pos];
-        for_lines([&](int64_t L) {
-          uint64_t a = 0, b = 0;
-          if (na == 0) {
-            if (L >= 0) load_lane(own, lane_words(L, j, s.len), p, a, b);
-          } else {
-            poll_ll128(L >= 0 ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) + 128 * L : nullptr, j, flag, a, b, w);
-            for (int q = 1; q < na; ++q) {
-              uint64_t a2 = 0, b2 = 0;
-              poll_ll128(L >= 0 ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][q]) + 128 * L : nullptr, j, flag, a2, b2, w);
-              a = fold64<DT, OP>(a, a2);
-              b = fold64<DT, OP>(b, b2);
-            }
-            if (L >= 0) {
-              uint64_t a2, b2;
-              load_lane(own, lane_words(L, j, s.len), p, a2, b2);
-              a = fold64<DT, OP>(a, a2);
-              b = fold64<DT, OP>(b, b2);
-            }
-          }
-          st_ll128(dst + 128 * (L < 0 ? 0 : L) + 16 * j, a, j == 7 ? flag : b, L >= 0);
-        });
-      }
-    }
-  }
-  if constexpr (KIND == kAG) {
-    for (int q = 0; q < p.nslots; ++q) {
-      const int origin = (s.R - p.slot_offset[q] + n) % n;
-      const char* slot = slot_ptr(p, s.R, s.c, s.buf, q);
-      for_lines([&](int64_t L) {
-        uint64_t a = 0, b = 0;
-        poll_ll128(L >= 0 ? slot + 128 * L : nullptr, j, flag, a, b, w);
-        if (L >= 0) store_lane(out + origin * Cb + s.off, lane_words(L, j, s.len), p, a, b);
-      });
-    }
-  } else {
-    for_lines([&](int64_t L) {
-      uint64_t a = 0, b = 0;
-      const LaneWords x = lane_words(L < 0 ? 0 : L, j, s.len);
-      if (L >= 0) load_lane(snd + s.R * Cb + s.off, x, p, a, b);
-      for (int f = 0; f < p.nfin; ++f) {
-        uint64_t a2 = 0, b2 = 0;
-        poll_ll128(L >= 0 ? slot_ptr(p, s.R, s.c, s.buf, p.fin[f]) + 128 * L : nullptr, j, flag, a2, b2, w);
-        a = fold64<DT, OP>(a, a2);
-        b = fold64<DT, OP>(b, b2);
-      }
-      if (L >= 0) store_lane(out + s.off, x, p, a, b);
-    });
-  }
-}
-
-template <int DT, int OP, int KIND>
-__global__ void __launch_bounds__(1024) pat_kernel(const __grid_constant__ KPlan p) {
+__global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant__ KPlan p) {
   const int lr = blockIdx.x / p.channels;
   const int c = blockIdx.x - lr * p.channels;
   const int R = p.rank[lr];
@@ -848,13 +669,12 @@ __global__ void __launch_bounds__(1024) pat_kernel(const __grid_constant__ KPlan
 
   if (p.proto == kProtoPull) {
     pull_role<DT, OP, KIND>(p, base, R, lr, c, w);
-  } else if (p.proto == kProtoLL || p.proto == kProtoLL128) {
+  } else if (p.proto == kProtoLL) {
     for (int i = 0; i < p.iters; ++i) {
       const Step s = make_step(p, base, i, R, lr, c);
       if (threadIdx.x == 0) wait_credits(p, s, w);
       __syncthreads();
-      if (p.proto == kProtoLL) step_ll<DT, OP, KIND>(p, s, w);
-      else step_ll128<DT, OP, KIND>(p, s, w);
+      step_ll<DT, OP, KIND>(p, s, w);
       __syncthreads();
       // done(step): every load of this step's inbox has returned (its value was consumed before
       // the barrier), so a relaxed store suffices to hand the buffers back

@@ -217,7 +217,7 @@ def test_reduce_scatter_ops(op, dt, executor):
             assert same(got[r], want[r]), (op, dt, n, r)
 
 
-@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
 def test_protocols_forced(proto):
     for n in (2, 5, 8):
         comm = comm_for(n, protocol=proto, fused=-1)
@@ -390,7 +390,7 @@ def test_no_async_error_left():
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
 @pytest.mark.parametrize("n", [2, 3, 4, 6, 8])
 def test_multi_gpu_bulk_protocols(n, proto):
     """SIMPLE (pushed slices through the inboxes) and PULL (receivers read the peers' buffers)
@@ -427,20 +427,16 @@ def test_pull_single_tree_schedules(trees):
 
 @pytest.mark.parametrize("spread", [False, True])
 def test_protocol_switches_share_no_inbox_state(spread):
-    """One communicator whose calls alternate LL / LL128 / bulk by size: the polling protocols
-    have their own inbox regions, so payload words a bulk protocol left behind can never pass
-    for a flag. The int32 payload holds small step-counter-like values to make a collision
+    """One communicator whose calls alternate LL / bulk by size: the polling protocol has its
+    own inbox region, so payload words a bulk protocol left behind can never pass for a flag. The int32 payload holds small step-counter-like values to make a collision
     likely if the regions were shared."""
     n = 4
     devices = [r % max(NGPU, 1) for r in range(n)] if spread else [0] * n
     if spread and NGPU < 2:
         pytest.skip("needs >= 2 GPUs")
-    # a staging budget whose slot size is not a multiple of 128 bytes: the LL128 region must
-    # still start line-aligned (a misaligned line is torn over NVLink)
-    comm = comm_for(n, devices, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=4096,
-                    ll128_threshold=40000)
+    comm = comm_for(n, devices, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=16384)
     for it in range(24):
-        elems = [200, 5000, 60000, 3000][it % 4]  # LL, LL128, bulk, LL128 (4-byte elements)
+        elems = [200, 5000, 60000, 3000][it % 4]  # LL, bulk, bulk, LL (4-byte elements)
         p = (np.arange(n * elems, dtype=np.int64) % 64 + 1 + it).astype(np.int32)
         got = gpu_allgather(comm, devices, p, elems, O.INT32)
         want = oracle_ag(n, O.max_trees(n), O.INT32, p, elems)
@@ -450,5 +446,5 @@ def test_protocol_switches_share_no_inbox_state(spread):
         want = oracle_rs(n, O.max_trees(n), O.INT32, O.SUM, q, elems)
         assert all(same(got[r], want[r]) for r in range(n)), (it, elems, mismatch(got, want, elems))
     plans = [comm.plan(k, e, O.INT32)["protocol"] for k in (0, 1) for e in (200, 5000, 60000)]
-    assert plans == [_lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_SIMPLE,
-                     _lib.PROTO_LL, _lib.PROTO_LL128, _lib.PROTO_PULL], plans
+    assert plans == [_lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_SIMPLE,
+                     _lib.PROTO_LL, _lib.PROTO_PULL, _lib.PROTO_PULL], plans

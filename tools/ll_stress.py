@@ -1,4 +1,5 @@
-"""Stress LL128 (and LL) against the oracle; print where mismatches are (debug tool)."""
+"""Stress the polling protocol (LL) against the oracle on odd sizes and 2-byte elements; print
+where mismatches are (debug tool)."""
 import os
 import sys
 
@@ -13,7 +14,7 @@ from test_gpu_parity import gpu_allgather, gpu_reduce_scatter, oracle_ag, oracle
 
 ngpu = torch.cuda.device_count()
 for n, devices in ((8, [r % ngpu for r in range(8)]), (8, [0] * 8), (4, list(range(min(4, ngpu))) if ngpu >= 4 else [0] * 4)):
-    for proto in (_lib.PROTO_LL128, _lib.PROTO_LL):
+    for proto in (_lib.PROTO_LL,):
         comm = PatComm.init_all(n, devices, protocol=proto, staging_bytes=n * 256 * 1024, channels=8, fused=-1)
         bad = 0
         for it in range(6):

@@ -12,8 +12,7 @@ from test_gpu_parity import gpu_allgather, gpu_reduce_scatter, oracle_ag, oracle
 
 n = 4
 for variant in ("full", "no-bulk", "no-rs"):
-    comm = PatComm.init_all(n, [0] * n, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=4096,
-                            ll128_threshold=40000)
+    comm = PatComm.init_all(n, [0] * n, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=16384)
     for it in range(16):
         elems = [200, 5000, 60000, 3000][it % 4]
         if variant == "no-bulk" and elems == 60000:

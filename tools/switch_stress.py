@@ -1,4 +1,4 @@
-"""Long protocol-switching sequence on one communicator (LL / LL128 / SIMPLE / PULL by size),
+"""Long protocol-switching sequence on one communicator (LL / SIMPLE / PULL by size),
 AG and RS interleaved, buffers re-allocated every call; counts mismatches (debug tool)."""
 import os
 import sys
@@ -16,8 +16,8 @@ ngpu = torch.cuda.device_count()
 rng = np.random.default_rng(1)
 for n, devices in ((4, [0] * 4), (4, list(range(4)) if ngpu >= 4 else [0] * 4), (8, [r % ngpu for r in range(8)])):
     for forced in (0, _lib.PROTO_PULL):
-        comm = PatComm.init_all(n, devices, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=4096,
-                                ll128_threshold=40000, protocol=forced)
+        comm = PatComm.init_all(n, devices, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=16384,
+                                protocol=forced)
         bad = 0
         for it in range(60):
             elems = int(rng.choice([200, 3000, 5000, 60000, 100003]))
