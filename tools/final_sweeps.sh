@@ -1,6 +1,6 @@
 # Round-1 measurement set (run on a 4-GPU box). Outputs under gpurun_out/final/.
 export PAT_TIMEOUT_MS=10000
-mkdir -p gpurun_out/final
+mkdir -p gpurun_out/final; rm -f gpurun_out/final/*
 O=gpurun_out/final
 # latency sweeps, graph mode, multi-process (torchrun) vs NCCL Ring
 for N in 2 3 4; do
