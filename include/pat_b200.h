@@ -96,7 +96,8 @@ typedef enum { patAlgoRing = 0, patAlgoBruckNearest = 1, patAlgoBruckFarthest = 
 /* LL: flag-in-line stores for small chunks. SIMPLE: pushed slices through the peers' inbox pools.
    PULL: receivers read the upstream's buffers (user sendbuf / recvbuf, staged RS partials);
    needs every rank's user buffers mapped in this process (patCommInitAll, cudaMalloc memory).
-   Auto: LL up to ll_threshold, then SIMPLE — except reduce-scatter
+   Auto: LL while the calibrated cost model predicts it faster (or up to ll_threshold when that
+   is set), then SIMPLE — except reduce-scatter
    below 128 MiB, which PULLs where possible (measured, profiles/r01_sp_simple_vs_pull.jsonl). */
 typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3 } patProtocol_t;
 
@@ -105,7 +106,7 @@ typedef struct {
   size_t staging_bytes;     /* cap on the per-rank inbox pool (all protocol regions, flags aside);
                                0 = default (512 MiB of SIMPLE slots + the LL region) */
   size_t slice_bytes;       /* SIMPLE bytes per slot per pipeline step; 0 = default 128 KiB */
-  size_t ll_threshold;      /* per-rank chunk bytes up to which LL is used; 0 = default */
+  size_t ll_threshold;      /* per-rank chunk bytes up to which LL is used; 0 = cost model */
   int trees;                /* PAT tree count T; 0 = max_trees(n) (full aggregation) */
   int max_channels;         /* CTAs per rank; 0 = default */
   int protocol;             /* patProtocol_t */
@@ -135,6 +136,7 @@ typedef struct {
   size_t pool_bytes;        /* the whole per-rank inbox pool (flags + every protocol region) */
   int64_t bytes_sent_per_rank;   /* (n-1) * chunk bytes */
   int peak_intermediate_slots;   /* reference accounting (simulate.hpp:50) */
+  double predicted_us;           /* the calibrated alpha-beta model's time for this call (comm.cpp) */
 } patPlanInfo_t;
 
 /* ExecStats (simulate.hpp:43-53) computed from a schedule; chunk_bytes as given. */

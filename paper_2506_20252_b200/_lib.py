@@ -74,6 +74,7 @@ class PlanInfo(ctypes.Structure):
         ("pool_bytes", ctypes.c_size_t),
         ("bytes_sent_per_rank", ctypes.c_int64),
         ("peak_intermediate_slots", ctypes.c_int),
+        ("predicted_us", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -44,9 +44,8 @@ constexpr uint32_t kMagic = 0x50415442;                                       //
 constexpr size_t kDefaultPoolBytes = 512ull << 20;  // inbox pool budget per rank (all channels)
 constexpr size_t kMinSlice = 64 << 10, kMaxSlice = 256 << 10;
 constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
-// Protocol crossovers measured on B200 (profiles/r01_ll128_n*_p{1,2}.jsonl, graph mode, n = 2
-// and 4): LL wins to 2 MiB, then the bulk protocols (SIMPLE; PULL for mid-size RS).
-constexpr size_t kDefaultLL = 2 << 20;
+// LL vs bulk is chosen by the calibrated cost model below (choose_slicing): LL to 2 MiB at
+// n <= 3, to 1 MiB at n >= 4 (profiles/r01c_forced_n*_p*.jsonl).
 constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
 constexpr size_t kLLSlotBytes = 32 << 10;  // LL slot: 16 KiB payload per channel-step (2 MiB per step)
 constexpr int kDefaultTimeoutMs = 20000;
@@ -187,7 +186,7 @@ void fill_defaults(patConfig_t* c, int n) {
     if (s < 256) s = 256;
     c->slice_bytes = s;
   }
-  if (c->ll_threshold == 0) c->ll_threshold = env_int("PAT_LL_THRESHOLD", &v) ? (size_t)v : kDefaultLL;
+  if (c->ll_threshold == 0 && env_int("PAT_LL_THRESHOLD", &v)) c->ll_threshold = (size_t)v;  // 0: cost model
   if (c->timeout_ms <= 0) c->timeout_ms = env_int("PAT_TIMEOUT_MS", &v) ? (int)v : kDefaultTimeoutMs;
   if (c->protocol == patProtoAuto && env_int("PAT_PROTOCOL", &v)) c->protocol = (int)v;
   if (c->threads <= 0) c->threads = env_int("PAT_THREADS", &v) ? (int)v : 512;
@@ -367,21 +366,28 @@ struct Slicing {
   int64_t slice;
 };
 
-Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int max_channels, bool pull_ok) {
+// Alpha-beta model of one call (the reference's costmodel.cpp:70-104 prices a
+// schedule as rounds x (alpha + beta x bytes)), calibrated on B200 by tools/fit_costmodel.py
+// from forced-protocol sweeps at n = 2, 3, 4 (profiles/r01c_costmodel_fit.json):
+//   t = steps x (a + b x R) + wire x (n-1) x C / B        (LL: one fixed cost per LL step)
+//   t = a + b x R + (n-1) x C / B                          (SIMPLE / PULL: steps pipelined)
+// R = PAT rounds. (n-1) x C does not depend on T, so T = max_trees (fewest rounds) is optimal.
+struct CostRow {
+  double a_us, b_us, gbs, wire;
+};
+constexpr CostRow kCostLL{3.59, 1.28, 510.0, 2.0};
+constexpr CostRow kCostBulk{5.83, 6.43, 561.0, 1.0};
+
+double predict_us(int proto, int n, int rounds, int64_t chunk_bytes, int iters) {
+  const CostRow& c = proto == kProtoLL ? kCostLL : kCostBulk;
+  const double fixed = (proto == kProtoLL ? std::max(iters, 1) : 1) * (c.a_us + c.b_us * rounds);
+  return fixed + c.wire * (n - 1) * static_cast<double>(chunk_bytes) / (c.gbs * 1e3);
+}
+
+Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int channels) {
   Slicing s{};
-  const int channels = std::max(1, std::min(comm->channels, max_channels));
-  int proto = comm->cfg.protocol;
-  if (proto == patProtoAuto)
-    proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold)      ? kProtoLL
-            // reduce-scatter reads faster than it pushes between 4 and 128 MiB (the receiver
-            // folds what it pulls, no inbox round trip); beyond that, and for all-gather,
-            // pushed stores win (profiles/r01_sp_simple_vs_pull.jsonl)
-            : pull_ok && kind == kRS && chunk_bytes < kPullMaxRS             ? kProtoPull
-                                                                             : kProtoSimple;
-  if (proto == kProtoPull && !pull_ok) proto = kProtoSimple;
   s.proto = proto;
-  int64_t cap = proto == kProtoLL      ? static_cast<int64_t>(comm->ll_slot_bytes / 2)
-                                       : static_cast<int64_t>(comm->slot_bytes);
+  int64_t cap = proto == kProtoLL ? static_cast<int64_t>(comm->ll_slot_bytes / 2) : static_cast<int64_t>(comm->slot_bytes);
   if (proto == kProtoPull && kind == kAG) cap = std::max<int64_t>(cap, comm->pull_slice);  // AG pull stages nothing
   const int64_t minslice = proto == kProtoLL ? 512 : 16 << 10;
   int64_t per = (chunk_bytes + channels - 1) / channels;
@@ -393,6 +399,30 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
   s.channels = static_cast<int>(std::min<int64_t>(channels, nslices));
   s.iters = static_cast<int>((nslices + s.channels - 1) / s.channels);
   return s;
+}
+
+Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int max_channels, bool pull_ok,
+                       int rounds) {
+  const int channels = std::max(1, std::min(comm->channels, max_channels));
+  int proto = comm->cfg.protocol;
+  if (proto == patProtoAuto) {
+    // reduce-scatter reads faster than it pushes between 4 and 128 MiB in one process (the
+    // receiver folds what it pulls, no inbox round trip); beyond that, and for all-gather,
+    // pushed stores win (profiles/r01_sp_simple_vs_pull.jsonl)
+    const int bulk = pull_ok && kind == kRS && chunk_bytes < kPullMaxRS ? kProtoPull : kProtoSimple;
+    if (comm->cfg.ll_threshold) {  // explicit threshold
+      proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold) ? kProtoLL : bulk;
+    } else {  // the cost model picks LL or the bulk protocol
+      const Slicing a = shape(comm, kProtoLL, kind, chunk_bytes, channels);
+      const Slicing b = shape(comm, bulk, kind, chunk_bytes, channels);
+      proto = predict_us(kProtoLL, comm->n, rounds, chunk_bytes, a.iters) <=
+                      predict_us(bulk, comm->n, rounds, chunk_bytes, b.iters)
+                  ? kProtoLL
+                  : bulk;
+    }
+  }
+  if (proto == kProtoPull && !pull_ok) proto = kProtoSimple;
+  return shape(comm, proto, kind, chunk_bytes, channels);
 }
 
 // Channels per rank such that every device's launch stays co-resident (cooperative launch).
@@ -524,7 +554,7 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple;
   for (size_t l = 0; l < comm->lranks.size() && pull_ok && !single_device; ++l)
     pull_ok = legacy_ipc_capable(sendbuffs[l]) && (kind == kRS || legacy_ipc_capable(recvbuffs[l]));
-  const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok);
+  const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds);
   int vec = 16;
   bool aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
   for (size_t l = 0; l < comm->lranks.size(); ++l) {
@@ -858,7 +888,8 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   DeviceGuard guard;
   int cap = 0;
   if (patResult_t e = channel_cap(comm, kind, dtype, 0, &cap)) return e;
-  const Slicing sl = choose_slicing(comm, kind, cb, cap, !comm->multiprocess);  // assumes cudaMalloc buffers
+  const Slicing sl = choose_slicing(comm, kind, cb, cap, !comm->multiprocess,  // assumes cudaMalloc buffers
+                                    cp->proto.nrounds);
   std::memset(info, 0, sizeof(*info));
   info->protocol = sl.proto;
   info->trees = trees;
@@ -872,6 +903,7 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   info->pool_bytes = comm->pool_bytes;  // the whole per-rank pool: flags + every protocol region
   info->bytes_sent_per_rank = static_cast<int64_t>(comm->n - 1) * cb;
   info->peak_intermediate_slots = cp->peak_slots;
+  info->predicted_us = predict_us(sl.proto, comm->n, cp->proto.nrounds, cb, sl.iters);
   return patSuccess;
 }
 

@@ -448,3 +448,18 @@ def test_protocol_switches_share_no_inbox_state(spread):
     plans = [comm.plan(k, e, O.INT32)["protocol"] for k in (0, 1) for e in (200, 5000, 60000)]
     assert plans == [_lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_SIMPLE,
                      _lib.PROTO_LL, _lib.PROTO_PULL, _lib.PROTO_PULL], plans
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_cost_model_protocol_choice():
+    """Without an explicit ll_threshold the calibrated alpha-beta model picks LL or the bulk
+    protocol (comm.cpp: predict_us); the crossovers it implies match the forced sweeps
+    (profiles/r01c_forced_n*_p*.jsonl): LL to 2 MiB at n=2, to 1 MiB at n=4."""
+    cases = [(2, 2 << 20, _lib.PROTO_LL), (2, 8 << 20, _lib.PROTO_SIMPLE)]
+    if NGPU >= 4:
+        cases += [(4, 1 << 20, _lib.PROTO_LL), (4, 4 << 20, _lib.PROTO_SIMPLE)]
+    for n, nbytes, want in cases:
+        comm = comm_for(n, list(range(n)))
+        plan = comm.plan(0, nbytes // 4, O.FLOAT32)
+        assert plan["protocol"] == want, (n, nbytes, plan)
+        assert plan["predicted_us"] > 0
