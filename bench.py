@@ -420,6 +420,19 @@ def run_pat(args, rank, world, local):
         except Exception:
             pass
 
+    # small messages are latency-bound: compare with the PAT step floor, the zero-byte LL time of
+    # R = ceil(log2 n) rounds (cost-model fit, profiles/r01c_costmodel_fit.json) plus the LL wire
+    # bytes (2 x payload) at the measured two-way SM-push ceiling (profiles/r01_bidir_probe_g4.txt)
+    lat_floor = None
+    if world > 1:
+        R = comm.plan(0, elems, FLOAT32)["rounds"]
+        zero_us = 3.59 + 1.28 * R
+        wire_us = 2.0 * (n - 1) * C / (704.0 * 1e3)
+        lat_floor = {"rounds": R, "zero_byte_us": zero_us, "wire_us_at_704gbs": wire_us,
+                     "floor_us": zero_us + wire_us, "achieved_us": 1e3 * ag_ms / K,
+                     "frac": (zero_us + wire_us) / (1e3 * ag_ms / K),
+                     "source": "profiles/r01c_costmodel_fit.json (LL a, b), profiles/r01_bidir_probe_g4.txt"}
+
     clk = clocks.summary()
     if world > 1:
         allc = [None] * world
@@ -461,6 +474,7 @@ def run_pat(args, rank, world, local):
                     "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host"},
             "gpu_launches": 2 * K,
             "roofline": roof,
+            "latency_floor": lat_floor,
             "cpu_baseline": cpu,
             "clocks": clk,
         }
