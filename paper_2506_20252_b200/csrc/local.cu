@@ -24,6 +24,7 @@
 #include <cstdint>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fold.cuh"
 
@@ -195,7 +196,12 @@ cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize,
   // per rank: enough blocks for ~2 resident CTAs on every SM overall, no more than the units
   const int64_t per_rank_units = vec == 16 ? (chunk_bytes >> 4) : (chunk_bytes / esize);
   const int64_t want = (per_rank_units + kLocalThreads - 1) / kLocalThreads;
-  const int bpr = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (4LL * sm_count + n - 1) / n)));
+  static const int ctas_per_sm = [] {  // PAT_LOCAL_CTAS_PER_SM: launch-shape experiments
+    const char* e = std::getenv("PAT_LOCAL_CTAS_PER_SM");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 4;
+  }();
+  const int bpr = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(want, (static_cast<int64_t>(ctas_per_sm) * sm_count + n - 1) / n)));
   if (kind == 0) local_ag_kernel<<<bpr * n, kLocalThreads, 0, stream>>>(p);
   else kLocalRs[dtype][op]<<<bpr * n, kLocalThreads, 0, stream>>>(p);
   return cudaGetLastError();
