@@ -111,6 +111,76 @@ __global__ void __launch_bounds__(kLocalThreads, 2) local_ag_kernel(const __grid
   }
 }
 
+// All-gather through the tensor memory accelerator: one elected thread per CTA streams tiles of
+// the inputs into shared memory with 1-D bulk copies (cp.async.bulk, mbarrier completion) and
+// writes each tile to the n outputs with n bulk stores, NS stages deep. Full-line writes and no
+// per-element instructions; the broadcast is write-bound (n^2 C written, n C read).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+constexpr int kTmaStages = 4;
+
+__global__ void __launch_bounds__(32) local_ag_tma_kernel(const __grid_constant__ LPlan p, int piece) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  if (threadIdx.x != 0) return;
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const int64_t per_rank = (Cb + piece - 1) / piece;
+  const int64_t total = per_rank * n;
+  const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  for (int s = 0; s < kTmaStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto tile = [&](int64_t k, int& o, int64_t& off, uint32_t& len) {
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    o = static_cast<int>(t / per_rank);
+    off = (t - static_cast<int64_t>(o) * per_rank) * piece;
+    len = static_cast<uint32_t>(Cb - off < piece ? Cb - off : piece);
+  };
+  auto load = [&](int64_t k) {
+    int o;
+    int64_t off;
+    uint32_t len;
+    tile(k, o, off, len);
+    const int s = static_cast<int>(k % kTmaStages);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bars[s])), "r"(len)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(smem + static_cast<int64_t>(s) * piece)),
+                 "l"(p.send[o] + off), "r"(len), "r"(smem_addr(&bars[s]))
+                 : "memory");
+  };
+  for (int64_t k = 0; k < mine && k < kTmaStages; ++k) load(k);
+  uint32_t phase = 0;  // bit s = parity of stage s
+  for (int64_t k = 0; k < mine; ++k) {
+    const int s = static_cast<int>(k % kTmaStages);
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+                   : "=r"(done)
+                   : "r"(smem_addr(&bars[s])), "r"((phase >> s) & 1u)
+                   : "memory");
+    phase ^= 1u << s;
+    int o;
+    int64_t off;
+    uint32_t len;
+    tile(k, o, off, len);
+    const bool inplace = p.recv[o] + o * Cb == p.send[o];
+    for (int r = 0; r < n; ++r) {
+      if (inplace && r == o) continue;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p.recv[r] + o * Cb + off),
+                   "r"(smem_addr(smem + static_cast<int64_t>(s) * piece)), "r"(len)
+                   : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // the previous tile's stores have read their stage: refill it NS tiles ahead
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    if (k >= 1 && k - 1 + kTmaStages < mine) load(k - 1 + kTmaStages);
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Reduce-scatter: out[r] = tree(x_0..x_{n-1}), x_j = send[(r+j) % n] block r.
 template <int DT, int OP, int N>
 __device__ __forceinline__ void local_rs_body(const LPlan& p) {
@@ -202,7 +272,19 @@ cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize,
   }();
   const int bpr = static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(want, (static_cast<int64_t>(ctas_per_sm) * sm_count + n - 1) / n)));
-  if (kind == 0) local_ag_kernel<<<bpr * n, kLocalThreads, 0, stream>>>(p);
+  static const int tma_piece = [] {  // PAT_LOCAL_TMA=<tile bytes>: bulk-copy all-gather
+    const char* e = std::getenv("PAT_LOCAL_TMA");
+    return e && std::atoi(e) >= 1024 ? (std::atoi(e) & ~15) : 0;
+  }();
+  if (kind == 0 && tma_piece && vec == 16) {
+    const int smem = kTmaStages * tma_piece;
+    static int configured = 0;
+    if (configured != smem) {
+      cudaFuncSetAttribute(local_ag_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      configured = smem;
+    }
+    local_ag_tma_kernel<<<sm_count * std::max(1, ctas_per_sm / 2), 32, smem, stream>>>(p, tma_piece);
+  } else if (kind == 0) local_ag_kernel<<<bpr * n, kLocalThreads, 0, stream>>>(p);
   else kLocalRs[dtype][op]<<<bpr * n, kLocalThreads, 0, stream>>>(p);
   return cudaGetLastError();
 }
