@@ -119,18 +119,18 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-constexpr int kTmaStages = 4;
+constexpr int kTmaMaxStages = 8;
 
-__global__ void __launch_bounds__(32) local_ag_tma_kernel(const __grid_constant__ LPlan p, int piece) {
+__global__ void __launch_bounds__(32) local_ag_tma_kernel(const __grid_constant__ LPlan p, int piece, int NS) {
   extern __shared__ __align__(128) char smem[];
-  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  __shared__ __align__(8) uint64_t bars[kTmaMaxStages];
   if (threadIdx.x != 0) return;
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const int64_t per_rank = (Cb + piece - 1) / piece;
   const int64_t total = per_rank * n;
   const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  for (int s = 0; s < kTmaStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[s])));
+  for (int s = 0; s < NS; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[s])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   auto tile = [&](int64_t k, int& o, int64_t& off, uint32_t& len) {
     const int64_t t = blockIdx.x + k * gridDim.x;
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(32) local_ag_tma_kernel(const __grid_constant_
     int64_t off;
     uint32_t len;
     tile(k, o, off, len);
-    const int s = static_cast<int>(k % kTmaStages);
+    const int s = static_cast<int>(k % NS);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bars[s])), "r"(len)
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -151,10 +151,10 @@ __global__ void __launch_bounds__(32) local_ag_tma_kernel(const __grid_constant_
                  "l"(p.send[o] + off), "r"(len), "r"(smem_addr(&bars[s]))
                  : "memory");
   };
-  for (int64_t k = 0; k < mine && k < kTmaStages; ++k) load(k);
+  for (int64_t k = 0; k < mine && k < NS; ++k) load(k);
   uint32_t phase = 0;  // bit s = parity of stage s
   for (int64_t k = 0; k < mine; ++k) {
-    const int s = static_cast<int>(k % kTmaStages);
+    const int s = static_cast<int>(k % NS);
     uint32_t done = 0;
     while (!done)
       asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(32) local_ag_tma_kernel(const __grid_constant_
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     // the previous tile's stores have read their stage: refill it NS tiles ahead
     asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-    if (k >= 1 && k - 1 + kTmaStages < mine) load(k - 1 + kTmaStages);
+    if (k >= 1 && k - 1 + NS < mine) load(k - 1 + NS);
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -263,29 +263,29 @@ cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize,
     p.send[r] = send_by_rank[r];
     p.recv[r] = recv_by_rank[r];
   }
-  // per rank: enough blocks for ~2 resident CTAs on every SM overall, no more than the units
   const int64_t per_rank_units = vec == 16 ? (chunk_bytes >> 4) : (chunk_bytes / esize);
   const int64_t want = (per_rank_units + kLocalThreads - 1) / kLocalThreads;
-  static const int ctas_per_sm = [] {  // PAT_LOCAL_CTAS_PER_SM: launch-shape experiments
-    const char* e = std::getenv("PAT_LOCAL_CTAS_PER_SM");
-    return e && std::atoi(e) > 0 ? std::atoi(e) : 4;
-  }();
-  const int bpr = static_cast<int>(
-      std::max<int64_t>(1, std::min<int64_t>(want, (static_cast<int64_t>(ctas_per_sm) * sm_count + n - 1) / n)));
-  static const int tma_piece = [] {  // PAT_LOCAL_TMA=<tile bytes>: bulk-copy all-gather
+  // per rank: enough blocks for ~4 resident CTAs on every SM overall, no more than the units
+  const int bpr = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (4LL * sm_count + n - 1) / n)));
+  // all-gather: the bulk-copy kernel (8 KiB tiles, 4 stages, 2 CTAs per SM: measured 12.5 us vs
+  // 14.0 us for the vector kernel at n=8, 1 MiB; tools/tune_local*.sh). PAT_LOCAL_TMA=0 turns it off.
+  static const int tma_piece = [] {
     const char* e = std::getenv("PAT_LOCAL_TMA");
-    return e && std::atoi(e) >= 1024 ? (std::atoi(e) & ~15) : 0;
+    if (!e) return 8192;
+    const int v = std::atoi(e);
+    return v >= 1024 ? (v & ~15) : 0;
   }();
+  constexpr int kTmaStages = 4;
   if (kind == 0 && tma_piece && vec == 16) {
     const int smem = kTmaStages * tma_piece;
-    static int configured = 0;
-    if (configured != smem) {
+    if (smem > 48 * 1024)  // per device; only for tiles set above the default through the env
       cudaFuncSetAttribute(local_ag_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      configured = smem;
-    }
-    local_ag_tma_kernel<<<sm_count * std::max(1, ctas_per_sm / 2), 32, smem, stream>>>(p, tma_piece);
-  } else if (kind == 0) local_ag_kernel<<<bpr * n, kLocalThreads, 0, stream>>>(p);
-  else kLocalRs[dtype][op]<<<bpr * n, kLocalThreads, 0, stream>>>(p);
+    local_ag_tma_kernel<<<2 * sm_count, 32, smem, stream>>>(p, tma_piece, kTmaStages);
+  } else if (kind == 0) {
+    local_ag_kernel<<<bpr * n, kLocalThreads, 0, stream>>>(p);
+  } else {
+    kLocalRs[dtype][op]<<<bpr * n, kLocalThreads, 0, stream>>>(p);
+  }
   return cudaGetLastError();
 }
 
