@@ -398,7 +398,7 @@ def run_pat(args, rank, world, local):
     if world == 1:
         algo_bytes = (n * n + n) * C  # local mode: read n*C + write n^2*C (AG) / read n^2*C + write n*C (RS)
         peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-        roof = {"bound": "hbm", "kernel": ("local_rs_kernel" if dom == "reduce_scatter" else "local_ag_kernel"), "unit": "GB/s",
+        roof = {"bound": "hbm", "kernel": ("local_rs_kernel" if dom == "reduce_scatter" else "local_ag_tma_kernel"), "unit": "GB/s",
                 "algorithmic_bytes_per_launch": algo_bytes, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
     else:
         algo_bytes = (n - 1) * C  # per rank, received over NVLink
