@@ -188,6 +188,35 @@ int main(int argc, char** argv) {
       }
     }, bytes);
   }
+  {  // copy engines and SM stores sharing the same link: fraction f of every GPU's 1 GiB rides
+     // the copy engine (second stream), the rest an SM push kernel, both started together
+    std::vector<cudaStream_t> st2(G);
+    for (int d = 0; d < G; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaStreamCreateWithFlags(&st2[d], cudaStreamNonBlocking));
+    }
+    std::vector<cudaEvent_t> fork(G), join(G);
+    for (int d = 0; d < G; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaEventCreateWithFlags(&fork[d], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&join[d], cudaEventDisableTiming));
+    }
+    for (int pct : {25, 33, 50, 67}) {
+      const size_t ce_bytes = (bytes * pct / 100) & ~size_t(4095);
+      const size_t sm16 = (bytes - ce_bytes) / 16;
+      char nm[64];
+      std::snprintf(nm, sizeof nm, "mixed-ring ce %d%% + sm push", pct);
+      run(nm, G, [&](int d) {
+        CK(cudaSetDevice(d));
+        CK(cudaEventRecord(fork[d], st[d]));
+        CK(cudaStreamWaitEvent(st2[d], fork[d], 0));
+        CK(cudaMemcpyPeerAsync(dst[(d + 1) % G], (d + 1) % G, src[d], d, ce_bytes, st2[d]));
+        copy_kernel<8><<<148, 512, 0, st[d]>>>((const uint4*)(src[d] + ce_bytes), (uint4*)(dst[(d + 1) % G] + ce_bytes), sm16);
+        CK(cudaEventRecord(join[d], st2[d]));
+        CK(cudaStreamWaitEvent(st[d], join[d], 0));
+      }, bytes);
+    }
+  }
   run("ce-uni", 1, [&](int d) { CK(cudaMemcpyPeerAsync(dst[1], 1, src[0], 0, bytes, st[d])); }, bytes);
   run("ce-ring", G, [&](int d) { CK(cudaMemcpyPeerAsync(dst[(d + 1) % G], (d + 1) % G, src[d], d, bytes, st[d])); },
       bytes);
