@@ -61,6 +61,17 @@ __global__ void __launch_bounds__(512) copy_blocked(const uint4* __restrict__ sr
   for (; i < end; i += B) dst[i] = src[i];
 }
 
+// A persistent kernel that occupies SMs while polling a local word (what the PAT kernel does
+// while the copy engines move leaves): does it slow the copy engines down?
+__global__ void __launch_bounds__(512) spin_kernel(const volatile uint64_t* flag, uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    (void)*flag;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 int main(int argc, char** argv) {
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -214,6 +225,24 @@ int main(int argc, char** argv) {
         copy_kernel<8><<<148, 512, 0, st[d]>>>((const uint4*)(src[d] + ce_bytes), (uint4*)(dst[(d + 1) % G] + ce_bytes), sm16);
         CK(cudaEventRecord(join[d], st2[d]));
         CK(cudaStreamWaitEvent(st[d], join[d], 0));
+      }, bytes);
+    }
+  }
+  {
+    std::vector<cudaStream_t> st3(G);
+    std::vector<uint64_t*> word(G);
+    for (int d = 0; d < G; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaStreamCreateWithFlags(&st3[d], cudaStreamNonBlocking));
+      CK(cudaMalloc(&word[d], 64));
+      CK(cudaMemset(word[d], 0, 64));
+    }
+    for (int ctas : {128, 148}) {
+      char nm[64];
+      std::snprintf(nm, sizeof nm, "ce-ring + spinning kernel %d CTAs", ctas);
+      run(nm, G, [&](int d) {
+        spin_kernel<<<ctas, 512, 0, st3[d]>>>(word[d], 1500000);  // 1.5 ms
+        CK(cudaMemcpyPeerAsync(dst[(d + 1) % G], (d + 1) % G, src[d], d, bytes, st[d]));
       }, bytes);
     }
   }
