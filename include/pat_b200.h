@@ -105,14 +105,14 @@ typedef struct {
   size_t size;              /* sizeof(patConfig_t) */
   size_t staging_bytes;     /* cap on the per-rank inbox pool (all protocol regions, flags aside);
                                0 = default (512 MiB of SIMPLE slots + the LL region) */
-  size_t slice_bytes;       /* SIMPLE bytes per slot per pipeline step; 0 = default 128 KiB */
+  size_t slice_bytes;       /* SIMPLE bytes per slot per pipeline step; 0 = 64-256 KiB from the pool budget */
   size_t ll_threshold;      /* per-rank chunk bytes up to which LL is used; 0 = cost model */
   int trees;                /* PAT tree count T; 0 = max_trees(n) (full aggregation) */
   int max_channels;         /* CTAs per rank; 0 = default */
   int protocol;             /* patProtocol_t */
   int timeout_ms;           /* device-side spin timeout; 0 = default 20000 */
-  int threads;              /* threads per CTA; 0 = default */
-  int depth;                /* inbox buffers per channel (pipeline depth); 0 = default 2 */
+  int threads;              /* threads per CTA, <= 512; 0 = 512 */
+  int depth;                /* inbox buffers per channel (pipeline depth); 0 = ceil(log2 n) + 1 */
   int direct;               /* all-gather zero-copy push into peers' recvbufs: -1 off, 0 auto, 1 on.
                                auto = single-process communicator whose recvbufs are reachable
                                (same device, or cudaMalloc memory with peer access) */
