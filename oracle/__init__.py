@@ -40,7 +40,7 @@ ERRORS = {
     1: "ScheduleError", 2: "NonPowerOfTwoError", 3: "InvalidTreeCountError",
     4: "BufferTooSmallError", 5: "RankOutOfRangeError", 10: "SimulationError",
     11: "PayloadShapeError", 12: "UnsupportedOpError", 13: "InvalidScheduleError",
-    20: "CapacityError",
+    20: "CapacityError", 30: "ParseError",
 }
 
 

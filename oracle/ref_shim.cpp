@@ -17,6 +17,7 @@
 #include "patsim/algorithms.hpp"
 #include "patsim/oracle.hpp"
 #include "patsim/schedule.hpp"
+#include "patsim/serialize.hpp"
 #include "patsim/simulate.hpp"
 
 using namespace patsim;
@@ -26,6 +27,7 @@ namespace {
 thread_local std::string g_last_error;
 
 int code_of(const std::exception& e) {
+  if (dynamic_cast<const ParseError*>(&e)) return 30;
   if (dynamic_cast<const NonPowerOfTwoError*>(&e)) return 2;
   if (dynamic_cast<const InvalidTreeCountError*>(&e)) return 3;
   if (dynamic_cast<const BufferTooSmallError*>(&e)) return 4;
@@ -146,6 +148,22 @@ int ref_schedule(int kind, int algo, int n, int trees, int32_t* buf, int64_t cap
     if (kind == 1) s = mirror_schedule(s);
     return encode(s, buf, cap, len);
   });
+}
+
+// schedule_to_json / schedule_from_json (serialize.cpp:49-101): the schedule file format
+int64_t ref_schedule_to_json(const int32_t* in, int64_t in_len, int indent, char* out, int64_t cap) {
+  int64_t n = -1;
+  guarded([&] {
+    const std::string t = schedule_to_json(decode(in, in_len), indent);
+    n = static_cast<int64_t>(t.size());
+    if (out && cap > n) std::memcpy(out, t.c_str(), t.size() + 1);
+    return 0;
+  });
+  return n;
+}
+
+int ref_schedule_from_json(const char* text, int32_t* out, int64_t cap, int64_t* len) {
+  return guarded([&] { return encode(schedule_from_json(text), out, cap, len); });
 }
 
 int ref_mirror(const int32_t* in, int64_t in_len, int32_t* out, int64_t cap, int64_t* len) {

@@ -7,6 +7,7 @@ Generation, mirroring, validation and slot accounting run in the product's C++ h
 from __future__ import annotations
 
 import ctypes
+import json
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import Optional
@@ -80,6 +81,105 @@ class RelativeSchedule:  # schedule.hpp:78-86
                                           b[p + 6: p + 6 + nk]))
             p += 6 + nk
         return s
+
+
+# ------------------------------------------------------------------ schedule files
+# The reference's schedule JSON format (serialize.cpp:49-101, proj/README.md:95-112): what
+# `patsim schedule` writes and `patsim verify` reads. Imported schedules reach the GPU executor
+# through patAllGatherSchedule / patReduceScatterSchedule, which validate them first.
+
+_ALGO_TAGS = {Algorithm.Ring: "ring", Algorithm.BruckNearest: "bruck-nearest",
+              Algorithm.BruckFarthest: "bruck-farthest", Algorithm.RecursiveDoubling: "recursive-doubling",
+              Algorithm.Pat: "pat"}
+_KIND_TAGS = {CollectiveKind.AllGather: "allgather", CollectiveKind.ReduceScatter: "reducescatter"}
+
+
+class ParseError(RuntimeError):  # serialize.hpp:12
+    pass
+
+
+def schedule_to_json(s: RelativeSchedule, indent: int = 2) -> str:
+    """serialize.cpp:49-72: key order algorithm, kind, n_ranks, params, rounds; arrays of
+    offsets on one line; the text nlohmann::ordered_json::dump(indent) produces, plus a newline."""
+    params = {} if s.params is None else {"trees": s.params.trees, "buffer_slots": s.params.buffer_slots}
+    rounds = [{"round": r.round_index, "dim": r.dimension, "split": r.split_index, "peer": r.peer_send_offset,
+               "chunks": list(r.chunk_offsets)} for r in s.rounds]
+    if indent < 0:
+        doc = {"algorithm": _ALGO_TAGS[Algorithm(s.algorithm)], "kind": _KIND_TAGS[CollectiveKind(s.kind)],
+               "n_ranks": s.n_ranks, "params": params, "rounds": rounds}
+        return json.dumps(doc, separators=(",", ":")) + "\n"
+    pad = " " * indent
+
+    def obj(d: dict, level: int) -> str:
+        if not d:
+            return "{}"
+        inner = pad * (level + 1)
+        items = []
+        for k, v in d.items():
+            if isinstance(v, list) and (not v or not isinstance(v[0], dict)):
+                val = "[" + ",".join(str(x) for x in v) + "]"
+            elif isinstance(v, list):
+                val = "[\n" + ",\n".join(inner + pad + obj(x, level + 2) for x in v) + "\n" + inner + "]"
+            elif isinstance(v, dict):
+                val = obj(v, level + 1)
+            else:
+                val = json.dumps(v)
+            items.append(f"{inner}{json.dumps(k)}: {val}")
+        return "{\n" + ",\n".join(items) + "\n" + pad * level + "}"
+
+    doc = {"algorithm": _ALGO_TAGS[Algorithm(s.algorithm)], "kind": _KIND_TAGS[CollectiveKind(s.kind)],
+           "n_ranks": s.n_ranks, "params": params, "rounds": rounds}
+    return obj(doc, 0) + "\n"
+
+
+def schedule_from_json(text: str) -> RelativeSchedule:
+    """serialize.cpp:74-101, with the reference's ParseError messages."""
+    try:
+        doc = json.loads(text)
+    except (ValueError, TypeError):
+        raise ParseError("malformed JSON in schedule") from None
+
+    def field(o: dict, name: str, where: str, types):
+        if not isinstance(o, dict) or name not in o:
+            raise ParseError(f'{where} is missing field "{name}"')
+        v = o[name]
+        if not isinstance(v, types) or (isinstance(v, bool) and types is not bool):
+            raise ParseError(f'{where} field "{name}" has the wrong type')
+        return v
+
+    algo = {v: k for k, v in _ALGO_TAGS.items()}
+    kind = {v: k for k, v in _KIND_TAGS.items()}
+    atag = field(doc, "algorithm", "schedule", str)
+    if atag not in algo:
+        raise ParseError(f'unknown algorithm tag "{atag}"')
+    ktag = field(doc, "kind", "schedule", str)
+    if ktag not in kind:
+        raise ParseError(f'unknown kind "{ktag}"')
+    n = field(doc, "n_ranks", "schedule", int)
+    if "params" not in doc:
+        raise ParseError('schedule is missing field "params"')
+    params = doc["params"]
+    if not isinstance(params, dict):
+        raise ParseError('schedule field "params" must be an object')
+    pp = None
+    if params:
+        pp = PatParams(field(params, "trees", "params", int), field(params, "buffer_slots", "params", int))
+    if "rounds" not in doc:
+        raise ParseError('schedule is missing field "rounds"')
+    rounds = doc["rounds"]
+    if not isinstance(rounds, list):
+        raise ParseError('schedule field "rounds" must be an array')
+    exchange = algo[atag] == Algorithm.RecursiveDoubling  # XOR partnering implied by the algorithm
+    out = RelativeSchedule(kind[ktag], algo[atag], n, pp, [])
+    for r in rounds:
+        rr = RelativeRound(field(r, "round", "round", int), field(r, "dim", "round", int),
+                           field(r, "split", "round", int), field(r, "peer", "round", int), exchange, [])
+        chunks = field(r, "chunks", "round", list)
+        if any(not isinstance(x, int) or isinstance(x, bool) for x in chunks):
+            raise ParseError('round field "chunks" has the wrong type')
+        rr.chunk_offsets = list(chunks)
+        out.rounds.append(rr)
+    return out
 
 
 def _i32(a: np.ndarray):

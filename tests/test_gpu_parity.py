@@ -463,3 +463,22 @@ def test_cost_model_protocol_choice():
         plan = comm.plan(0, nbytes // 4, O.FLOAT32)
         assert plan["protocol"] == want, (n, nbytes, plan)
         assert plan["predicted_us"] > 0
+
+
+def test_schedule_imported_from_json_runs_on_gpu():
+    """§8 f2: a schedule read from the reference's JSON format runs on the generic executor; an
+    invalid one is refused with the reference's InvalidScheduleError before any launch."""
+    n = 8
+    comm = comm_for(n, fused=-1)
+    for ag in (S.pat_allgather(n, 1), S.bruck_nearest(n)):
+        imported = S.schedule_from_json(S.schedule_to_json(ag))
+        p = O.random_payload(O.INT32, n, 999, 5)
+        got = gpu_allgather(comm, [0] * n, p, 999, O.INT32, schedule=imported)
+        want, _ = O.run_allgather(ag.encode(), O.INT32, p, 999)
+        assert all(same(got[r], want[r]) for r in range(n))
+    partial = S.schedule_from_json('{"algorithm": "pat", "kind": "allgather", "n_ranks": 8, "params": '
+                                   '{"trees": 2, "buffer_slots": 4}, "rounds": [{"round": 0, "dim": 2, '
+                                   '"split": 0, "peer": 4, "chunks": [0]}]}')
+    with pytest.raises(PatError) as e:
+        gpu_allgather(comm, [0] * n, O.random_payload(O.INT32, n, 10, 1), 10, O.INT32, schedule=partial)
+    assert e.value.kind == "InvalidScheduleError"
