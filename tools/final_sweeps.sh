@@ -2,6 +2,8 @@
 export PAT_TIMEOUT_MS=10000
 mkdir -p gpurun_out/final; rm -f gpurun_out/final/*
 O=gpurun_out/final
+timeout 900 python -m pytest tests -q -m gpu > $O/pytest.log 2>&1; echo pytest rc=$?; tail -2 $O/pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke rc=$?; tail -1 $O/smoke.log
 # latency sweeps, graph mode, multi-process (torchrun) vs NCCL Ring
 for N in 2 3 4; do
   timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2970$N \
@@ -9,7 +11,7 @@ for N in 2 3 4; do
   echo graph $N rc=$?
 done
 # bandwidth sweeps, loop mode (L2 flushed per call), multi-process vs NCCL Ring
-for N in 2 4; do
+for N in 2 3 4; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2971$N \
     bench_sweep.py --mode loop --min-bytes 8388608 --max-bytes 1073741824 --iters 10 --warmup 3 --dtypes f32,bf16 \
     --out $O/sweep_n${N}_loop.jsonl > $O/sweep_n${N}_loop.log 2>&1
