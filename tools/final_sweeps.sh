@@ -28,7 +28,7 @@ for N in 2 4; do
   timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2972$N bench.py --gpus $N > $O/bench$N.json 2> $O/bench$N.err; echo bench$N rc=$?
 done
 # ncu: launch list of the N=1 bench command, full set on the fused local kernels and on the
-# transport kernel (local mode, LL128 at 1 MiB)
+# transport kernel (local mode, LL at 1 MiB)
 C="python bench.py --steps 20 --warmup 3 --no-cpu-baseline"
 timeout 200 $C > $O/plain.log 2>&1 && timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_local.csv $C > $O/ncu_l.log 2>&1; echo ncu-launch rc=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:local_ -s 40 -c 4 -o $O/prof_local_fused $C > $O/ncu_f.log 2>&1; echo ncu-full rc=$?

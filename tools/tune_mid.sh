@@ -1,5 +1,5 @@
 # SIMPLE mid-size knobs (4-64 MiB per rank), n=4 torchrun, loop + graph mode.
-export PAT_TIMEOUT_MS=10000 PAT_LL128_THRESHOLD=1
+export PAT_TIMEOUT_MS=10000 PAT_LL_THRESHOLD=1
 mkdir -p gpurun_out/tunemid
 run() {  # tag, env...
   tag=$1; shift
