@@ -47,6 +47,7 @@ constexpr int kDefaultChannels = 128;            // clamped to co-residency at l
 // LL vs bulk is chosen by the calibrated cost model below (choose_slicing): LL to 2 MiB at
 // n <= 3, to 1 MiB at n >= 4 (profiles/r01c_forced_n*_p*.jsonl).
 constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
+constexpr int64_t kPullMinRS = 1 << 20;    // ... and above this one (LL wins below anyway)
 constexpr size_t kLLSlotBytes = 32 << 10;  // LL slot: 16 KiB payload per channel-step (2 MiB per step)
 constexpr int kDefaultTimeoutMs = 20000;
 
@@ -99,6 +100,7 @@ struct patComm {
   size_t ll_slot_bytes = 0;                // LL inbox slot (own region, common_init)
   size_t region_off[4] = {};               // inbox region of each protocol within a pool
   int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
+  int skew = 1;            // SIMPLE / PULL sender skew distance (PAT_SKEW; 0 = rounds in order)
   int channels = 0;
   int* err_host = nullptr;
   int* err_dev = nullptr;
@@ -467,6 +469,7 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   {
     long long v = 0;
     comm->pull_slice = env_int("PAT_PULL_SLICE", &v) && v >= 256 ? (v & ~15LL) : (512 << 10);
+    comm->skew = env_int("PAT_SKEW", &v) ? static_cast<int>(std::max(0LL, v)) : 1;
   }
   const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
   // Inbox regions: SIMPLE/PULL slots, then LL slots. LL polls its lines, so it gets its own
@@ -550,8 +553,10 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   if (patResult_t e = channel_cap(comm, kind, dtype, op, &cap)) return e;
   // one device holds every rank: .gpu-scope flags; zero-copy all-gather is always safe
   const bool single_device = !comm->multiprocess && comm->groups.size() == 1;
-  // PULL reads the peers' user buffers: they must be mapped into every device of this process
-  bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple;
+  // PULL reads the peers' user buffers: they must be mapped into every device of this process.
+  // Auto mode only pulls mid-size reduce-scatters, so small calls skip the pointer queries.
+  bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple &&
+                 (comm->cfg.protocol == patProtoPull || (kind == kRS && chunk_bytes > kPullMinRS));
   for (size_t l = 0; l < comm->lranks.size() && pull_ok && !single_device; ++l)
     pull_ok = legacy_ipc_capable(sendbuffs[l]) && (kind == kRS || legacy_ipc_capable(recvbuffs[l]));
   const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds);
@@ -588,10 +593,8 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL ? comm->ll_slot_bytes : comm->slot_bytes);
     p.depth = comm->cfg.depth;
     {
-      long long sk = 1;
-      env_int("PAT_SKEW", &sk);
       // skew distance L: the sender keeps (nrounds-1)*L+1 steps in flight -> needs that many buffers
-      const int L = static_cast<int>(std::max(0LL, sk));
+      const int L = comm->skew;
       if (p.proto == kProtoPull)  // all-gather pull stages nothing: no credit bound on the skew
         p.skew = (L > 0 && p.nrounds > 1 && (kind == kAG || p.depth >= (p.nrounds - 1) * L + 1)) ? L : 0;
       else
@@ -888,8 +891,10 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   DeviceGuard guard;
   int cap = 0;
   if (patResult_t e = channel_cap(comm, kind, dtype, 0, &cap)) return e;
-  const Slicing sl = choose_slicing(comm, kind, cb, cap, !comm->multiprocess,  // assumes cudaMalloc buffers
-                                    cp->proto.nrounds);
+  // as run_collective decides, assuming cudaMalloc'd (peer-reachable) buffers
+  const bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple &&
+                       (comm->cfg.protocol == patProtoPull || (kind == kRS && cb > kPullMinRS));
+  const Slicing sl = choose_slicing(comm, kind, cb, cap, pull_ok, cp->proto.nrounds);
   std::memset(info, 0, sizeof(*info));
   info->protocol = sl.proto;
   info->trees = trees;

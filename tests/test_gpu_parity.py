@@ -436,7 +436,7 @@ def test_protocol_switches_share_no_inbox_state(spread):
         pytest.skip("needs >= 2 GPUs")
     comm = comm_for(n, devices, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=16384)
     for it in range(24):
-        elems = [200, 5000, 60000, 3000][it % 4]  # LL, bulk, bulk, LL (4-byte elements)
+        elems = [200, 5000, 300000, 3000][it % 4]  # LL, bulk, bulk (RS: PULL), LL (4-byte elements)
         p = (np.arange(n * elems, dtype=np.int64) % 64 + 1 + it).astype(np.int32)
         got = gpu_allgather(comm, devices, p, elems, O.INT32)
         want = oracle_ag(n, O.max_trees(n), O.INT32, p, elems)
@@ -445,9 +445,9 @@ def test_protocol_switches_share_no_inbox_state(spread):
         got = gpu_reduce_scatter(comm, devices, q, elems, O.INT32, O.SUM)
         want = oracle_rs(n, O.max_trees(n), O.INT32, O.SUM, q, elems)
         assert all(same(got[r], want[r]) for r in range(n)), (it, elems, mismatch(got, want, elems))
-    plans = [comm.plan(k, e, O.INT32)["protocol"] for k in (0, 1) for e in (200, 5000, 60000)]
+    plans = [comm.plan(k, e, O.INT32)["protocol"] for k in (0, 1) for e in (200, 5000, 300000)]
     assert plans == [_lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_SIMPLE,
-                     _lib.PROTO_LL, _lib.PROTO_PULL, _lib.PROTO_PULL], plans
+                     _lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_PULL], plans
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
