@@ -893,7 +893,7 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   if (patResult_t e = channel_cap(comm, kind, dtype, 0, &cap)) return e;
   // as run_collective decides, assuming cudaMalloc'd (peer-reachable) buffers
   const bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple &&
-                       (comm->cfg.protocol == patProtoPull || (kind == kRS && cb > kPullMinRS));
+                       (comm->cfg.protocol == patProtoPull || (static_cast<int>(kind) == kRS && cb > kPullMinRS));
   const Slicing sl = choose_slicing(comm, kind, cb, cap, pull_ok, cp->proto.nrounds);
   std::memset(info, 0, sizeof(*info));
   info->protocol = sl.proto;
