@@ -482,3 +482,31 @@ def test_schedule_imported_from_json_runs_on_gpu():
     with pytest.raises(PatError) as e:
         gpu_allgather(comm, [0] * n, O.random_payload(O.INT32, n, 10, 1), 10, O.INT32, schedule=partial)
     assert e.value.kind == "InvalidScheduleError"
+
+
+def test_randomized_configurations():
+    """Fuzz: random rank counts, placements, dtypes, ops, sizes, alignments, protocols and tree
+    counts on long-lived communicators, every result bit-exact against the oracle."""
+    rng = np.random.default_rng(2506)
+    dtypes = [O.INT8, O.UINT8, O.INT32, O.UINT32, O.INT64, O.FLOAT16, O.FLOAT32, O.FLOAT64, O.BFLOAT16]
+    for case in range(40):
+        n = int(rng.integers(2, 9))
+        spread = NGPU >= 2 and rng.random() < 0.5
+        devices = [r % NGPU for r in range(n)] if spread else [0] * n
+        proto = int(rng.choice([_lib.PROTO_AUTO, _lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_PULL]))
+        trees = int(rng.choice(O.valid_tree_counts(n)))
+        comm = comm_for(n, devices, protocol=proto, trees=trees, fused=-1 if rng.random() < 0.7 else 0,
+                        channels=int(rng.choice([1, 3, 8, 32])), staging_bytes=n * int(rng.choice([64, 512])) * 1024)
+        dt = int(rng.choice(dtypes))
+        es = _lib.DTYPE_SIZE[dt]
+        elems = int(rng.choice([1, 3, 17, 1000, 4099, 65536, 200003]))
+        pad = int(rng.choice([0, es, 16]))
+        p = O.random_payload(dt, n, elems, case)
+        got = gpu_allgather(comm, devices, p, elems, dt, pad=pad)
+        want = oracle_ag(n, trees, dt, p, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), ("ag", case, n, devices, proto, trees, dt, elems, pad)
+        op = int(rng.choice([O.SUM, O.PROD, O.MAX, O.MIN]))
+        q = O.random_payload(dt, n * n, elems, case + 1000)
+        got = gpu_reduce_scatter(comm, devices, q, elems, dt, op, pad=pad)
+        want = oracle_rs(n, trees, dt, op, q, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), ("rs", case, n, devices, proto, trees, dt, op, elems, pad)
