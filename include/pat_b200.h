@@ -93,20 +93,24 @@ typedef enum { patSum = 0, patProd = 1, patMax = 2, patMin = 3, patNumOps = 4 } 
 typedef enum { patAllGatherKind = 0, patReduceScatterKind = 1 } patCollKind_t;
 typedef enum { patAlgoRing = 0, patAlgoBruckNearest = 1, patAlgoBruckFarthest = 2,
                patAlgoRecursiveDoubling = 3, patAlgoPat = 4 } patAlgorithm_t;
-/* LL: flag-in-line stores for small chunks. SIMPLE: pushed slices through the peers' inbox pools.
+/* LL32: 32-byte lines {28 payload bytes, flag} written by one 32-byte store each, polled by the
+   receiver: small and mid-size chunks. LL: 16-byte lines {4 B, flag, 4 B, flag} (8-byte store
+   atomicity only; selectable, no longer chosen by auto).
+   SIMPLE: pushed slices through the peers' inbox pools.
    PULL: receivers read the upstream's buffers (user sendbuf / recvbuf, staged RS partials);
    needs every rank's user buffers mapped in this process (patCommInitAll, cudaMalloc memory).
-   Auto: LL while the calibrated cost model predicts it faster (or up to ll_threshold when that
+   Auto: LL32 while the calibrated cost model predicts it faster (or up to ll_threshold when that
    is set), then SIMPLE — except reduce-scatter
    below 128 MiB, which PULLs where possible (measured, profiles/r01_sp_simple_vs_pull.jsonl). */
-typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3 } patProtocol_t;
+typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3,
+               patProtoLL32 = 5 } patProtocol_t;
 
 typedef struct {
   size_t size;              /* sizeof(patConfig_t) */
   size_t staging_bytes;     /* cap on the per-rank inbox pool (all protocol regions, flags aside);
                                0 = default (512 MiB of SIMPLE slots + the LL region) */
   size_t slice_bytes;       /* SIMPLE bytes per slot per pipeline step; 0 = 64-256 KiB from the pool budget */
-  size_t ll_threshold;      /* per-rank chunk bytes up to which LL is used; 0 = cost model */
+  size_t ll_threshold;      /* per-rank chunk bytes up to which LL32 is used; 0 = cost model */
   int trees;                /* PAT tree count T; 0 = max_trees(n) (full aggregation) */
   int max_channels;         /* CTAs per rank; 0 = default */
   int protocol;             /* patProtocol_t */

@@ -27,7 +27,7 @@ RESULTS = {
 # datatypes (ncclDataType_t numbering) and ops (ncclRedOp_t numbering)
 INT8, UINT8, INT32, UINT32, INT64, UINT64, FLOAT16, FLOAT32, FLOAT64, BFLOAT16 = range(10)
 SUM, PROD, MAX, MIN = range(4)
-PROTO_AUTO, PROTO_LL, PROTO_SIMPLE, PROTO_PULL = 0, 1, 2, 3
+PROTO_AUTO, PROTO_LL, PROTO_SIMPLE, PROTO_PULL, PROTO_LL32 = 0, 1, 2, 3, 5
 DTYPE_SIZE = {INT8: 1, UINT8: 1, INT32: 4, UINT32: 4, INT64: 8, UINT64: 8, FLOAT16: 2,
               FLOAT32: 4, FLOAT64: 8, BFLOAT16: 2}
 

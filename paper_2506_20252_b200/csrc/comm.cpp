@@ -44,11 +44,10 @@ constexpr uint32_t kMagic = 0x50415442;                                       //
 constexpr size_t kDefaultPoolBytes = 512ull << 20;  // inbox pool budget per rank (all channels)
 constexpr size_t kMinSlice = 64 << 10, kMaxSlice = 256 << 10;
 constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
-// LL vs bulk is chosen by the calibrated cost model below (choose_slicing): LL to 2 MiB at
-// n <= 3, to 1 MiB at n >= 4 (profiles/r01c_forced_n*_p*.jsonl).
+// LL32 vs bulk is chosen by the calibrated cost model below (choose_slicing).
 constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
 constexpr int64_t kPullMinRS = 1 << 20;    // ... and above this one (LL wins below anyway)
-constexpr size_t kLLSlotBytes = 32 << 10;  // LL slot: 16 KiB payload per channel-step (2 MiB per step)
+constexpr size_t kLLSlotBytes = 32 << 10;  // LL / LL32 slot: 16 / 28 KiB payload per channel-step
 constexpr int kDefaultTimeoutMs = 20000;
 
 struct Compiled {
@@ -97,8 +96,8 @@ struct patComm {
   std::vector<DevGroup> groups;
   std::vector<void*> ipc_opened;
   size_t slot_bytes = 0, pool_bytes = 0;
-  size_t ll_slot_bytes = 0;                // LL inbox slot (own region, common_init)
-  size_t region_off[4] = {};               // inbox region of each protocol within a pool
+  size_t ll_slot_bytes = 0;                // LL and LL32 inbox slot (own regions, common_init)
+  size_t region_off[kNumProtoSlots] = {};  // inbox region of each protocol within a pool
   int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
   int skew = 1;            // SIMPLE / PULL sender skew distance (PAT_SKEW; 0 = rounds in order)
   int channels = 0;
@@ -181,9 +180,9 @@ void fill_defaults(patConfig_t* c, int n) {
   c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(15));
   if (c->staging_bytes != 0) {
     // explicit budget for the whole pool (flags aside): channels * depth * (n-1) slot triples,
-    // one SIMPLE/PULL slot plus the LL slot (<= 32 KiB)
+    // one SIMPLE/PULL slot plus the LL and LL32 slots (<= 32 KiB each)
     const size_t b = c->staging_bytes > 8192 ? (c->staging_bytes - 8192) / slots : 0;
-    size_t s = b >= 2 * kLLSlotBytes ? b - kLLSlotBytes : b / 2;
+    size_t s = b >= 3 * kLLSlotBytes ? b - 2 * kLLSlotBytes : b / 3;
     s &= ~size_t(127);
     if (s < 256) s = 256;
     c->slice_bytes = s;
@@ -370,28 +369,41 @@ struct Slicing {
 
 // Alpha-beta model of one call (the reference's costmodel.cpp:70-104 prices a
 // schedule as rounds x (alpha + beta x bytes)), calibrated on B200 by tools/fit_costmodel.py
-// from forced-protocol sweeps at n = 2, 3, 4 (profiles/r01c_costmodel_fit.json):
-//   t = steps x (a + b x R) + wire x (n-1) x C / B        (LL: one fixed cost per LL step)
+// from forced-protocol sweeps at n = 2, 3, 4 (profiles/r01f_costmodel_fit.json):
+//   t = steps x (a + b x R) + wire x (n-1) x C / B        (LL, LL32: one fixed cost per step)
 //   t = a + b x R + (n-1) x C / B                          (SIMPLE / PULL: steps pipelined)
 // R = PAT rounds. (n-1) x C does not depend on T, so T = max_trees (fewest rounds) is optimal.
 struct CostRow {
   double a_us, b_us, gbs, wire;
 };
-constexpr CostRow kCostLL{3.59, 1.28, 510.0, 2.0};
-constexpr CostRow kCostBulk{5.83, 6.43, 561.0, 1.0};
+constexpr CostRow kCostLL{3.41, 1.40, 565.0, 2.0};
+constexpr CostRow kCostLL32{3.92, 1.49, 604.0, 32.0 / 28.0};
+constexpr CostRow kCostBulk{5.99, 6.11, 560.0, 1.0};
 
 double predict_us(int proto, int n, int rounds, int64_t chunk_bytes, int iters) {
-  const CostRow& c = proto == kProtoLL ? kCostLL : kCostBulk;
-  const double fixed = (proto == kProtoLL ? std::max(iters, 1) : 1) * (c.a_us + c.b_us * rounds);
+  const bool ll = proto == kProtoLL || proto == kProtoLL32;
+  const CostRow& c = proto == kProtoLL ? kCostLL : proto == kProtoLL32 ? kCostLL32 : kCostBulk;
+  const double fixed = (ll ? std::max(iters, 1) : 1) * (c.a_us + c.b_us * rounds);
   return fixed + c.wire * (n - 1) * static_cast<double>(chunk_bytes) / (c.gbs * 1e3);
 }
 
-Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int channels) {
+// LL32 payload bytes per group of 32 lines (transport.cuh, LL32Shape): 28-byte lines, 24 for
+// 8-byte reductions.
+int64_t ll32_group(int kind, int64_t es) { return kind == kRS && es == 8 ? 768 : 896; }
+
+Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int channels, int64_t es) {
   Slicing s{};
   s.proto = proto;
-  int64_t cap = proto == kProtoLL ? static_cast<int64_t>(comm->ll_slot_bytes / 2) : static_cast<int64_t>(comm->slot_bytes);
+  int64_t cap = static_cast<int64_t>(comm->slot_bytes);
+  int64_t minslice = 16 << 10;
+  if (proto == kProtoLL) {
+    cap = static_cast<int64_t>(comm->ll_slot_bytes / 2);
+    minslice = 512;
+  } else if (proto == kProtoLL32) {
+    cap = static_cast<int64_t>(comm->ll_slot_bytes / 1024) * ll32_group(kind, es);
+    minslice = ll32_group(kind, es);
+  }
   if (proto == kProtoPull && kind == kAG) cap = std::max<int64_t>(cap, comm->pull_slice);  // AG pull stages nothing
-  const int64_t minslice = proto == kProtoLL ? 512 : 16 << 10;
   int64_t per = (chunk_bytes + channels - 1) / channels;
   per = (per + 15) & ~int64_t(15);
   per = std::max<int64_t>(per, std::min<int64_t>(minslice, cap));
@@ -404,7 +416,7 @@ Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int
 }
 
 Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int max_channels, bool pull_ok,
-                       int rounds) {
+                       int rounds, int64_t es) {
   const int channels = std::max(1, std::min(comm->channels, max_channels));
   int proto = comm->cfg.protocol;
   if (proto == patProtoAuto) {
@@ -413,18 +425,21 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
     // pushed stores win (profiles/r01_sp_simple_vs_pull.jsonl)
     const int bulk = pull_ok && kind == kRS && chunk_bytes < kPullMaxRS ? kProtoPull : kProtoSimple;
     if (comm->cfg.ll_threshold) {  // explicit threshold
-      proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold) ? kProtoLL : bulk;
-    } else {  // the cost model picks LL or the bulk protocol
-      const Slicing a = shape(comm, kProtoLL, kind, chunk_bytes, channels);
-      const Slicing b = shape(comm, bulk, kind, chunk_bytes, channels);
-      proto = predict_us(kProtoLL, comm->n, rounds, chunk_bytes, a.iters) <=
-                      predict_us(bulk, comm->n, rounds, chunk_bytes, b.iters)
-                  ? kProtoLL
-                  : bulk;
+      proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold) ? kProtoLL32 : bulk;
+    } else {  // the cost model picks the fastest of LL, LL32 and the bulk protocol
+      double best = 0;
+      for (const int cand : std::array<int, 3>{kProtoLL, kProtoLL32, bulk}) {
+        const double t = predict_us(cand, comm->n, rounds, chunk_bytes,
+                                    shape(comm, cand, kind, chunk_bytes, channels, es).iters);
+        if (cand == kProtoLL || t < best) {
+          best = t;
+          proto = cand;
+        }
+      }
     }
   }
   if (proto == kProtoPull && !pull_ok) proto = kProtoSimple;
-  return shape(comm, proto, kind, chunk_bytes, channels);
+  return shape(comm, proto, kind, chunk_bytes, channels, es);
 }
 
 // Channels per rank such that every device's launch stays co-resident (cooperative launch).
@@ -463,6 +478,9 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   if (c.trees != 0) {
     if (!is_pow2(c.trees) || c.trees > max_trees(nranks)) return patInvalidTreeCount;
   }
+  if (c.protocol != patProtoAuto && c.protocol != patProtoLL && c.protocol != patProtoLL32 &&
+      c.protocol != patProtoSimple && c.protocol != patProtoPull)
+    return patInvalidArgument;
   comm->cfg = c;
   comm->channels = c.max_channels;
   comm->slot_bytes = c.slice_bytes;
@@ -474,12 +492,13 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
   // Inbox regions: SIMPLE/PULL slots, then LL slots. LL polls its lines, so it gets its own
   // memory: a stale payload word left by a bulk protocol could otherwise pass for a flag.
-  comm->ll_slot_bytes = std::max<size_t>(256, std::min<size_t>(kLLSlotBytes, comm->slot_bytes) & ~size_t(127));
+  comm->ll_slot_bytes = std::max<size_t>(1024, std::min<size_t>(kLLSlotBytes, comm->slot_bytes) & ~size_t(1023));
   const size_t nslots = static_cast<size_t>(comm->channels) * c.depth * slots;
   auto align = [](size_t x) { return (x + 4095) & ~size_t(4095); };
   comm->region_off[kProtoSimple] = comm->region_off[kProtoPull] = 0;
   comm->region_off[kProtoLL] = align(nslots * comm->slot_bytes);
-  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL] + nslots * comm->ll_slot_bytes;
+  comm->region_off[kProtoLL32] = comm->region_off[kProtoLL] + align(nslots * comm->ll_slot_bytes);
+  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL32] + nslots * comm->ll_slot_bytes;
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&comm->err_host), sizeof(int),
                          cudaHostAllocMapped | cudaHostAllocPortable));
   *comm->err_host = 0;
@@ -559,16 +578,18 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
                  (comm->cfg.protocol == patProtoPull || (kind == kRS && chunk_bytes > kPullMinRS));
   for (size_t l = 0; l < comm->lranks.size() && pull_ok && !single_device; ++l)
     pull_ok = legacy_ipc_capable(sendbuffs[l]) && (kind == kRS || legacy_ipc_capable(recvbuffs[l]));
-  const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds);
+  const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es));
   int vec = 16;
-  bool aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
+  bool aligned4 = (chunk_bytes % 4) == 0, aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
   for (size_t l = 0; l < comm->lranks.size(); ++l) {
     if (!sendbuffs[l] || !recvbuffs[l]) return patInvalidArgument;
     const uintptr_t a = reinterpret_cast<uintptr_t>(sendbuffs[l]) | reinterpret_cast<uintptr_t>(recvbuffs[l]);
     aligned16 &= (a % 16) == 0;
     aligned8 &= (a % 8) == 0;
+    aligned4 &= (a % 4) == 0;
   }
   vec = aligned16 ? 16 : (aligned8 ? 8 : 0);
+  if (sl.proto == kProtoLL32 && vec == 0 && aligned4) vec = 4;  // LL32 moves 4-byte units
   if (sl.proto == kProtoSimple && vec == 8) vec = 0;  // SIMPLE vectors are 16 bytes
   const bool fused = single_device && comm->cfg.fused >= 0 && cp->fused_ok &&
                      static_cast<int>(comm->groups[0].lidx.size()) == n;
@@ -590,7 +611,8 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.iters = sl.iters;
     p.chunk_bytes = chunk_bytes;
     p.slice_bytes = sl.slice;
-    p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL ? comm->ll_slot_bytes : comm->slot_bytes);
+    p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL || sl.proto == kProtoLL32 ? comm->ll_slot_bytes
+                                                                                          : comm->slot_bytes);
     p.depth = comm->cfg.depth;
     {
       // skew distance L: the sender keeps (nrounds-1)*L+1 steps in flight -> needs that many buffers
@@ -894,7 +916,7 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   // as run_collective decides, assuming cudaMalloc'd (peer-reachable) buffers
   const bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple &&
                        (comm->cfg.protocol == patProtoPull || (static_cast<int>(kind) == kRS && cb > kPullMinRS));
-  const Slicing sl = choose_slicing(comm, kind, cb, cap, pull_ok, cp->proto.nrounds);
+  const Slicing sl = choose_slicing(comm, kind, cb, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es));
   std::memset(info, 0, sizeof(*info));
   info->protocol = sl.proto;
   info->trees = trees;

@@ -37,6 +37,11 @@ struct LPlan {
   char* recv[kLocalMaxRanks];        // by rank
 };
 
+// Programmatic dependent launch (launch_local): wait for the stream's previous kernel before
+// touching memory. The successor is released only at exit (no early launch_dependents): these
+// grids run in more than one wave, and an early-resident successor would take their registers.
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint4 ld_nc16(const void* p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -72,6 +77,7 @@ constexpr int kU = 4;
 
 // All-gather: unit u of origin o is read once and written to all n outputs.
 __global__ void __launch_bounds__(kLocalThreads, 2) local_ag_kernel(const __grid_constant__ LPlan p) {
+  pdl_enter();
   const int n = p.n;
   const int bpr = gridDim.x / n;
   const int o = blockIdx.x / bpr;
@@ -124,6 +130,7 @@ constexpr int kTmaMaxStages = 8;
 __global__ void __launch_bounds__(32) local_ag_tma_kernel(const __grid_constant__ LPlan p, int piece, int NS) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t bars[kTmaMaxStages];
+  pdl_enter();
   if (threadIdx.x != 0) return;
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
@@ -216,6 +223,7 @@ __device__ __forceinline__ void local_rs_body(const LPlan& p) {
 
 template <int DT, int OP>
 __global__ void __launch_bounds__(kLocalThreads, 2) local_rs_kernel(const __grid_constant__ LPlan p) {
+  pdl_enter();
   switch (p.n) {
     case 1: local_rs_body<DT, OP, 1>(p); break;
     case 2: local_rs_body<DT, OP, 2>(p); break;
@@ -250,6 +258,15 @@ const char* local_tree_string(int n) {
   }
 }
 
+// PAT_PDL=0 launches without programmatic stream serialization (A/B experiments).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PAT_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize, int64_t chunk_bytes,
                          const char* const* send_by_rank, char* const* recv_by_rank, int sm_count,
                          cudaStream_t stream) {
@@ -276,17 +293,26 @@ cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize,
     return v >= 1024 ? (v & ~15) : 0;
   }();
   constexpr int kTmaStages = 4;
+  cudaLaunchConfig_t cfg = {};
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see pdl_enter
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   if (kind == 0 && tma_piece && vec == 16) {
     const int smem = kTmaStages * tma_piece;
     if (smem > 48 * 1024)  // per device; only for tiles set above the default through the env
       cudaFuncSetAttribute(local_ag_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    local_ag_tma_kernel<<<2 * sm_count, 32, smem, stream>>>(p, tma_piece, kTmaStages);
-  } else if (kind == 0) {
-    local_ag_kernel<<<bpr * n, kLocalThreads, 0, stream>>>(p);
-  } else {
-    kLocalRs[dtype][op]<<<bpr * n, kLocalThreads, 0, stream>>>(p);
+    cfg.gridDim = dim3(2 * sm_count);
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = smem;
+    return cudaLaunchKernelEx(&cfg, local_ag_tma_kernel, p, tma_piece, kTmaStages);
   }
-  return cudaGetLastError();
+  cfg.gridDim = dim3(bpr * n);
+  cfg.blockDim = dim3(kLocalThreads);
+  if (kind == 0) return cudaLaunchKernelEx(&cfg, local_ag_kernel, p);
+  return cudaLaunchKernelEx(&cfg, kLocalRs[dtype][op], p);
 }
 
 }  // namespace pat

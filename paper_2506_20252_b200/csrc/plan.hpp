@@ -20,8 +20,10 @@ constexpr int kFlagWords = 32;  // per channel: data flag per round [0,8), done-
                                 // ready-from per rank [16,24) (direct mode entry handshake)
 
 // (4 is retired: LL128, 128-byte lines with one flag word, was measured to tear over NVLink —
-// a line's flag sector can land before its data sectors — and was removed.)
-enum Proto : int { kProtoLL = 1, kProtoSimple = 2, kProtoPull = 3 };
+// a line's flag sector can land before its data sectors — and was removed. LL32's lines are
+// written by ONE 32-byte store each, which lands whole: tools/atomicity_probe.cu.)
+enum Proto : int { kProtoLL = 1, kProtoSimple = 2, kProtoPull = 3, kProtoLL32 = 5 };
+constexpr int kNumProtoSlots = 6;
 
 // PULL reduce-scatter: what a rank does with the arrival it pulled into slot j.
 enum PullAct : int8_t {

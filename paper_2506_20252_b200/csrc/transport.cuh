@@ -8,7 +8,9 @@
 // (simulate.cpp:180-218 all-gather, :247-296 reduce-scatter) and its Mailbox rendezvous +
 // lockstep join (simulate.cpp:49-70, 131-149) with per-step release/acquire flags.
 //
-// Two protocols:
+// Protocols:
+//  * LL32 (small messages, default): like LL below with 32-byte lines and one flag word
+//    (87.5% wire efficiency); see step_ll32.
 //  * LL (small messages): 16-byte lines {data32, flag, data32, flag} stored with one
 //    st.volatile.v4 into the peer's inbox; the receiver polls the line itself, so data and
 //    signal travel together and no fence or separate flag is needed. 50% wire efficiency.
@@ -527,6 +529,218 @@ __device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
   }
 }
 
+// ------------------------------------------------------------------------- LL32 protocol
+// 32-byte lines {payload, flag} written with ONE st.volatile.v8 (STG.256) and polled with one
+// ld.volatile.v8: a single flag word per line. This relies on a 32-byte vector store landing
+// whole at the peer, which tools/atomicity_probe.cu measured on this fabric (0 torn lines of
+// 7.3e9 per GPU pair, 2 and 4 GPUs, every GPU sending and receiving; profiles/r01f_*). LL
+// assumes only 8-byte atomicity and spends half of every line on flags; LL32 carries 28
+// payload bytes per 32 (87.5%).
+//
+// Payload units: a line holds R units of U bytes (U = 4, R = 7; U = 8 for 8-byte reductions so
+// every unit is a whole element, R = 3). Lines go in groups of 32 (one per lane): unit r of
+// lane l's line is slice bytes [U (32 r + l), +U) of the group, so every row r of a warp's
+// loads and stores is one contiguous 32 U-byte access. Lines whose first unit lies past the
+// slice end are empty; sender and receiver skip the same ones.
+struct Line32 {
+  uint32_t w[8];  // w[7] = flag
+};
+
+__device__ __forceinline__ void st_line32(void* p, const Line32& v) {
+  asm volatile("st.volatile.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
+               "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+               : "memory");
+}
+__device__ __forceinline__ Line32 ld_volatile32(const void* p) {
+  Line32 v;
+  asm volatile("ld.volatile.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
+                 "=r"(v.w[7])
+               : "l"(p)
+               : "memory");
+  return v;
+}
+// Poll one line until its flag word carries `flag`.
+__device__ __forceinline__ Line32 ld_line32(const char* line, uint32_t flag, Waiter& w) {
+  Line32 v = ld_volatile32(line);
+  if (v.w[7] == flag) return v;
+  uint64_t start = 0;
+  uint32_t spins = 0;
+  while (!w.aborted) {
+    v = ld_volatile32(line);
+    if (v.w[7] == flag) break;
+    if ((++spins & 1023u) == 0) {
+      const uint64_t now = globaltimer();
+      if (start == 0) start = now;
+      else if (now - start > w.timeout_ns) report_timeout(w);
+    }
+  }
+  return v;
+}
+
+template <int U>
+struct LL32Shape {
+  static constexpr int R = U == 4 ? 7 : 3;  // units per line
+  static constexpr int G = 32 * R * U;      // payload bytes per group of 32 lines
+};
+
+// Units of line (group base `gb`, lane) from a user buffer `p` (slice start). With an aligned
+// buffer every unit that starts before `len` is one aligned U-byte load (each row a contiguous
+// warp access); the chunk's last unit may extend past `len`, but an aligned unit never crosses a
+// page, and those bytes are never stored (store_units) — a fold of them is discarded. Unaligned
+// buffers go byte by byte.
+template <int U>
+__device__ __forceinline__ Line32 load_units(const char* p, int64_t gb, int lane, int64_t len, const KPlan& pl) {
+  constexpr int R = LL32Shape<U>::R;
+  Line32 v;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v.w[k] = 0;
+  if (pl.vec >= U) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t off = gb + static_cast<int64_t>(U) * (32 * r + lane);
+      if (off < len) {
+        if constexpr (U == 4) {
+          v.w[r] = *reinterpret_cast<const uint32_t*>(p + off);
+        } else {
+          const uint2 x = *reinterpret_cast<const uint2*>(p + off);
+          v.w[2 * r] = x.x;
+          v.w[2 * r + 1] = x.y;
+        }
+      }
+    }
+    return v;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t off = gb + static_cast<int64_t>(U) * (32 * r + lane);
+    if (off < len) {
+      const int valid = static_cast<int>(min(static_cast<int64_t>(U), len - off));
+      uint64_t x = 0;
+#pragma unroll
+      for (int b = 0; b < U; ++b)
+        if (b < valid) x |= static_cast<uint64_t>(static_cast<uint8_t>(p[off + b])) << (8 * b);
+      if constexpr (U == 4) {
+        v.w[r] = static_cast<uint32_t>(x);
+      } else {
+        v.w[2 * r] = static_cast<uint32_t>(x);
+        v.w[2 * r + 1] = static_cast<uint32_t>(x >> 32);
+      }
+    }
+  }
+  return v;
+}
+
+// Units of a line into a user buffer: whole aligned units as one store, the chunk's last
+// partial unit (or an unaligned buffer) byte by byte, never past `len`.
+template <int U>
+__device__ __forceinline__ void store_units(char* p, const Line32& v, int64_t gb, int lane, int64_t len,
+                                            const KPlan& pl) {
+  constexpr int R = LL32Shape<U>::R;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t off = gb + static_cast<int64_t>(U) * (32 * r + lane);
+    if (off + U <= len && pl.vec >= U) {
+      if constexpr (U == 4) *reinterpret_cast<uint32_t*>(p + off) = v.w[r];
+      else *reinterpret_cast<uint2*>(p + off) = make_uint2(v.w[2 * r], v.w[2 * r + 1]);
+    } else if (off < len) {
+      const int valid = static_cast<int>(min(static_cast<int64_t>(U), len - off));
+      const uint64_t x = U == 4 ? v.w[r] : (static_cast<uint64_t>(v.w[2 * r + 1]) << 32 | v.w[2 * r]);
+#pragma unroll
+      for (int b = 0; b < U; ++b)
+        if (b < valid) p[off + b] = static_cast<char>((x >> (8 * b)) & 0xff);
+    }
+  }
+}
+
+// a = a (op) b, unit by unit (every unit holds whole elements).
+template <int DT, int OP, int U>
+__device__ __forceinline__ void fold_line32(Line32& a, const Line32& b) {
+  if constexpr (U == 4) {
+#pragma unroll
+    for (int r = 0; r < 7; ++r) fold_vec<DT, OP>(a.w[r], b.w[r]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      uint2 x = make_uint2(a.w[2 * r], a.w[2 * r + 1]);
+      fold_vec<DT, OP>(x, make_uint2(b.w[2 * r], b.w[2 * r + 1]));
+      a.w[2 * r] = x.x;
+      a.w[2 * r + 1] = x.y;
+    }
+  }
+}
+
+// One LL32 pipeline step: the same rounds, slots and fold order as step_ll.
+template <int DT, int OP, int KIND, int U>
+__device__ void step_ll32(const KPlan& p, const Step& s, Waiter& w) {
+  constexpr int G = LL32Shape<U>::G;
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const char* snd = p.send[s.lr] + s.off;
+  char* out = p.recv[s.lr];
+  const uint32_t flag = static_cast<uint32_t>(s.g + 1);
+  const int64_t nlines = (s.len + G - 1) / G * 32;
+  const int B = blockDim.x;
+  const int lane = threadIdx.x & 31;
+
+  // rounds outer, lines inner (as step_ll): a round's stores are all in flight before the
+  // next round polls its first arrival
+#define PAT_LL32_LINES                                       \
+  for (int64_t q = threadIdx.x; q < nlines; q += B)          \
+    if (const int64_t gb = (q >> 5) * G; gb + U * lane < s.len)
+  if constexpr (KIND == kAG) {
+    if (out + s.R * Cb != p.send[s.lr])  // own chunk placement (simulate.cpp:160-165)
+      PAT_LL32_LINES store_units<U>(out + s.R * Cb + s.off, load_units<U>(snd, gb, lane, s.len, p), gb, lane, s.len, p);
+  }
+  for (int t = 0; t < p.nrounds; ++t) {
+    const KRound& r = p.rounds[t];
+    const int P = (s.R + r.peer) % n;
+    for (int pos = 0; pos < r.nchunks; ++pos) {
+      char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
+      if constexpr (KIND == kAG) {
+        const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
+        PAT_LL32_LINES {
+          Line32 v = fwd ? ld_line32(fwd + 32 * q, flag, w) : load_units<U>(snd, gb, lane, s.len, p);
+          v.w[7] = flag;
+          st_line32(dst + 32 * q, v);
+        }
+      } else {
+        const char* own = snd + ((s.R - r.chunk[pos] + n) % n) * Cb;
+        const int na = r.narr[pos];
+        PAT_LL32_LINES {
+          const Line32 mine = load_units<U>(own, gb, lane, s.len, p);
+          Line32 v;
+          if (na == 0) {
+            v = mine;
+          } else {  // fold(arrivals in round order) (+) own (simulate.cpp:257-266, 281-285)
+            v = ld_line32(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) + 32 * q, flag, w);
+            for (int a = 1; a < na; ++a)
+              fold_line32<DT, OP, U>(v, ld_line32(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][a]) + 32 * q, flag, w));
+            fold_line32<DT, OP, U>(v, mine);
+          }
+          v.w[7] = flag;
+          st_line32(dst + 32 * q, v);
+        }
+      }
+    }
+  }
+  if constexpr (KIND == kAG) {
+    for (int j = 0; j < p.nslots; ++j) {
+      const char* slot = slot_ptr(p, s.R, s.c, s.buf, j);
+      char* o = out + ((s.R - p.slot_offset[j] + n) % n) * Cb + s.off;
+      PAT_LL32_LINES store_units<U>(o, ld_line32(slot + 32 * q, flag, w), gb, lane, s.len, p);
+    }
+  } else {  // output = own (+) offset-0 arrivals in round order (simulate.cpp:239, 278-279)
+    PAT_LL32_LINES {
+      Line32 acc = load_units<U>(snd + s.R * Cb, gb, lane, s.len, p);
+      for (int f = 0; f < p.nfin; ++f)
+        fold_line32<DT, OP, U>(acc, ld_line32(slot_ptr(p, s.R, s.c, s.buf, p.fin[f]) + 32 * q, flag, w));
+      store_units<U>(out + s.off, acc, gb, lane, s.len, p);
+    }
+  }
+#undef PAT_LL32_LINES
+}
+
 // ------------------------------------------------------------------------- PULL protocol
 // The receiver reads. In round t rank R pulls the chunks K_t from its upstream Q = R - peer_t
 // (the rank that pushes to it in the reference's send/deliver, simulate.cpp:186-212, 252-290):
@@ -649,6 +863,11 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
   const int R = p.rank[lr];
   __shared__ uint64_t s_base;
   __shared__ volatile uint64_t s_sent;
+  // programmatic dependent launch (kernels.cu): this grid may be scheduled while its
+  // predecessor on the stream drains; it touches memory only once that grid completed and
+  // flushed. No early launch_dependents: a successor made resident early would take registers
+  // from this grid's later CTAs (measured: the fused reduce-scatter lost half its occupancy).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) {
     s_base = p.iter_state[lr][c];
     s_sent = 0;
@@ -669,16 +888,29 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
 
   if (p.proto == kProtoPull) {
     pull_role<DT, OP, KIND>(p, base, R, lr, c, w);
-  } else if (p.proto == kProtoLL) {
+  } else if (p.proto == kProtoLL || p.proto == kProtoLL32) {
+    // done(step) for the previous call's last step, deferred from its exit (below): every step
+    // before `base` finished, since that kernel completed before this one started
+    if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
+      st_relaxed(chan_flags(p, threadIdx.x, c) + 8 + R, base, w.gpu);
     for (int i = 0; i < p.iters; ++i) {
       const Step s = make_step(p, base, i, R, lr, c);
       if (threadIdx.x == 0) wait_credits(p, s, w);
       __syncthreads();
-      step_ll<DT, OP, KIND>(p, s, w);
+      if (p.proto == kProtoLL) {
+        step_ll<DT, OP, KIND>(p, s, w);
+      } else {
+        // 8-byte reductions use 8-byte units (whole elements); everything else 4-byte units
+        constexpr bool wide = KIND == kRS && sizeof(typename DType<DT>::S) == 8;
+        step_ll32<DT, OP, KIND, wide ? 8 : 4>(p, s, w);
+      }
       __syncthreads();
       // done(step): every load of this step's inbox has returned (its value was consumed before
-      // the barrier), so a relaxed store suffices to hand the buffers back
-      if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
+      // the barrier), so a relaxed store suffices to hand the buffers back. The last step's is
+      // published by the next call's kernel (above): a remote store at exit would hold the
+      // grid's completion for its NVLink acknowledgement, and no sender needs it earlier — the
+      // first step of the next call waits for step base - depth + 1 <= base - 1 (depth >= 2).
+      if (i + 1 < p.iters && threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
         st_relaxed(chan_flags(p, threadIdx.x, c) + 8 + R, s.g + 1, w.gpu);
     }
   } else {

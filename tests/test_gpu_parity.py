@@ -217,7 +217,7 @@ def test_reduce_scatter_ops(op, dt, executor):
             assert same(got[r], want[r]), (op, dt, n, r)
 
 
-@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL32, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
 def test_protocols_forced(proto):
     for n in (2, 5, 8):
         comm = comm_for(n, protocol=proto, fused=-1)
@@ -230,6 +230,37 @@ def test_protocols_forced(proto):
             got = gpu_reduce_scatter(comm, [0] * n, q, elems, O.BFLOAT16, O.SUM)
             want = oracle_rs(n, O.max_trees(n), O.BFLOAT16, O.SUM, q, elems)
             assert all(same(got[r], want[r]) for r in range(n)), (proto, n, elems)
+
+
+@pytest.mark.parametrize("spread", [False, True])
+def test_ll32_units_tails_and_alignment(spread):
+    """LL32 packs 4-byte units (8-byte units for 8-byte reductions) into 32-byte lines in groups
+    of 32; slice tails, element sizes 1..8, 2-, 4- and 8-byte misaligned buffers, in-place
+    all-gather and every op stay bit-exact."""
+    n = 5
+    devices = [r % max(NGPU, 1) for r in range(n)] if spread else [0] * n
+    if spread and NGPU < 2:
+        pytest.skip("needs >= 2 GPUs")
+    comm = comm_for(n, devices, protocol=_lib.PROTO_LL32, fused=-1, channels=3, staging_bytes=n * 96 * 1024)
+    for dt in (O.INT8, O.FLOAT16, O.BFLOAT16, O.INT32, O.FLOAT32, O.INT64, O.FLOAT64):
+        es = _lib.DTYPE_SIZE[dt]
+        for elems in (1, 7, 29, 225, 1031, 28673, 100003):
+            for pad in (0, 2, 4, 8):
+                if pad % es and pad < es:
+                    pad = es
+                p = O.random_payload(dt, n, elems, elems + pad)
+                got = gpu_allgather(comm, devices, p, elems, dt, pad=pad)
+                want = oracle_ag(n, O.max_trees(n), dt, p, elems)
+                assert all(same(got[r], want[r]) for r in range(n)), ("ag", dt, elems, pad)
+                op = [O.SUM, O.MAX, O.PROD, O.MIN][(elems + pad) % 4]
+                q = O.random_payload(dt, n * n, elems, elems + pad + 7)
+                got = gpu_reduce_scatter(comm, devices, q, elems, dt, op, pad=pad)
+                want = oracle_rs(n, O.max_trees(n), dt, op, q, elems)
+                assert all(same(got[r], want[r]) for r in range(n)), ("rs", dt, op, elems, pad)
+        p = O.random_payload(dt, n, 4099, 77)
+        got = gpu_allgather(comm, devices, p, 4099, dt, inplace=True)
+        assert all(same(got[r], oracle_ag(n, O.max_trees(n), dt, p, 4099)[r]) for r in range(n)), ("inplace", dt)
+    assert comm.plan(0, 1000, O.FLOAT32)["protocol"] == _lib.PROTO_LL32
 
 
 @pytest.mark.parametrize("executor", EXECUTORS)
@@ -390,7 +421,7 @@ def test_no_async_error_left():
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL32, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
 @pytest.mark.parametrize("n", [2, 3, 4, 6, 8])
 def test_multi_gpu_bulk_protocols(n, proto):
     """SIMPLE (pushed slices through the inboxes) and PULL (receivers read the peers' buffers)
@@ -446,18 +477,18 @@ def test_protocol_switches_share_no_inbox_state(spread):
         want = oracle_rs(n, O.max_trees(n), O.INT32, O.SUM, q, elems)
         assert all(same(got[r], want[r]) for r in range(n)), (it, elems, mismatch(got, want, elems))
     plans = [comm.plan(k, e, O.INT32)["protocol"] for k in (0, 1) for e in (200, 5000, 300000)]
-    assert plans == [_lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_SIMPLE,
-                     _lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_PULL], plans
+    assert plans == [_lib.PROTO_LL32, _lib.PROTO_SIMPLE, _lib.PROTO_SIMPLE,
+                     _lib.PROTO_LL32, _lib.PROTO_SIMPLE, _lib.PROTO_PULL], plans
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_cost_model_protocol_choice():
-    """Without an explicit ll_threshold the calibrated alpha-beta model picks LL or the bulk
+    """Without an explicit ll_threshold the calibrated alpha-beta model picks LL32 or the bulk
     protocol (comm.cpp: predict_us); the crossovers it implies match the forced sweeps
-    (profiles/r01c_forced_n*_p*.jsonl): LL to 2 MiB at n=2, to 1 MiB at n=4."""
-    cases = [(2, 2 << 20, _lib.PROTO_LL), (2, 8 << 20, _lib.PROTO_SIMPLE)]
+    (profiles/r01*_forced_n*_p*.jsonl)."""
+    cases = [(2, 2 << 20, _lib.PROTO_LL32), (2, 16 << 20, _lib.PROTO_SIMPLE)]
     if NGPU >= 4:
-        cases += [(4, 1 << 20, _lib.PROTO_LL), (4, 4 << 20, _lib.PROTO_SIMPLE)]
+        cases += [(4, 1 << 20, _lib.PROTO_LL32), (4, 8 << 20, _lib.PROTO_SIMPLE)]
     for n, nbytes, want in cases:
         comm = comm_for(n, list(range(n)))
         plan = comm.plan(0, nbytes // 4, O.FLOAT32)
@@ -493,7 +524,7 @@ def test_randomized_configurations():
         n = int(rng.integers(2, 9))
         spread = NGPU >= 2 and rng.random() < 0.5
         devices = [r % NGPU for r in range(n)] if spread else [0] * n
-        proto = int(rng.choice([_lib.PROTO_AUTO, _lib.PROTO_LL, _lib.PROTO_SIMPLE, _lib.PROTO_PULL]))
+        proto = int(rng.choice([_lib.PROTO_AUTO, _lib.PROTO_LL, _lib.PROTO_LL32, _lib.PROTO_SIMPLE, _lib.PROTO_PULL]))
         trees = int(rng.choice(O.valid_tree_counts(n)))
         comm = comm_for(n, devices, protocol=proto, trees=trees, fused=-1 if rng.random() < 0.7 else 0,
                         channels=int(rng.choice([1, 3, 8, 32])), staging_bytes=n * int(rng.choice([64, 512])) * 1024)

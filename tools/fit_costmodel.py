@@ -7,7 +7,7 @@ remains, and the protocol decides the constants:
     t(n, C) = a_p + b_p * R(n, T) + w_p * (n - 1) * C / B_p
 
 R = PAT rounds (ceil(log2 n) at T = max_trees), C = chunk bytes, w_p = wire bytes per payload
-byte (LL 2, SIMPLE 1), B_p = sustained link GB/s, a_p launch + completion, b_p per-round
+byte (LL 2, LL32 32/28, SIMPLE 1), B_p = sustained link GB/s, a_p launch + completion, b_p per-round
 synchronisation. Fitted by least squares on single-step points of forced-protocol sweeps.
 Since (n-1)*C does not depend on T and b_p > 0, T = max_trees (fewest rounds) minimises t for
 every size: the model justifies the library's fixed T. The LL/SIMPLE crossover it predicts is
@@ -21,9 +21,9 @@ import math
 
 import numpy as np
 
-WIRE = {1: 2.0, 2: 1.0}  # protocol -> wire bytes per payload byte
-NAME = {1: "LL", 2: "SIMPLE"}
-LL_STEP_BYTES = 128 * 16 * 1024  # one LL step: 128 channels x 16 KiB payload (comm.cpp kLLSlotBytes)
+WIRE = {1: 2.0, 2: 1.0, 5: 32.0 / 28.0}  # protocol -> wire bytes per payload byte
+NAME = {1: "LL", 2: "SIMPLE", 5: "LL32"}
+STEP_BYTES = {"LL": 128 * 16 * 1024, "LL32": 128 * 28 * 1024}  # one polling step: 128 channels x slot payload
 
 
 def rounds(n):
@@ -36,7 +36,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--ll-threshold", type=int, default=2 << 20)
     args = ap.parse_args()
-    pts = {1: [], 2: []}
+    pts = {1: [], 2: [], 5: []}
     for f in args.files:
         for line in open(f):
             r = json.loads(line)
@@ -61,22 +61,25 @@ def main():
                         "rel_err_median": float(np.median(np.abs(pred - y) / y)),
                         "rel_err_max": float(np.max(np.abs(pred - y) / y))}
     out = {"model": "t = a + b*R + w*(n-1)*C/B", "fit": fit, "crossover_bytes": {}}
-    if "LL" in fit and "SIMPLE" in fit:
-        L, S = fit["LL"], fit["SIMPLE"]
+    for ll in ("LL", "LL32"):
+        if ll not in fit or "SIMPLE" not in fit:
+            continue
+        L, S = fit[ll], fit["SIMPLE"]
+        out["crossover_bytes"][ll] = {}
         for n in range(2, 9):
             R = rounds(n)
-            # LL beyond one step pays its fixed cost again per extra step: walk sizes on a grid
+            # a polling protocol beyond one step pays its fixed cost again per extra step
             best = None
             for k in range(10, 28):
                 C = 1 << k
-                steps = max(1, -(-C // LL_STEP_BYTES))
+                steps = max(1, -(-C // STEP_BYTES[ll]))
                 tl = steps * (L["a_us"] + L["b_us_per_round"] * R) + L["wire"] * (n - 1) * C / (L["link_gbs"] * 1e3)
                 ts = S["a_us"] + S["b_us_per_round"] * R + S["wire"] * (n - 1) * C / (S["link_gbs"] * 1e3)
                 if tl > ts:
                     best = C
                     break
-            out["crossover_bytes"][n] = best
-        out["library_ll_threshold"] = args.ll_threshold
+            out["crossover_bytes"][ll][n] = best
+    out["library_ll_threshold"] = args.ll_threshold
     print(json.dumps(out, indent=1))
     if args.out:
         with open(args.out, "w") as f:
