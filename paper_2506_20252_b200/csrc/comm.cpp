@@ -47,7 +47,16 @@ constexpr int kDefaultChannels = 128;            // clamped to co-residency at l
 // LL32 vs bulk is chosen by the calibrated cost model below (choose_slicing).
 constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
 constexpr int64_t kPullMinRS = 1 << 20;    // ... and above this one (LL wins below anyway)
-constexpr size_t kLLSlotBytes = 32 << 10;  // LL / LL32 slot: 16 / 28 KiB payload per channel-step
+constexpr size_t kLLSlotBytes = 32 << 10;  // LL slot: 16 KiB payload per channel-step
+// LL32 slot (28/32 of it payload per channel-step); PAT_LL32_SLOT overrides (experiments)
+size_t ll32_slot_default() {
+  static const size_t v = [] {
+    const char* e = std::getenv("PAT_LL32_SLOT");
+    const long long x = e ? std::atoll(e) : 0;
+    return x >= 1024 ? static_cast<size_t>(x) & ~size_t(1023) : size_t(32) << 10;
+  }();
+  return v;
+}
 constexpr int kDefaultTimeoutMs = 20000;
 
 struct Compiled {
@@ -96,7 +105,8 @@ struct patComm {
   std::vector<DevGroup> groups;
   std::vector<void*> ipc_opened;
   size_t slot_bytes = 0, pool_bytes = 0;
-  size_t ll_slot_bytes = 0;                // LL and LL32 inbox slot (own regions, common_init)
+  size_t ll_slot_bytes = 0;                // LL inbox slot (own region, common_init)
+  size_t ll32_slot_bytes = 0;              // LL32 inbox slot (own region)
   size_t region_off[kNumProtoSlots] = {};  // inbox region of each protocol within a pool
   int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
   int skew = 1;            // SIMPLE / PULL sender skew distance (PAT_SKEW; 0 = rounds in order)
@@ -180,9 +190,10 @@ void fill_defaults(patConfig_t* c, int n) {
   c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(15));
   if (c->staging_bytes != 0) {
     // explicit budget for the whole pool (flags aside): channels * depth * (n-1) slot triples,
-    // one SIMPLE/PULL slot plus the LL and LL32 slots (<= 32 KiB each)
+    // one SIMPLE/PULL slot plus the LL and LL32 slots (each capped by the SIMPLE slot)
     const size_t b = c->staging_bytes > 8192 ? (c->staging_bytes - 8192) / slots : 0;
-    size_t s = b >= 3 * kLLSlotBytes ? b - 2 * kLLSlotBytes : b / 3;
+    const size_t ll = kLLSlotBytes + ll32_slot_default();
+    size_t s = b >= ll + std::max(kLLSlotBytes, ll32_slot_default()) ? b - ll : b / 3;
     s &= ~size_t(127);
     if (s < 256) s = 256;
     c->slice_bytes = s;
@@ -400,7 +411,7 @@ Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int
     cap = static_cast<int64_t>(comm->ll_slot_bytes / 2);
     minslice = 512;
   } else if (proto == kProtoLL32) {
-    cap = static_cast<int64_t>(comm->ll_slot_bytes / 1024) * ll32_group(kind, es);
+    cap = static_cast<int64_t>(comm->ll32_slot_bytes / 1024) * ll32_group(kind, es);
     minslice = ll32_group(kind, es);
   }
   if (proto == kProtoPull && kind == kAG) cap = std::max<int64_t>(cap, comm->pull_slice);  // AG pull stages nothing
@@ -493,12 +504,14 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   // Inbox regions: SIMPLE/PULL slots, then LL slots. LL polls its lines, so it gets its own
   // memory: a stale payload word left by a bulk protocol could otherwise pass for a flag.
   comm->ll_slot_bytes = std::max<size_t>(1024, std::min<size_t>(kLLSlotBytes, comm->slot_bytes) & ~size_t(1023));
+  comm->ll32_slot_bytes =
+      std::max<size_t>(1024, std::min<size_t>(ll32_slot_default(), comm->slot_bytes) & ~size_t(1023));
   const size_t nslots = static_cast<size_t>(comm->channels) * c.depth * slots;
   auto align = [](size_t x) { return (x + 4095) & ~size_t(4095); };
   comm->region_off[kProtoSimple] = comm->region_off[kProtoPull] = 0;
   comm->region_off[kProtoLL] = align(nslots * comm->slot_bytes);
   comm->region_off[kProtoLL32] = comm->region_off[kProtoLL] + align(nslots * comm->ll_slot_bytes);
-  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL32] + nslots * comm->ll_slot_bytes;
+  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL32] + nslots * comm->ll32_slot_bytes;
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&comm->err_host), sizeof(int),
                          cudaHostAllocMapped | cudaHostAllocPortable));
   *comm->err_host = 0;
@@ -611,8 +624,9 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.iters = sl.iters;
     p.chunk_bytes = chunk_bytes;
     p.slice_bytes = sl.slice;
-    p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL || sl.proto == kProtoLL32 ? comm->ll_slot_bytes
-                                                                                          : comm->slot_bytes);
+    p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL     ? comm->ll_slot_bytes
+                                         : sl.proto == kProtoLL32 ? comm->ll32_slot_bytes
+                                                                  : comm->slot_bytes);
     p.depth = comm->cfg.depth;
     {
       // skew distance L: the sender keeps (nrounds-1)*L+1 steps in flight -> needs that many buffers

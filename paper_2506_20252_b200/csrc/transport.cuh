@@ -236,8 +236,8 @@ __device__ __forceinline__ void grp_fold(char* dst, const char* const* src, int 
 
 // 8-byte user words for LL (zero padded past `valid`).
 __device__ __forceinline__ uint2 load_word(const char* p, int valid, const KPlan& pl) {
-  if (valid == 8 && pl.vec >= 8) {
-    const uint64_t v = ld_cg_bytes<8>(p);
+  if (valid == 8 && pl.vec >= 8) {  // user buffer, read-only during the call
+    const uint64_t v = *reinterpret_cast<const uint64_t*>(p);
     return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
   }
   uint64_t v = 0;

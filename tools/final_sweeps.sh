@@ -13,7 +13,7 @@ done
 # bandwidth sweeps, loop mode (L2 flushed per call), multi-process vs NCCL Ring
 for N in 2 3 4; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2971$N \
-    bench_sweep.py --mode loop --min-bytes 8388608 --max-bytes 1073741824 --iters 10 --warmup 3 --dtypes f32,bf16 \
+    bench_sweep.py --mode loop --min-bytes 8388608 --max-bytes 1073741824 --iters 10 --warmup 3 --dtypes ${LOOP_DTYPES:-f32,bf16} \
     --out $O/sweep_n${N}_loop.jsonl > $O/sweep_n${N}_loop.log 2>&1
   echo loop $N rc=$?
 done
