@@ -420,18 +420,20 @@ def run_pat(args, rank, world, local):
         except Exception:
             pass
 
-    # small messages are latency-bound: compare with the PAT step floor, the zero-byte LL time of
-    # R = ceil(log2 n) rounds (cost-model fit, profiles/r01c_costmodel_fit.json) plus the LL wire
-    # bytes (2 x payload) at the measured two-way SM-push ceiling (profiles/r01_bidir_probe_g4.txt)
+    # small messages are latency-bound: compare with the PAT step floor — the zero-byte time of
+    # R = ceil(log2 n) polling rounds (LL, the lowest fixed cost of the cost-model fit,
+    # profiles/r01f_costmodel_fit.json) plus the payload on the wire with LL32's one flag word
+    # per 28 bytes, at the measured two-way SM-push ceiling (profiles/r01_bidir_probe_g4.txt)
     lat_floor = None
     if world > 1:
-        R = comm.plan(0, elems, FLOAT32)["rounds"]
-        zero_us = 3.59 + 1.28 * R
-        wire_us = 2.0 * (n - 1) * C / (704.0 * 1e3)
-        lat_floor = {"rounds": R, "zero_byte_us": zero_us, "wire_us_at_704gbs": wire_us,
-                     "floor_us": zero_us + wire_us, "achieved_us": 1e3 * ag_ms / K,
+        plan = comm.plan(0, elems, FLOAT32)
+        R = plan["rounds"]
+        zero_us = 3.41 + 1.40 * R
+        wire_us = (32.0 / 28.0) * (n - 1) * C / (704.0 * 1e3)
+        lat_floor = {"rounds": R, "protocol": plan["protocol"], "zero_byte_us": zero_us,
+                     "wire_us_at_704gbs": wire_us, "floor_us": zero_us + wire_us, "achieved_us": 1e3 * ag_ms / K,
                      "frac": (zero_us + wire_us) / (1e3 * ag_ms / K),
-                     "source": "profiles/r01c_costmodel_fit.json (LL a, b), profiles/r01_bidir_probe_g4.txt"}
+                     "source": "profiles/r01f_costmodel_fit.json (LL a, b), profiles/r01_bidir_probe_g4.txt"}
 
     clk = clocks.summary()
     if world > 1:

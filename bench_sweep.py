@@ -4,9 +4,10 @@ Run under torchrun, one process per GPU (N >= 2), or plain (N = 1: logical ranks
 
   torchrun --nproc-per-node 4 --master-addr 127.0.0.1 bench_sweep.py --out gpurun_out/sweep4.json
 
-Every point: W warm-up calls, then K calls timed with CUDA events per call (median), the max
-over ranks. Latency points (<= 1 MiB) are back-to-back calls without an L2 flush (the
-nccl-tests convention); bandwidth points (>= 1 MiB) flush L2 before every call.
+Every point: W warm-up calls, then K calls timed with CUDA events (graph mode: the median over
+--trials replays of a graph of K calls, each trial the max over ranks; loop mode: one pass, the
+max over ranks). Calls run back to back without an L2 flush (the nccl-tests convention); events
+mode flushes L2 before every call from 1 MiB up.
 Writes one JSON object per line: {"coll", "impl", "n", "dtype", "bytes_per_rank", "us", "busbw_gbs"}.
 """
 from __future__ import annotations
@@ -32,6 +33,7 @@ def main():
     ap.add_argument("--ranks", type=int, default=8, help="logical ranks when run without torchrun")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--protocol", type=int, default=0)
+    ap.add_argument("--trials", type=int, default=5, help="graph mode: timed replays per point (median)")
     ap.add_argument("--mode", default="loop", choices=["loop", "events", "graph"],
                     help="loop: K back-to-back calls between two events (nccl-tests style); events: one "
                          "event pair per call (median); graph: K calls captured in a CUDA graph")
@@ -94,11 +96,22 @@ def main():
                 stream.wait_stream(s2)
                 g.replay()
                 torch.cuda.synchronize(dev)
+                # several trials, each (barrier, one replay of K calls); per trial the max over ranks,
+                # then the median over trials: one rank entering a replay late (host jitter after
+                # the barrier) inflates one trial, not the point
+                trials = []
+                for _ in range(args.trials):
+                    if world > 1:
+                        dist.barrier()
+                    a.record(stream)
+                    g.replay()
+                    b.record(stream)
+                    torch.cuda.synchronize(dev)
+                    trials.append(a.elapsed_time(b) * 1e3 / args.iters)
+                t = torch.tensor(trials, dtype=torch.float64, device=dev)
                 if world > 1:
-                    dist.barrier()
-                a.record(stream)
-                g.replay()
-                b.record(stream)
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                return float(t.median().item())
             else:
                 a.record(stream)
                 for _ in range(args.iters):
