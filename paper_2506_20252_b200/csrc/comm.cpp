@@ -388,13 +388,19 @@ struct CostRow {
   double a_us, b_us, gbs, wire;
 };
 constexpr CostRow kCostLL{3.41, 1.40, 565.0, 2.0};
-constexpr CostRow kCostLL32{3.92, 1.49, 604.0, 32.0 / 28.0};
+constexpr CostRow kCostLL32{3.26, 2.31, 605.0, 32.0 / 28.0};  // one fixed cost per call (below)
+// LL32 is eligible while a rank moves at most this much payload per call: measured against
+// SIMPLE, LL32 wins up to (n-1) C = 32 MiB at n = 2 and 4 and is 6% behind at n = 3, 16 MiB
+// (profiles/r01f_ll32_noskew_n*.jsonl vs r01f_forced_n*_p2.jsonl); the linear model alone would
+// keep it far beyond, where SIMPLE's pipelined pushes reach 670+ GB/s.
+constexpr int64_t kLL32MaxPayload = 32ll << 20;
 constexpr CostRow kCostBulk{5.99, 6.11, 560.0, 1.0};
 
 double predict_us(int proto, int n, int rounds, int64_t chunk_bytes, int iters) {
-  const bool ll = proto == kProtoLL || proto == kProtoLL32;
+  // LL pays its fixed cost per step; LL32's extra steps cost nothing measurable (fit over
+  // 1-10 steps, profiles/r01f_ll32_noskew_n*.jsonl), SIMPLE / PULL pipeline theirs
   const CostRow& c = proto == kProtoLL ? kCostLL : proto == kProtoLL32 ? kCostLL32 : kCostBulk;
-  const double fixed = (ll ? std::max(iters, 1) : 1) * (c.a_us + c.b_us * rounds);
+  const double fixed = (proto == kProtoLL ? std::max(iters, 1) : 1) * (c.a_us + c.b_us * rounds);
   return fixed + c.wire * (n - 1) * static_cast<double>(chunk_bytes) / (c.gbs * 1e3);
 }
 
@@ -423,6 +429,11 @@ Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int
   const int64_t nslices = std::max<int64_t>(1, (chunk_bytes + s.slice - 1) / s.slice);
   s.channels = static_cast<int>(std::min<int64_t>(channels, nslices));
   s.iters = static_cast<int>((nslices + s.channels - 1) / s.channels);
+  if (proto == kProtoLL32 && s.iters > 1) {
+    // equal steps: every channel runs `iters` steps of the same size (no short last wave)
+    const int64_t even = (chunk_bytes + int64_t{s.channels} * s.iters - 1) / (int64_t{s.channels} * s.iters);
+    s.slice = std::min(s.slice, (even + 15) & ~int64_t(15));
+  }
   return s;
 }
 
@@ -440,6 +451,7 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
     } else {  // the cost model picks the fastest of LL, LL32 and the bulk protocol
       double best = 0;
       for (const int cand : std::array<int, 3>{kProtoLL, kProtoLL32, bulk}) {
+        if (cand == kProtoLL32 && static_cast<int64_t>(comm->n - 1) * chunk_bytes > kLL32MaxPayload) continue;
         const double t = predict_us(cand, comm->n, rounds, chunk_bytes,
                                     shape(comm, cand, kind, chunk_bytes, channels, es).iters);
         if (cand == kProtoLL || t < best) {

@@ -670,9 +670,11 @@ __device__ __forceinline__ void fold_line32(Line32& a, const Line32& b) {
   }
 }
 
-// One LL32 pipeline step: the same rounds, slots and fold order as step_ll.
+// One phase of an LL32 pipeline step: phase t in [0, nrounds) sends round t; phase nrounds
+// finishes the step (all-gather: own chunk placement and delivery of every slot; reduce-scatter:
+// the output fold). The same rounds, slots and fold order as step_ll.
 template <int DT, int OP, int KIND, int U>
-__device__ void step_ll32(const KPlan& p, const Step& s, Waiter& w) {
+__device__ void ll32_phase(const KPlan& p, const Step& s, int t, Waiter& w) {
   constexpr int G = LL32Shape<U>::G;
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
@@ -683,16 +685,11 @@ __device__ void step_ll32(const KPlan& p, const Step& s, Waiter& w) {
   const int B = blockDim.x;
   const int lane = threadIdx.x & 31;
 
-  // rounds outer, lines inner (as step_ll): a round's stores are all in flight before the
-  // next round polls its first arrival
+  // lines inner: a round's stores are all in flight before the next round polls its first arrival
 #define PAT_LL32_LINES                                       \
   for (int64_t q = threadIdx.x; q < nlines; q += B)          \
     if (const int64_t gb = (q >> 5) * G; gb + U * lane < s.len)
-  if constexpr (KIND == kAG) {
-    if (out + s.R * Cb != p.send[s.lr])  // own chunk placement (simulate.cpp:160-165)
-      PAT_LL32_LINES store_units<U>(out + s.R * Cb + s.off, load_units<U>(snd, gb, lane, s.len, p), gb, lane, s.len, p);
-  }
-  for (int t = 0; t < p.nrounds; ++t) {
+  if (t < p.nrounds) {
     const KRound& r = p.rounds[t];
     const int P = (s.R + r.peer) % n;
     for (int pos = 0; pos < r.nchunks; ++pos) {
@@ -723,8 +720,9 @@ __device__ void step_ll32(const KPlan& p, const Step& s, Waiter& w) {
         }
       }
     }
-  }
-  if constexpr (KIND == kAG) {
+  } else if constexpr (KIND == kAG) {
+    if (out + s.R * Cb != p.send[s.lr])  // own chunk placement (simulate.cpp:160-165)
+      PAT_LL32_LINES store_units<U>(out + s.R * Cb + s.off, load_units<U>(snd, gb, lane, s.len, p), gb, lane, s.len, p);
     for (int j = 0; j < p.nslots; ++j) {
       const char* slot = slot_ptr(p, s.R, s.c, s.buf, j);
       char* o = out + ((s.R - p.slot_offset[j] + n) % n) * Cb + s.off;
@@ -893,6 +891,11 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
     // before `base` finished, since that kernel completed before this one started
     if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
       st_relaxed(chan_flags(p, threadIdx.x, c) + 8 + R, base, w.gpu);
+    // 8-byte reductions use 8-byte LL32 units (whole elements); everything else 4-byte units
+    constexpr int U = KIND == kRS && sizeof(typename DType<DT>::S) == 8 ? 8 : 4;
+    // Steps in order. (A wavefront — phase t of step k - t in iteration k, as send_role — was
+    // built and measured slower: LL32 is bound by the polled lines' bandwidth, not by flight
+    // times; profiles/r01f_ll32_{skew,noskew}_n*.jsonl.)
     for (int i = 0; i < p.iters; ++i) {
       const Step s = make_step(p, base, i, R, lr, c);
       if (threadIdx.x == 0) wait_credits(p, s, w);
@@ -900,9 +903,7 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
       if (p.proto == kProtoLL) {
         step_ll<DT, OP, KIND>(p, s, w);
       } else {
-        // 8-byte reductions use 8-byte units (whole elements); everything else 4-byte units
-        constexpr bool wide = KIND == kRS && sizeof(typename DType<DT>::S) == 8;
-        step_ll32<DT, OP, KIND, wide ? 8 : 4>(p, s, w);
+        for (int t = 0; t <= p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w);
       }
       __syncthreads();
       // done(step): every load of this step's inbox has returned (its value was consumed before

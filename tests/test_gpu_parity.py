@@ -486,9 +486,10 @@ def test_cost_model_protocol_choice():
     """Without an explicit ll_threshold the calibrated alpha-beta model picks LL32 or the bulk
     protocol (comm.cpp: predict_us); the crossovers it implies match the forced sweeps
     (profiles/r01*_forced_n*_p*.jsonl)."""
-    cases = [(2, 2 << 20, _lib.PROTO_LL32), (2, 16 << 20, _lib.PROTO_SIMPLE)]
+    cases = [(2, 64 << 10, _lib.PROTO_LL), (2, 2 << 20, _lib.PROTO_LL32), (2, 16 << 20, _lib.PROTO_LL32),
+             (2, 64 << 20, _lib.PROTO_SIMPLE)]
     if NGPU >= 4:
-        cases += [(4, 1 << 20, _lib.PROTO_LL32), (4, 8 << 20, _lib.PROTO_SIMPLE)]
+        cases += [(4, 1 << 20, _lib.PROTO_LL32), (4, 16 << 20, _lib.PROTO_SIMPLE)]
     for n, nbytes, want in cases:
         comm = comm_for(n, list(range(n)))
         plan = comm.plan(0, nbytes // 4, O.FLOAT32)
