@@ -353,6 +353,27 @@ def test_explicit_schedules_generic_executor(executor):
             assert all(same(got[r], want[r]) for r in range(n)), (n, rs.algorithm)
 
 
+@pytest.mark.parametrize("proto", [_lib.PROTO_LL, _lib.PROTO_LL32, _lib.PROTO_SIMPLE, _lib.PROTO_PULL])
+def test_explicit_schedules_every_protocol(proto):
+    """Ring (n-1 rounds, more rounds than pipeline buffers), Bruck and single-tree PAT schedules
+    on every transport protocol, across GPUs where there are several, with a small pool so every
+    call runs several pipeline steps per channel."""
+    for n in (3, 6):
+        devices = [r % NGPU for r in range(n)] if NGPU >= 2 else [0] * n
+        comm = comm_for(n, devices, protocol=proto, fused=-1, channels=2, staging_bytes=n * 128 * 1024)
+        elems = 70001
+        for ag in (S.ring_allgather(n), S.bruck_nearest(n), S.pat_allgather(n, 1)):
+            p = O.random_payload(O.INT32, n, elems, 31)
+            got = gpu_allgather(comm, devices, p, elems, O.INT32, schedule=ag)
+            want, _ = O.run_allgather(ag.encode(), O.INT32, p, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (proto, n, ag.algorithm)
+            rs = S.mirror_schedule(ag)
+            q = O.random_payload(O.BFLOAT16, n * n, elems, 32)
+            got = gpu_reduce_scatter(comm, devices, q, elems, O.BFLOAT16, O.SUM, schedule=rs)
+            want, _ = O.run_reduce_scatter(rs.encode(), O.BFLOAT16, O.SUM, q, elems)
+            assert all(same(got[r], want[r]) for r in range(n)), (proto, n, rs.algorithm)
+
+
 @pytest.mark.parametrize("executor", EXECUTORS)
 def test_large_property_checks(executor):
     """Full-size properties: AG output = concatenation; RS int32 = column

@@ -1,5 +1,5 @@
-"""Stress the polling protocol (LL) against the oracle on odd sizes and 2-byte elements; print
-where mismatches are (debug tool)."""
+"""Stress the polling protocols (LL, LL32) against the oracle on odd sizes and 2-byte elements;
+print where mismatches are (debug tool). ITERS (env) sets the repetitions per configuration."""
 import os
 import sys
 
@@ -14,11 +14,11 @@ from test_gpu_parity import gpu_allgather, gpu_reduce_scatter, oracle_ag, oracle
 
 ngpu = torch.cuda.device_count()
 for n, devices in ((8, [r % ngpu for r in range(8)]), (8, [0] * 8), (4, list(range(min(4, ngpu))) if ngpu >= 4 else [0] * 4)):
-    for proto in (_lib.PROTO_LL,):
+    for proto in (_lib.PROTO_LL, _lib.PROTO_LL32):
         comm = PatComm.init_all(n, devices, protocol=proto, staging_bytes=n * 256 * 1024, channels=8, fused=-1)
         bad = 0
-        for it in range(6):
-            for elems in (70001, 4099, 65536, 123457):
+        for it in range(int(os.environ.get("ITERS", "6"))):
+            for elems in (70001, 4099, 65536, 123457, 1000003):
                 for dt in (O.BFLOAT16, O.FLOAT32, O.INT32):
                     q = O.random_payload(dt, n * n, elems, elems + it)
                     got = gpu_reduce_scatter(comm, devices, q, elems, dt, O.SUM)
