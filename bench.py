@@ -417,6 +417,9 @@ def run_pat(args, rank, world, local):
             if key in tr:
                 roof["traffic"] = tr[key]["dram_bytes_per_launch"]
                 roof["traffic_source"] = tr[key].get("source")
+                if "nvlink_tx_bytes_per_launch" in tr[key]:  # NVLink egress of the same ncu launch
+                    roof["nvlink_tx_bytes"] = tr[key]["nvlink_tx_bytes_per_launch"]
+                    roof["nvlink_tx_user_bytes"] = tr[key]["nvlink_tx_user_bytes_per_launch"]
         except Exception:
             pass
 

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpatb200.so")
+# PAT_LIB_VARIANT=x loads libpatb200_x.so (an in-tree A/B build of the same sources, tools/)
+LIB_PATH = os.path.join(HERE, "libpatb200" + (f"_{os.environ['PAT_LIB_VARIANT']}" if os.environ.get("PAT_LIB_VARIANT") else "") + ".so")
 HANDLE_BYTES = 128
 MAX_RANKS = 8
 
