@@ -65,7 +65,7 @@ def load_peaks():
 
 # ------------------------------------------------------------------ reference CPU path
 
-def reference_time(n: int, chunk_bytes: int, seconds: float, mode: int = 1):
+def reference_time(n: int, chunk_bytes: int, seconds: float, mode: int = 1, max_steps: int = 10000):
     """The reference executor (oracle/_ref) on the host: run_allgather(int64) +
     run_reduce_scatter(float64, FloatSum) with equal bytes per chunk. Returns
     (seconds per step, steps, threads)."""
@@ -101,7 +101,7 @@ def reference_time(n: int, chunk_bytes: int, seconds: float, mode: int = 1):
         one()
         steps += 1
         el = time.perf_counter() - t0
-        if el >= seconds or steps >= 10000:
+        if el >= seconds or steps >= max_steps:
             break
     return el / steps, steps, threads if mode else 1
 
@@ -313,18 +313,42 @@ def run_pat(args, rank, world, local):
     for i in range(L):
         h_ag_send[i].copy_(ag_send[i].cpu())
         h_rs_send[i].copy_(rs_send[i].cpu())
+    # Double-buffered: step k's inputs go up on a copy stream into device set k % 2 while step
+    # k-1 runs, and step k-1's results come down on another copy stream (PCIe is full duplex, so
+    # the two directions overlap); every step still copies all of its inputs in and its results
+    # out inside the timed region.
     E = max(3, min(K, 20))
+    dsets = [sets[j % len(sets)] for j in range(2)]
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    h2d_done, comp_done, d2h_done = [ev() for _ in range(E)], [ev() for _ in range(E)], [ev() for _ in range(E)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record(stream)
-    for _ in range(E):
-        for i in range(L):
-            ag_send[i].copy_(h_ag_send[i], non_blocking=True)
-            rs_send[i].copy_(h_rs_send[i], non_blocking=True)
-        step()
-        for i in range(L):
-            h_ag_recv[i].copy_(ag_recv[i], non_blocking=True)
-            h_rs_recv[i].copy_(rs_recv[i], non_blocking=True)
+    s_in.wait_stream(stream)
+    s_out.wait_stream(stream)
+    for k in range(E):
+        bs = dsets[k % 2]
+        with torch.cuda.stream(s_in):
+            if k >= 2:
+                s_in.wait_event(comp_done[k - 2])  # set k % 2's inputs are free
+            for i in range(L):
+                bs["ag_send"][i].copy_(h_ag_send[i], non_blocking=True)
+                bs["rs_send"][i].copy_(h_rs_send[i], non_blocking=True)
+            h2d_done[k].record(s_in)
+        stream.wait_event(h2d_done[k])
+        if k >= 2:
+            stream.wait_event(d2h_done[k - 2])  # set k % 2's outputs were read back
+        step(bs)
+        comp_done[k].record(stream)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(comp_done[k])
+            for i in range(L):
+                h_ag_recv[i].copy_(bs["ag_recv"][i], non_blocking=True)
+                h_rs_recv[i].copy_(bs["rs_recv"][i], non_blocking=True)
+            d2h_done[k].record(s_out)
+    stream.wait_event(d2h_done[E - 1])
+    stream.wait_event(h2d_done[E - 1])
     e1.record(stream)
     barrier()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / E], dtype=torch.float64, device=dev)
@@ -476,7 +500,7 @@ def run_pat(args, rank, world, local):
             "latency_us_eager": dict(eager_us, timing="eager C-ABI calls, CUDA events per call"),
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host"},
+                    "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host; double-buffered: step k+1 uploads while step k downloads (PCIe full duplex)"},
             "gpu_launches": 2 * K,
             "roofline": roof,
             "latency_floor": lat_floor,
@@ -497,13 +521,16 @@ def run_reference(args, rank, world):
         return None
     n = world if world > 1 else (args.ranks or 8)
     C = args.chunk_bytes
-    per = []
-    for _ in range(args.warmup):
-        reference_time(n, C, 0.0)
-    budget = max(1.0, min(args.cpu_seconds, 60.0))
-    sec, steps, thr = reference_time(n, C, budget)
+    # W warm-up steps (at most 3: each is the whole workload, ~90 ms), then exactly K timed steps
+    # unless K steps would exceed ~2 minutes of host time: then as many as fit, reported in
+    # "steps" and in the sample description
+    for _ in range(min(args.warmup, 3)):
+        reference_time(n, C, 0.0, max_steps=1)
+    est, _, _ = reference_time(n, C, 0.0, max_steps=1)
+    timed = max(1, min(args.steps, int(120.0 / max(est, 1e-6))))
+    sec, steps, thr = reference_time(n, C, 1e9, max_steps=timed)
+    budget = sec * steps
     value = busbw_gbs(n, C, sec)
-    del per
     return {"impl": "reference", "metric": "PAT all-gather + reduce-scatter(sum) aggregate bus bandwidth, 1 MiB fp32 per rank",
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -511,7 +538,8 @@ def run_reference(args, rank, world):
             "config": {"workload": "BASELINE configs[0]: PAT AG + RS(sum), 1 MiB per rank", "nranks": n,
                        "chunk_bytes": C, "placement": "in-process ranks on host cores"},
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": thr, "kind": "reference",
-                             "sample": f"{steps} steps, ExecMode::Parallel x{thr} threads, ~{budget:.0f} s"},
+                             "sample": f"{steps} timed steps (of --steps {args.steps}) of the whole workload, "
+                                       f"ExecMode::Parallel x{thr} threads, {budget:.1f} s"},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
