@@ -10,7 +10,7 @@
 //
 // Protocols:
 //  * LL32 (small messages, default): like LL below with 32-byte lines and one flag word
-//    (87.5% wire efficiency); see step_ll32.
+//    (87.5% wire efficiency); see ll32_phase.
 //  * LL (small messages): 16-byte lines {data32, flag, data32, flag} stored with one
 //    st.volatile.v4 into the peer's inbox; the receiver polls the line itself, so data and
 //    signal travel together and no fence or separate flag is needed. 50% wire efficiency.
