@@ -390,10 +390,11 @@ struct CostRow {
 constexpr CostRow kCostLL{3.41, 1.40, 565.0, 2.0};
 constexpr CostRow kCostLL32{3.26, 2.31, 605.0, 32.0 / 28.0};  // one fixed cost per call (below)
 // LL32 is eligible while a rank moves at most this much payload per call: measured against
-// SIMPLE, LL32 wins up to (n-1) C = 32 MiB at n = 2 and 4 and is 6% behind at n = 3, 16 MiB
-// (profiles/r01f_ll32_noskew_n*.jsonl vs r01f_forced_n*_p2.jsonl); the linear model alone would
-// keep it far beyond, where SIMPLE's pipelined pushes reach 670+ GB/s.
-constexpr int64_t kLL32MaxPayload = 32ll << 20;
+// SIMPLE, LL32 wins up to (n-1) C = 48 MiB at n = 2 and 4 (n = 4, 16 MiB: 106 vs 110 us graph
+// mode; loop mode SIMPLE is 0.95x NCCL there) and is within 6% at n = 3, 16 MiB
+// (profiles/r01f_ll32_noskew_n*.jsonl, r01f_forced_n*_p2.jsonl, r01f_loopmid_n*.jsonl); the
+// linear model alone would keep it far beyond, where SIMPLE's pipelined pushes reach 670 GB/s.
+constexpr int64_t kLL32MaxPayload = 48ll << 20;
 constexpr CostRow kCostBulk{5.99, 6.11, 560.0, 1.0};
 
 double predict_us(int proto, int n, int rounds, int64_t chunk_bytes, int iters) {

@@ -510,7 +510,7 @@ def test_cost_model_protocol_choice():
     cases = [(2, 64 << 10, _lib.PROTO_LL), (2, 2 << 20, _lib.PROTO_LL32), (2, 16 << 20, _lib.PROTO_LL32),
              (2, 64 << 20, _lib.PROTO_SIMPLE)]
     if NGPU >= 4:
-        cases += [(4, 1 << 20, _lib.PROTO_LL32), (4, 16 << 20, _lib.PROTO_SIMPLE)]
+        cases += [(4, 1 << 20, _lib.PROTO_LL32), (4, 16 << 20, _lib.PROTO_LL32), (4, 32 << 20, _lib.PROTO_SIMPLE)]
     for n, nbytes, want in cases:
         comm = comm_for(n, list(range(n)))
         plan = comm.plan(0, nbytes // 4, O.FLOAT32)
