@@ -171,6 +171,17 @@ size_t dtype_size(int dt) {
   }
 }
 
+// Bytes of an explicit staging budget (patConfig_t::staging_bytes) per slot triple (one
+// SIMPLE/PULL slot + one LL slot + one LL32 slot for each of channels * depth * (n-1) slots).
+size_t budget_per_slot(const patConfig_t& c, int n) {
+  const size_t slots = static_cast<size_t>(c.max_channels) * c.depth * std::max(n - 1, 1);
+  return c.staging_bytes > 8192 ? (c.staging_bytes - 8192) / slots : 0;
+}
+// A polling protocol's slot under a budget of b bytes per triple: at most a sixth of it, so a
+// tight budget goes to the bulk slices that carry the large calls (ZeRO-3 shape at a 64 MiB
+// cap: 19 -> 38 KiB slices).
+size_t polling_slot(size_t def, size_t b) { return std::max<size_t>(1024, std::min(def, b / 6) & ~size_t(1023)); }
+
 void fill_defaults(patConfig_t* c, int n) {
   long long v;
   if (c->max_channels <= 0) c->max_channels = env_int("PAT_CHANNELS", &v) ? (int)v : kDefaultChannels;
@@ -190,10 +201,10 @@ void fill_defaults(patConfig_t* c, int n) {
   c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(15));
   if (c->staging_bytes != 0) {
     // explicit budget for the whole pool (flags aside): channels * depth * (n-1) slot triples,
-    // one SIMPLE/PULL slot plus the LL and LL32 slots (each capped by the SIMPLE slot)
-    const size_t b = c->staging_bytes > 8192 ? (c->staging_bytes - 8192) / slots : 0;
-    const size_t ll = kLLSlotBytes + ll32_slot_default();
-    size_t s = b >= ll + std::max(kLLSlotBytes, ll32_slot_default()) ? b - ll : b / 3;
+    // one SIMPLE/PULL slot plus the LL and LL32 slots (polling_slot)
+    const size_t b = budget_per_slot(*c, n);
+    const size_t ll = polling_slot(kLLSlotBytes, b) + polling_slot(ll32_slot_default(), b);
+    size_t s = b > ll ? b - ll : 0;
     s &= ~size_t(127);
     if (s < 256) s = 256;
     c->slice_bytes = s;
@@ -516,9 +527,13 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
   // Inbox regions: SIMPLE/PULL slots, then LL slots. LL polls its lines, so it gets its own
   // memory: a stale payload word left by a bulk protocol could otherwise pass for a flag.
-  comm->ll_slot_bytes = std::max<size_t>(1024, std::min<size_t>(kLLSlotBytes, comm->slot_bytes) & ~size_t(1023));
-  comm->ll32_slot_bytes =
-      std::max<size_t>(1024, std::min<size_t>(ll32_slot_default(), comm->slot_bytes) & ~size_t(1023));
+  size_t llb = kLLSlotBytes, ll32b = ll32_slot_default();
+  if (c.staging_bytes != 0) {  // as fill_defaults sized the bulk slots
+    llb = polling_slot(llb, budget_per_slot(c, nranks));
+    ll32b = polling_slot(ll32b, budget_per_slot(c, nranks));
+  }
+  comm->ll_slot_bytes = std::max<size_t>(1024, std::min<size_t>(llb, comm->slot_bytes) & ~size_t(1023));
+  comm->ll32_slot_bytes = std::max<size_t>(1024, std::min<size_t>(ll32b, comm->slot_bytes) & ~size_t(1023));
   const size_t nslots = static_cast<size_t>(comm->channels) * c.depth * slots;
   auto align = [](size_t x) { return (x + 4095) & ~size_t(4095); };
   comm->region_off[kProtoSimple] = comm->region_off[kProtoPull] = 0;
