@@ -116,7 +116,7 @@ typedef struct {
   int protocol;             /* patProtocol_t */
   int timeout_ms;           /* device-side spin timeout; 0 = default 20000 */
   int threads;              /* threads per CTA, <= 512; 0 = 512 */
-  int depth;                /* inbox buffers per channel (pipeline depth); 0 = ceil(log2 n) + 1 */
+  int depth;                /* inbox buffers per channel (pipeline depth, >= 2); 0 = ceil(log2 n) + 1 */
   int direct;               /* all-gather zero-copy push into peers' recvbufs: -1 off, 0 auto, 1 on.
                                auto = single-process communicator whose recvbufs are reachable
                                (same device, or cudaMalloc memory with peer access) */

@@ -189,7 +189,9 @@ void fill_defaults(patConfig_t* c, int n) {
   // one inbox buffer per PAT round of the full-aggregation schedule, plus one: the skewed
   // sender keeps ceil(log2 n) steps in flight (kernels.cu, send_role)
   if (c->depth <= 0) c->depth = env_int("PAT_DEPTH", &v) ? (int)v : ceil_log2(std::max(n, 2)) + 1;
-  c->depth = std::min(std::max(c->depth, 1), 16);
+  // at least 2: the polling protocols publish a call's last done(step) only when the next call
+  // starts (transport.cuh), which a first step waiting for step base - depth + 1 must not need
+  c->depth = std::min(std::max(c->depth, 2), 16);
   const size_t slots = static_cast<size_t>(c->max_channels) * c->depth * std::max(n - 1, 1);
   if (c->slice_bytes == 0) {
     // large slices amortise the per-round fence + flag (measured: 85 KiB -> 256 KiB slices

@@ -477,8 +477,9 @@ def test_pull_single_tree_schedules(trees):
         assert all(same(got[r], want[r]) for r in range(n)), (trees, elems)
 
 
+@pytest.mark.parametrize("depth", [0, 2])
 @pytest.mark.parametrize("spread", [False, True])
-def test_protocol_switches_share_no_inbox_state(spread):
+def test_protocol_switches_share_no_inbox_state(spread, depth):
     """One communicator whose calls alternate LL / bulk by size: the polling protocol has its
     own inbox region, so payload words a bulk protocol left behind can never pass for a flag. The int32 payload holds small step-counter-like values to make a collision
     likely if the regions were shared."""
@@ -486,7 +487,7 @@ def test_protocol_switches_share_no_inbox_state(spread):
     devices = [r % max(NGPU, 1) for r in range(n)] if spread else [0] * n
     if spread and NGPU < 2:
         pytest.skip("needs >= 2 GPUs")
-    comm = comm_for(n, devices, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=16384)
+    comm = comm_for(n, devices, fused=-1, channels=2, staging_bytes=n * 32 * 1024, ll_threshold=16384, depth=depth)
     for it in range(24):
         elems = [200, 5000, 300000, 3000][it % 4]  # LL, bulk, bulk (RS: PULL), LL (4-byte elements)
         p = (np.arange(n * elems, dtype=np.int64) % 64 + 1 + it).astype(np.int32)
