@@ -1,4 +1,5 @@
-// kernels.cu — sm_100a kernels for PAT all-gather and reduce-scatter.
+// transport.cuh — the sm_100a transport kernel for PAT all-gather and reduce-scatter
+// (instantiated in kernels.cu and rs_*.cu).
 //
 // One cooperative launch per device per collective. CTA (lr, c) runs channel c of local rank
 // lr through `iters` pipeline steps; step i moves slice (i*channels + c) of every chunk
@@ -8,10 +9,10 @@
 // (simulate.cpp:180-218 all-gather, :247-296 reduce-scatter) and its Mailbox rendezvous +
 // lockstep join (simulate.cpp:49-70, 131-149) with per-step release/acquire flags.
 //
-// Protocols:
-//  * LL32 (small messages, default): like LL below with 32-byte lines and one flag word
+// Protocols (the host's calibrated cost model picks one per call, comm.cpp: choose_slicing):
+//  * LL32 (512 KiB up to (n-1) C = 48 MiB): like LL below with 32-byte lines and one flag word
 //    (87.5% wire efficiency); see ll32_phase.
-//  * LL (small messages): 16-byte lines {data32, flag, data32, flag} stored with one
+//  * LL (up to 256 KiB): 16-byte lines {data32, flag, data32, flag} stored with one
 //    st.volatile.v4 into the peer's inbox; the receiver polls the line itself, so data and
 //    signal travel together and no fence or separate flag is needed. 50% wire efficiency.
 //    Every thread owns the same words of every chunk in every round: no CTA barriers.
@@ -21,6 +22,8 @@
 //    (NCCL-style: named barrier, then a single release). Receiver warps wait for the flags
 //    and deliver (all-gather) or fold the output (reduce-scatter), so step g+1's pushes
 //    overlap step g's delivery.
+//  * PULL (mid-size reduce-scatter in one process): receivers read the upstream's buffers;
+//    see pull_role.
 // Inbox slots are `depth`-buffered by step; a rank re-uses a peer's slot buffer only after
 // that peer published "done with step g-depth" (credit flags), so the pool is bounded:
 // channels * depth * (n-1) slots per rank, independent of the message size.
