@@ -33,6 +33,21 @@ def test_library_exports_every_declared_symbol():
     assert L.patGetErrorString(33) == b"InvalidScheduleError"
 
 
+def test_python_constants_match_header_enums():
+    """The binding's protocol / op / dtype numbers are the header's (ABI drift guard)."""
+    header = open(os.path.join(ROOT, "include", "pat_b200.h")).read()
+    enum = {k: int(v) for k, v in re.findall(r"\b(pat\w+)\s*=\s*(\d+)", header)}
+    assert {k: enum[k] for k in ("patProtoAuto", "patProtoLL", "patProtoSimple", "patProtoPull", "patProtoLL32")} == {
+        "patProtoAuto": _lib.PROTO_AUTO, "patProtoLL": _lib.PROTO_LL, "patProtoSimple": _lib.PROTO_SIMPLE,
+        "patProtoPull": _lib.PROTO_PULL, "patProtoLL32": _lib.PROTO_LL32}
+    assert [enum[k] for k in ("patSum", "patProd", "patMax", "patMin")] == [_lib.SUM, _lib.PROD, _lib.MAX, _lib.MIN]
+    names = ["patInt8", "patUint8", "patInt32", "patUint32", "patInt64", "patUint64", "patFloat16", "patFloat32",
+             "patFloat64", "patBfloat16"]
+    consts = [_lib.INT8, _lib.UINT8, _lib.INT32, _lib.UINT32, _lib.INT64, _lib.UINT64, _lib.FLOAT16, _lib.FLOAT32,
+              _lib.FLOAT64, _lib.BFLOAT16]
+    assert [enum[k] for k in names] == consts
+
+
 def test_library_has_sm100a_code():
     so = _lib.LIB_PATH
     import subprocess
