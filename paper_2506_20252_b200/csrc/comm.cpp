@@ -10,14 +10,19 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <unistd.h>
 #include <vector>
 
@@ -95,6 +100,63 @@ bool env_int(const char* name, long long* out) {
 
 }  // namespace
 
+// One host thread per extra device of a one-process communicator. An eager call submits to
+// every device (a cooperative launch costs ~4 us of host time, tools/capi_latency.cpp); the
+// workers submit to their devices while the calling thread does the first, so a call costs one
+// launch instead of one per device. A worker spins for a while after each job (back-to-back
+// calls find it awake), then sleeps on a condition variable.
+struct LaunchWorker {
+  std::thread th;
+  std::atomic<uint32_t> posted{0}, finished{0};
+  std::atomic<bool> stop{false}, sleeping{false};
+  std::mutex m;
+  std::condition_variable cv;
+  const std::function<int()>* job = nullptr;  // valid while posted != finished
+  int result = 0;
+
+  void run() {
+    uint32_t seen = 0;
+    for (;;) {
+      auto t0 = std::chrono::steady_clock::now();
+      uint32_t spins = 0;
+      while (posted.load(std::memory_order_acquire) == seen && !stop.load(std::memory_order_relaxed)) {
+        if ((++spins & 255u) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
+          std::unique_lock<std::mutex> lk(m);
+          sleeping.store(true, std::memory_order_seq_cst);
+          cv.wait(lk, [&] { return posted.load(std::memory_order_acquire) != seen || stop.load(); });
+          sleeping.store(false, std::memory_order_relaxed);
+          t0 = std::chrono::steady_clock::now();
+        }
+      }
+      if (stop.load()) return;
+      seen = posted.load(std::memory_order_acquire);
+      result = (*job)();
+      finished.store(seen, std::memory_order_release);
+    }
+  }
+  void post(const std::function<int()>* j) {
+    job = j;
+    posted.fetch_add(1, std::memory_order_seq_cst);
+    if (sleeping.load(std::memory_order_seq_cst)) {
+      std::lock_guard<std::mutex> lk(m);
+      cv.notify_one();
+    }
+  }
+  int wait() {
+    const uint32_t want = posted.load(std::memory_order_relaxed);
+    while (finished.load(std::memory_order_acquire) != want) std::this_thread::yield();
+    return result;
+  }
+  void shutdown() {
+    {
+      std::lock_guard<std::mutex> lk(m);
+      stop.store(true);
+    }
+    cv.notify_one();
+    if (th.joinable()) th.join();
+  }
+};
+
 struct patComm {
   int n = 0;
   patConfig_t cfg{};
@@ -117,6 +179,7 @@ struct patComm {
   std::map<int, Compiled*> pat_cache;                  // kind*64 + trees -> compiled PAT
   std::map<std::array<int, 5>, int> occupancy;
   std::vector<cudaEvent_t> events;   // per local index
+  std::vector<std::unique_ptr<LaunchWorker>> workers;  // groups[1..] of a one-process comm
   std::mutex mu;
 };
 
@@ -644,8 +707,11 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       for (size_t l = 0; l < comm->lranks.size() && direct; ++l) direct = legacy_ipc_capable(recvbuffs[l]);
     }
   }
-  for (DevGroup& g : comm->groups) {
-    KPlan p = cp->proto;
+  std::vector<KPlan> plans(comm->groups.size());
+  for (size_t gi = 0; gi < comm->groups.size(); ++gi) {
+    DevGroup& g = comm->groups[gi];
+    KPlan& p = plans[gi];
+    p = cp->proto;
     p.nlocal = static_cast<int>(g.lidx.size());
     p.proto = sl.proto;
     p.vec = vec;
@@ -700,6 +766,11 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       p.recv[i] = static_cast<char*>(recvbuffs[l]);
       p.iter_state[i] = g.iter_state + i * kMaxChannels;
     }
+  }
+  // submission to one device: join the stream of every local rank of the device, one launch
+  auto submit = [&](size_t gi) -> patResult_t {
+    const DevGroup& g = comm->groups[gi];
+    const KPlan& p = plans[gi];
     CUDA_TRY(cudaSetDevice(g.device));
     const int threads = comm->cfg.threads;
     cudaStream_t s0 = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr;
@@ -721,14 +792,45 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     } else {
       CUDA_TRY(launch(p, dtype, op, threads, s0));
     }
-    CUDA_TRY(cudaEventRecord(comm->events[g.lidx[0]], s0));
+    bool joined = false;
     for (size_t i = 1; i < g.lidx.size(); ++i) {
       cudaStream_t si = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[i]]) : nullptr;
       if (si == s0) continue;
+      if (!joined) CUDA_TRY(cudaEventRecord(comm->events[g.lidx[0]], s0));
+      joined = true;
       CUDA_TRY(cudaStreamWaitEvent(si, comm->events[g.lidx[0]], 0));
     }
+    return patSuccess;
+  };
+  // Several devices and an eager call: the launch workers submit to devices 1.. while this
+  // thread submits to device 0. A stream being captured into a graph is submitted inline (the
+  // launch cost is paid once at capture then).
+  bool parallel = comm->workers.size() + 1 == comm->groups.size() && comm->groups.size() > 1;
+  if (parallel) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaSetDevice(comm->groups[0].device));
+    const cudaStream_t s0 = streams ? reinterpret_cast<cudaStream_t>(streams[comm->groups[0].lidx[0]]) : nullptr;
+    if (cudaStreamIsCapturing(s0, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      parallel = false;
+    }
   }
-  return patSuccess;
+  if (!parallel) {
+    for (size_t gi = 0; gi < comm->groups.size(); ++gi)
+      if (patResult_t e = submit(gi)) return e;
+    return patSuccess;
+  }
+  std::vector<std::function<int()>> jobs(comm->groups.size());
+  for (size_t gi = 1; gi < comm->groups.size(); ++gi) {
+    jobs[gi] = [&submit, gi] { return static_cast<int>(submit(gi)); };
+    comm->workers[gi - 1]->post(&jobs[gi]);
+  }
+  patResult_t first = submit(0);
+  for (size_t gi = 1; gi < comm->groups.size(); ++gi) {
+    const auto e = static_cast<patResult_t>(comm->workers[gi - 1]->wait());
+    if (first == patSuccess) first = e;
+  }
+  return first;
 }
 
 }  // namespace
@@ -815,6 +917,19 @@ patResult_t patCommInitAll(patComm_t* out, int nranks, const int* devlist, const
   if (patResult_t e = setup_groups(comm.get())) return e;
   for (DevGroup& g : comm->groups)
     for (int r = 0; r < nranks; ++r) g.pool_view[r] = comm->owned_pool[r];
+  long long lt = 1;
+  env_int("PAT_LAUNCH_THREADS", &lt);  // 0: one thread submits to every device in turn
+  if (lt != 0)
+    for (size_t gi = 1; gi < comm->groups.size(); ++gi) {
+      auto w = std::make_unique<LaunchWorker>();
+      const int dev = comm->groups[gi].device;
+      LaunchWorker* wp = w.get();
+      w->th = std::thread([wp, dev] {
+        cudaSetDevice(dev);
+        wp->run();
+      });
+      comm->workers.push_back(std::move(w));
+    }
   comm->finished = true;
   *out = comm.release();
   return patSuccess;
@@ -881,6 +996,8 @@ patResult_t patCommInitRankFinish(patComm_t comm, const void* all_handles) {
 
 patResult_t patCommDestroy(patComm_t comm) {
   if (!comm) return patInvalidArgument;
+  for (auto& w : comm->workers) w->shutdown();
+  comm->workers.clear();
   {
     DeviceGuard guard;
     for (size_t l = 0; l < comm->ldevs.size(); ++l) {
