@@ -1,0 +1,69 @@
+// launch_worker.hpp — host threads that submit one device's share of a collective call
+// (comm.cpp). Header-only so the hand-off protocol is unit-tested on the CPU
+// (tests/test_launch_worker.py).
+#pragma once
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdint>
+#include <functional>
+#include <mutex>
+#include <thread>
+
+// One host thread per extra device of a one-process communicator. An eager call submits to
+// every device (a cooperative launch costs ~4 us of host time, tools/capi_latency.cpp); the
+// workers submit to their devices while the calling thread does the first, so a call costs one
+// launch instead of one per device. A worker spins for a while after each job (back-to-back
+// calls find it awake), then sleeps on a condition variable.
+struct LaunchWorker {
+  std::thread th;
+  std::atomic<uint32_t> posted{0}, finished{0};
+  std::atomic<bool> stop{false}, sleeping{false};
+  std::mutex m;
+  std::condition_variable cv;
+  const std::function<int()>* job = nullptr;  // valid while posted != finished
+  int result = 0;
+
+  void run() {
+    uint32_t seen = 0;
+    for (;;) {
+      auto t0 = std::chrono::steady_clock::now();
+      uint32_t spins = 0;
+      while (posted.load(std::memory_order_acquire) == seen && !stop.load(std::memory_order_relaxed)) {
+        if ((++spins & 255u) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
+          std::unique_lock<std::mutex> lk(m);
+          sleeping.store(true, std::memory_order_seq_cst);
+          cv.wait(lk, [&] { return posted.load(std::memory_order_acquire) != seen || stop.load(); });
+          sleeping.store(false, std::memory_order_relaxed);
+          t0 = std::chrono::steady_clock::now();
+        }
+      }
+      if (stop.load()) return;
+      seen = posted.load(std::memory_order_acquire);
+      result = (*job)();
+      finished.store(seen, std::memory_order_release);
+    }
+  }
+  void post(const std::function<int()>* j) {
+    job = j;
+    posted.fetch_add(1, std::memory_order_seq_cst);
+    if (sleeping.load(std::memory_order_seq_cst)) {
+      std::lock_guard<std::mutex> lk(m);
+      cv.notify_one();
+    }
+  }
+  int wait() {
+    const uint32_t want = posted.load(std::memory_order_relaxed);
+    while (finished.load(std::memory_order_acquire) != want) std::this_thread::yield();
+    return result;
+  }
+  void shutdown() {
+    {
+      std::lock_guard<std::mutex> lk(m);
+      stop.store(true);
+    }
+    cv.notify_one();
+    if (th.joinable()) th.join();
+  }
+};
