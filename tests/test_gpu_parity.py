@@ -564,3 +564,48 @@ def test_randomized_configurations():
         got = gpu_reduce_scatter(comm, devices, q, elems, dt, op, pad=pad)
         want = oracle_rs(n, trees, dt, op, q, elems)
         assert all(same(got[r], want[r]) for r in range(n)), ("rs", case, n, devices, proto, trees, dt, op, elems, pad)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_one_process_graph_capture_and_eager_launch_threads():
+    """One process over several GPUs: eager calls submit through the per-device launch threads,
+    calls captured into per-device CUDA graphs (relaxed, concurrent captures) submit inline;
+    both replay bit-exact."""
+    n = min(NGPU, 4)
+    devices = list(range(n))
+    comm = comm_for(n, devices)
+    elems = 70001
+    p = O.random_payload(O.INT32, n, elems, 41)
+    want = oracle_ag(n, O.max_trees(n), O.INT32, p, elems)
+    sends = [torch.from_numpy(p[r * elems:(r + 1) * elems].copy()).to(f"cuda:{r}") for r in range(n)]
+    recvs = [torch.zeros(n * elems, dtype=torch.int32, device=f"cuda:{r}") for r in range(n)]
+    streams = [torch.cuda.Stream(r) for r in range(n)]
+    for _ in range(3):  # eager, launch threads
+        comm.all_gather(sends, recvs, elems, O.INT32, streams=streams)
+    for r in range(n):
+        torch.cuda.synchronize(r)
+        assert same(recvs[r].cpu().numpy(), want[r])
+        recvs[r].zero_()
+    graphs = [torch.cuda.CUDAGraph() for _ in range(n)]
+    for r in range(n):
+        with torch.cuda.device(r):
+            torch.cuda.set_stream(streams[r])
+            graphs[r].capture_begin(capture_error_mode="relaxed")
+    for _ in range(4):
+        comm.all_gather(sends, recvs, elems, O.INT32, streams=streams)
+    for r in range(n):
+        with torch.cuda.device(r):
+            graphs[r].capture_end()
+            torch.cuda.set_stream(torch.cuda.default_stream(r))
+    for r in range(n):
+        torch.cuda.synchronize(r)
+        recvs[r].zero_()
+        torch.cuda.synchronize(r)
+    for _ in range(2):
+        for r in range(n):
+            with torch.cuda.device(r), torch.cuda.stream(streams[r]):
+                graphs[r].replay()
+    for r in range(n):
+        torch.cuda.synchronize(r)
+        assert same(recvs[r].cpu().numpy(), want[r]), r
+    comm.raise_async_error()
