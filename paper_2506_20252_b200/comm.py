@@ -143,7 +143,11 @@ class PatComm:
     def _streams(self, streams):
         if streams is None:
             if torch is not None and torch.cuda.is_available():
-                streams = [torch.cuda.current_stream(d).cuda_stream for d in self.devices]
+                cur = {}  # one current-stream lookup per device, not per local rank
+                for d in self.devices:
+                    if d not in cur:
+                        cur[d] = torch.cuda.current_stream(d).cuda_stream
+                streams = [cur[d] for d in self.devices]
             else:
                 streams = [0] * len(self.local_ranks)
         return ptr_array([int(getattr(s, "cuda_stream", s)) for s in streams])
