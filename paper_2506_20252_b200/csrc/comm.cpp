@@ -408,7 +408,7 @@ struct CostRow {
   double a_us, b_us, gbs, wire;
 };
 constexpr CostRow kCostLL{3.41, 1.40, 565.0, 2.0};
-constexpr CostRow kCostLL32{3.26, 2.31, 605.0, 32.0 / 28.0};  // one fixed cost per call (below)
+constexpr CostRow kCostLL32{3.07, 2.42, 608.0, 32.0 / 28.0};  // one fixed cost per call (below)
 // LL32 is eligible while a rank moves at most this much payload per call: measured against
 // SIMPLE, LL32 wins up to (n-1) C = 48 MiB at n = 2 and 4 (n = 4, 16 MiB: 106 vs 110 us graph
 // mode; loop mode SIMPLE is 0.95x NCCL there) and is within 6% at n = 3, 16 MiB

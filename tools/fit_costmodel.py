@@ -13,7 +13,8 @@ Since (n-1)*C does not depend on T and b_p > 0, T = max_trees (fewest rounds) mi
 every size: the model justifies the library's fixed T. The LL/SIMPLE crossover it predicts is
 compared with the library's threshold.
 
-  python tools/fit_costmodel.py profiles/r01_ll128_n{2,4}_p{1,2}.jsonl --out profiles/r01_costmodel_fit.json
+  python tools/fit_costmodel.py profiles/r01f_forced_n*_p{1,2}.jsonl profiles/r01f_ll32_noskew_n*.jsonl \
+      > profiles/r01f_costmodel_fit.json
 """
 import argparse
 import json
@@ -43,8 +44,8 @@ def main():
             if r.get("impl") != "pat":
                 continue
             p = r["plan"]["protocol"]
-            if p not in pts or r["plan"]["iterations"] != 1:
-                continue  # single-step points only: multi-step LL adds a per-step term
+            if p not in pts or (r["plan"]["iterations"] != 1 and p != 5):
+                continue  # LL and SIMPLE: single-step points; LL32's extra steps cost nothing (library model)
             n, C = r["n"], r["bytes_per_rank"]
             pts[p].append((n, C, r["us"]))
     fit = {}
@@ -72,7 +73,7 @@ def main():
             best = None
             for k in range(10, 28):
                 C = 1 << k
-                steps = max(1, -(-C // STEP_BYTES[ll]))
+                steps = max(1, -(-C // STEP_BYTES[ll])) if ll == "LL" else 1
                 tl = steps * (L["a_us"] + L["b_us_per_round"] * R) + L["wire"] * (n - 1) * C / (L["link_gbs"] * 1e3)
                 ts = S["a_us"] + S["b_us_per_round"] * R + S["wire"] * (n - 1) * C / (S["link_gbs"] * 1e3)
                 if tl > ts:
