@@ -6,7 +6,7 @@ device's launches works: the other devices' kernels were launched (unprofiled, a
 just before and run alongside. Kernel replay would re-run the profiled kernel without its
 peers, so the whole application is replayed instead:
 
-  ncu --devices 1 --replay-mode application --clock-control none -k regex:pat_kernel \\
+  PAT_LAUNCH_THREADS=0 ncu --devices 1 --replay-mode application --clock-control none -k regex:pat_kernel \\
       --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \\
       --csv --log-file gpurun_out/ncu_nvlink.csv python tools/ncu_nvlink.py --gpus 2
 
@@ -29,6 +29,8 @@ def main():
     args = ap.parse_args()
     import torch
 
+    # device 0's launch must be issued before ncu holds the profiled one: one submitting thread
+    os.environ.setdefault("PAT_LAUNCH_THREADS", "0")
     from paper_2506_20252_b200 import FLOAT32, SUM, PatComm
 
     n = args.gpus
