@@ -2,11 +2,20 @@
 
 Workload (BASELINE.json configs[0]): 1 MiB fp32 per rank (262,144 elements), all-gather of
 one chunk per rank and reduce-scatter of n chunks per rank into one.
-  * N = 1 (plain `python bench.py`): n = 8 logical ranks on cuda:0, one cooperative kernel
-    per collective ("local mode"; every rank's data in one GPU's HBM -> HBM roofline).
-  * N > 1 (torchrun, one process per GPU): n = N ranks over NVLink, inbox pools mapped with
-    CUDA IPC. NCCL's Ring all-gather / reduce-scatter is timed on the same buffers as a
-    comparison (`nccl_ring`).
+
+Placement, chosen from how the script is launched:
+  * N = 1 (`python bench.py`): n = 8 logical ranks on cuda:0 (the reference's in-process ranks,
+    BASELINE configs[0] exactly); the fused single-device executor (local.cu) runs it — every
+    rank's data in one GPU's HBM, so the HBM roofline applies. The same n = 8 call through the
+    PAT transport kernel (per-round messages and flags, `fused = -1`) is timed beside it
+    (`transport_local`).
+  * N > 1 under torchrun (the driver's form; WORLD_SIZE = N): n = N ranks, one process per
+    GPU, inbox pools mapped with CUDA IPC; NCCL's Ring all-gather / reduce-scatter is timed on
+    the same buffers the same way (CUDA graphs) as the comparison (`nccl_ring`).
+  * N > 1 without torchrun (`python bench.py --gpus N [--ranks M]`): ONE process drives all N
+    GPUs (patCommInitAll, the north-star process model); M ranks (default N) placed round-robin,
+    e.g. `--gpus 4 --ranks 8` puts the n = 8 workload on devices [0,1,2,3,0,1,2,3].
+  A line whose n_gpus differs from --gpus is never printed: a mismatch exits with status 2.
 
 metric: aggregate bus bandwidth of the step = 2 * n * (n-1) * C bytes / step time (GB/s);
 every rank receives (n-1)*C per collective (test_simulate.cpp:101-111). Per-collective
@@ -14,7 +23,7 @@ latencies are reported beside it.
 
 `--impl reference` times the reference's own CPU executor (oracle/_ref, compiled from
 /root/reference/proj/src) on the host cores on the same n and C (int64 all-gather + float64
-reduce-scatter: equal bytes), rank 0 only.
+reduce-scatter: equal bytes; the reference supports only those), rank 0 only.
 """
 from __future__ import annotations
 
@@ -32,27 +41,53 @@ sys.path.insert(0, ROOT)
 CHUNK_BYTES = 1 << 20  # 1 MiB per rank
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 L2_BYTES = 126 * 1000 * 1000
-NVLINK_MEASURED_GBS = 770.0  # peer copy per direction (B200_PROFILING.md)
+NVLINK_PEER_COPY_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_NOMINAL_GBS = 900.0    # NVLink 5, 18 links, per direction per GPU
+NVLINK_SM_PUSH_GBS = 704.0    # SM stores into peers, every GPU sending (profiles/r01_bidir_probe_g4.txt)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="pat", choices=["pat", "reference"])
     ap.add_argument("--chunk-bytes", type=int, default=CHUNK_BYTES)
-    ap.add_argument("--ranks", type=int, default=0, help="logical ranks at N=1 (default 8)")
+    ap.add_argument("--ranks", type=int, default=0,
+                    help="ranks without torchrun (default: 8 at --gpus 1, else --gpus), placed round-robin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip transport_local / ref_dtypes records")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
     if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1:
         return int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ.get("LOCAL_RANK", 0))
     return 0, 1, 0
+
+
+def placement(args, world: int, ngpu_visible: int):
+    """(n, devices of the ranks this process drives, n_gpus of the job, mode) or raises
+    SystemExit(2) when the request cannot be honoured as asked."""
+    if world > 1:  # torchrun: one rank per process, one GPU each
+        if args.gpus != world:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to report n_gpus={world}")
+        if args.ranks not in (0, world):
+            raise SystemExit("bench.py: --ranks must equal WORLD_SIZE under torchrun (one rank per process)")
+        return world, None, world, "torchrun"
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.gpus > ngpu_visible:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {ngpu_visible} GPU(s) visible")
+    if args.gpus == 1:
+        n = args.ranks or 8
+        return n, [0] * n, 1, "local"
+    n = args.ranks or args.gpus
+    if n < args.gpus:
+        raise SystemExit(f"bench.py: --ranks {n} < --gpus {args.gpus} would leave GPUs idle")
+    return n, [r % args.gpus for r in range(n)], args.gpus, "one-process"
 
 
 def load_peaks():
@@ -65,44 +100,31 @@ def load_peaks():
 
 # ------------------------------------------------------------------ reference CPU path
 
-def reference_time(n: int, chunk_bytes: int, seconds: float, mode: int = 1, max_steps: int = 10000):
+def reference_time(n: int, chunk_bytes: int, seconds: float, mode: int = 1, max_steps: int = 10000,
+                   warmup: int = 1):
     """The reference executor (oracle/_ref) on the host: run_allgather(int64) +
-    run_reduce_scatter(float64, FloatSum) with equal bytes per chunk. Returns
-    (seconds per step, steps, threads)."""
-    import ctypes
-
-    import numpy as np
-
+    run_reduce_scatter(float64, FloatSum) with equal bytes per chunk. The schedules and the
+    reference's own Payload<T>s are built once (ref_prepare); a timed step calls only the
+    reference's run_* (no marshalling, results dropped). Returns (seconds per step, steps, threads)."""
     import oracle as O
 
     R = O.ref()
-    elems = chunk_bytes // 8
-    ag = O.pat_allgather(n, O.max_trees(n))
-    rs = O.pat_reduce_scatter(n, O.max_trees(n))
-    pin = np.zeros(n * elems, np.int64)
-    R.ref_random_payload(0, O.INT64, n, elems, 0, pin.ctypes.data)
-    pout = np.zeros(n * n * elems, np.int64)
-    qin = np.zeros(n * n * elems, np.float64)
-    R.ref_random_payload(1, O.FLOAT64, n, elems, 0, qin.ctypes.data)
-    qout = np.zeros(n * elems, np.float64)
     threads = os.cpu_count() or 1
-    st = np.zeros(600, np.int64)
-
-    def one():
-        rc = R.ref_run_allgather(ag.ctypes.data_as(O.I32P), len(ag), O.INT64, elems, pin.ctypes.data,
-                                 pout.ctypes.data, st.ctypes.data_as(O.I64P), mode, threads)
-        rc |= R.ref_run_reduce_scatter(rs.ctypes.data_as(O.I32P), len(rs), O.FLOAT64, elems, qin.ctypes.data,
-                                       qout.ctypes.data, st.ctypes.data_as(O.I64P), mode, threads)
-        assert rc == 0
-
-    one()  # warm-up
-    steps, t0 = 0, time.perf_counter()
-    while True:
-        one()
-        steps += 1
-        el = time.perf_counter() - t0
-        if el >= seconds or steps >= max_steps:
-            break
+    h = R.ref_prepare(n, O.max_trees(n), chunk_bytes // 8, mode, threads)
+    if not h:
+        raise RuntimeError(R.ref_last_error().decode())
+    try:
+        for _ in range(warmup):
+            assert R.ref_run_prepared(h, 3) == 0
+        steps, t0 = 0, time.perf_counter()
+        while True:
+            assert R.ref_run_prepared(h, 3) == 0
+            steps += 1
+            el = time.perf_counter() - t0
+            if el >= seconds or steps >= max_steps:
+                break
+    finally:
+        R.ref_free_prepared(h)
     return el / steps, steps, threads if mode else 1
 
 
@@ -118,9 +140,9 @@ def busbw_gbs(n: int, chunk_bytes: int, seconds: float) -> float:
 # ------------------------------------------------------------------ clocks during the timed region
 
 class ClockSampler:
-    """NVML sampling of SM clock + throttle reasons every ~5 ms on one GPU."""
+    """NVML sampling of SM clock + throttle reasons every ~2 ms on the GPUs this process drives."""
 
-    def __init__(self, device: int):
+    def __init__(self, devices):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
         self.ok = False
@@ -129,13 +151,13 @@ class ClockSampler:
 
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.hs = [pynvml.nvmlDeviceGetHandleByIndex(d) for d in devices]
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.hs[0], pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception:
             pass
 
-    def _run(self):
+    def _sample(self):
         nv = self.nv
         names = {
             "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
@@ -144,19 +166,24 @@ class ClockSampler:
             "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
             "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
         }
-        while not self._stop.is_set():
+        for h in self.hs:
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 for k, bit in names.items():
                     if mask & bit:
                         self.reasons.add(k)
             except Exception:
                 pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
             time.sleep(0.002)
 
     def __enter__(self):
         if self.ok:
+            self._sample()  # at least one sample inside a short timed region
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         return self
@@ -171,273 +198,387 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# ------------------------------------------------------------------ per-device graph plumbing
+
+class Devices:
+    """The GPUs this process drives: one dedicated stream each; CUDA graphs captured concurrently
+    on every device (relaxed mode), replayed together, timed per device with events on the
+    launching stream and reduced as the max over devices (then over ranks)."""
+
+    def __init__(self, torch, devs, dist=None):
+        self.torch, self.devs, self.dist = torch, list(devs), dist
+        self.streams = {d: torch.cuda.Stream(d) for d in self.devs}
+
+    def sync(self):
+        for d in self.devs:
+            self.torch.cuda.synchronize(d)
+
+    def barrier(self):
+        self.sync()
+        if self.dist is not None:
+            self.dist.barrier()
+        self.sync()
+
+    def capture(self, body):
+        torch = self.torch
+        graphs = {d: torch.cuda.CUDAGraph() for d in self.devs}
+        for d in self.devs:
+            self.streams[d].wait_stream(torch.cuda.current_stream(d))
+            with torch.cuda.device(d):
+                torch.cuda.set_stream(self.streams[d])
+                graphs[d].capture_begin(capture_error_mode="relaxed")
+        try:
+            body()
+        finally:
+            for d in self.devs:
+                with torch.cuda.device(d):
+                    graphs[d].capture_end()
+                    torch.cuda.set_stream(torch.cuda.default_stream(d))
+        return graphs
+
+    def replay(self, graphs):
+        torch = self.torch
+        for d in self.devs:
+            with torch.cuda.device(d), torch.cuda.stream(self.streams[d]):
+                graphs[d].replay()
+
+    def events(self):
+        E = self.torch.cuda.Event
+        return {d: (E(enable_timing=True), E(enable_timing=True)) for d in self.devs}
+
+    def time_ms(self, run):
+        """barrier; start events; run(); end events; barrier -> max over devices (ms)."""
+        ev = self.events()
+        self.barrier()
+        for d in self.devs:
+            ev[d][0].record(self.streams[d])
+        run()
+        for d in self.devs:
+            ev[d][1].record(self.streams[d])
+        self.barrier()
+        return max(ev[d][0].elapsed_time(ev[d][1]) for d in self.devs)
+
+
+def max_over_ranks(torch, dist, dev, values):
+    t = torch.tensor(values, dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
 # ------------------------------------------------------------------ PAT arm
 
 def run_pat(args, rank, world, local):
     import torch
-    import torch.distributed as dist
 
-    from paper_2506_20252_b200 import FLOAT32, SUM, PatComm
+    dist = None
+    n, devices, n_gpus, mode = placement(args, world, torch.cuda.device_count())
+    from paper_2506_20252_b200 import FLOAT32, FLOAT64, INT64, SUM, PatComm
 
-    dev = torch.device(f"cuda:{local}")
-    torch.cuda.set_device(dev)
     C = args.chunk_bytes
     elems = C // 4
-    if world > 1:
+    if mode == "torchrun":
+        import torch.distributed as dist
+
+        dev0 = torch.device(f"cuda:{local}")
+        torch.cuda.set_device(dev0)
         os.environ.setdefault("NCCL_ALGO", "Ring")  # affects only the NCCL comparison below
-        dist.init_process_group("nccl", device_id=dev)
-        n = world
+        dist.init_process_group("nccl", device_id=dev0)
+        devices = [local]
         comm = PatComm.from_process_group(device=local)
-        ranks_here = [rank]
-        placement = f"{n} ranks on {n} GPUs (1 process per GPU, CUDA IPC pools)"
+        desc = f"{n} ranks on {n} GPUs (torchrun: 1 process per GPU, CUDA IPC inbox pools)"
     else:
-        n = args.ranks or 8
-        comm = PatComm.init_all(n, [local] * n)
-        ranks_here = list(range(n))
-        placement = f"{n} logical ranks on 1 GPU (fused single-device executor, local.cu)"
-    L = len(ranks_here)
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    # Inputs larger than L2: the step's buffers are rotated over S sets whose total exceeds
-    # twice the 126 MB L2, so every timed step starts cold.
-    step_bytes = L * 2 * (n + 1) * C
+        torch.cuda.set_device(devices[0])
+        comm = PatComm.init_all(n, devices)
+        desc = (f"{n} logical ranks on 1 GPU (fused single-device executor, local.cu)" if mode == "local" else
+                f"{n} ranks on {n_gpus} GPUs, one process (patCommInitAll), devices {devices}")
+    dev0 = torch.device(f"cuda:{devices[0]}")
+    L = len(devices)  # ranks this process drives
+    D = Devices(torch, sorted(set(devices)), dist)
+    streams = [D.streams[d] for d in devices]
+    g = {d: torch.Generator(device=f"cuda:{d}").manual_seed(1234 + 17 * rank + d) for d in D.devs}
+
+    def rnd(numel, d):
+        return torch.rand(numel, device=f"cuda:{d}", generator=g[d])
+
+    # Inputs larger than L2: the step's buffers are rotated over S sets whose total per GPU
+    # exceeds twice the 126 MB L2, so every timed step starts cold.
+    per_gpu_ranks = max(devices.count(d) for d in D.devs)
+    step_bytes = per_gpu_ranks * 2 * (n + 1) * C
     S = max(2, -(-(2 * L2_BYTES) // step_bytes) + 1)
     sets = []
     for _ in range(S):
         sets.append({
-            "ag_send": [torch.rand(elems, device=dev, generator=g) for _ in range(L)],
-            "ag_recv": [torch.empty(n * elems, device=dev) for _ in range(L)],
-            "rs_send": [torch.rand(n * elems, device=dev, generator=g) for _ in range(L)],
-            "rs_recv": [torch.empty(elems, device=dev) for _ in range(L)],
+            "ag_send": [rnd(elems, d) for d in devices],
+            "ag_recv": [torch.empty(n * elems, device=f"cuda:{d}") for d in devices],
+            "rs_send": [rnd(n * elems, d) for d in devices],
+            "rs_recv": [torch.empty(elems, device=f"cuda:{d}") for d in devices],
         })
-    ag_send, ag_recv, rs_send, rs_recv = (sets[0][k] for k in ("ag_send", "ag_recv", "rs_send", "rs_recv"))
-    stream = torch.cuda.current_stream(dev)
 
-    def step(bs=None):
-        bs = bs or sets[0]
-        comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
-        comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
+    def call(c, kinds, bs, dtype=FLOAT32, count=elems):
+        if "ag" in kinds:
+            c.all_gather(bs["ag_send"], bs["ag_recv"], count, dtype, streams=streams)
+        if "rs" in kinds:
+            c.reduce_scatter(bs["rs_send"], bs["rs_recv"], count, dtype, SUM, streams=streams)
 
     dbg("warmup")
     for _ in range(args.warmup):
         for bs in sets:
-            step(bs)
-    barrier()
+            call(comm, ("ag", "rs"), bs)
+    D.barrier()
     comm.raise_async_error()
-    dbg("capture")
-    # The timed region replays ONE CUDA graph holding exactly K steps (step k = PAT all-gather +
+
+    # The timed region replays CUDA graphs holding exactly K steps (step k = PAT all-gather +
     # PAT reduce-scatter on buffer set k % S), captured from the C-ABI calls: the launches are
-    # the library's own kernels back to back, without Python/ctypes host gaps. Two more graphs
-    # of K all-gathers and K reduce-scatters give the per-collective latencies.
+    # the library's own kernels back to back, without Python/ctypes host gaps. More graphs of K
+    # all-gathers and K reduce-scatters give the per-collective latencies.
     K = args.steps
     G = min(K, 1000)  # steps per graph; the timed region replays it K // G times (+ a remainder graph)
-
-    def capture(kinds, count):
-        gph = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream(dev)
-        cap.wait_stream(stream)
-        with torch.cuda.stream(cap):
-            with torch.cuda.graph(gph, stream=cap):
-                for k in range(count):
-                    bs = sets[k % S]
-                    if "ag" in kinds:
-                        comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
-                    if "rs" in kinds:
-                        comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
-        stream.wait_stream(cap)
-        return gph
-
     rem = K % G
-    graphs = {kinds: (capture(kinds, G), capture(kinds, rem) if rem else None)
-              for kinds in (("ag", "rs"), ("ag",), ("rs",))}
-    dbg("replay-warm")
-    for full, part in graphs.values():
-        full.replay()
-        if part is not None:
-            part.replay()
-    barrier()
+
+    def graphs_for(c, kinds, sets_=sets, **kw):
+        def body(count):
+            def run():
+                for k in range(count):
+                    call(c, kinds, sets_[k % len(sets_)], **kw)
+            return run
+        full = D.capture(body(G))
+        part = D.capture(body(rem)) if rem else None
+        return full, part
+
+    def replay_k(pair):
+        full, part = pair
+
+        def run():
+            for _ in range(K // G):
+                D.replay(full)
+            if part is not None:
+                D.replay(part)
+        return run
+
+    dbg("capture")
+    graphs = {kinds: graphs_for(comm, kinds) for kinds in (("ag", "rs"), ("ag",), ("rs",))}
+    for pair in graphs.values():  # warm replay
+        replay_k(pair)()
+    D.barrier()
+
     dbg("timed")
-
-    def timed_replay(kinds):
-        full, part = graphs[kinds]
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier()
-        a.record(stream)
-        for _ in range(K // G):  # exactly K steps: K // G replays of G steps + the remainder
-            full.replay()
-        if part is not None:
-            part.replay()
-        b.record(stream)
-        barrier()
-        return a.elapsed_time(b)
-
-    with ClockSampler(local) as clocks:
-        step_ms = timed_replay(("ag", "rs"))
-        ag_ms, rs_ms = timed_replay(("ag",)), timed_replay(("rs",))
+    with ClockSampler(D.devs) as clocks:
+        step_ms = D.time_ms(replay_k(graphs[("ag", "rs")]))
+        ag_ms = D.time_ms(replay_k(graphs[("ag",)]))
+        rs_ms = D.time_ms(replay_k(graphs[("rs",)]))
     comm.raise_async_error()
-    tot = torch.tensor([step_ms, ag_ms, rs_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    tot_ms, ag_ms, rs_ms = (float(x) for x in tot.tolist())
-    ms_per_step = tot_ms / K
+    step_ms, ag_ms, rs_ms = max_over_ranks(torch, dist, dev0, [step_ms, ag_ms, rs_ms])
+    del graphs
+    ms_per_step = step_ms / K
     value = busbw_gbs(n, C, ms_per_step / 1e3)
 
-    # ---- the same steps launched eagerly through the C ABI (apples-to-apples with NCCL eager)
+    # ---- the same steps launched eagerly through the C ABI (events per call)
     KE = min(K, 100)
-    eev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(KE)]
-    barrier()
+    eev = [D.events() for _ in range(3 * KE)]
+    D.barrier()
     for k in range(KE):
         bs = sets[k % S]
-        eev[k][0].record(stream)
-        comm.all_gather(bs["ag_send"], bs["ag_recv"], elems, FLOAT32)
-        eev[k][1].record(stream)
-        comm.reduce_scatter(bs["rs_send"], bs["rs_recv"], elems, FLOAT32, SUM)
-        eev[k][2].record(stream)
-    barrier()
-    et = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in eev), sum(e[1].elapsed_time(e[2]) for e in eev)],
-                      dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    eager_us = {"all_gather": 1e3 * float(et[0]) / KE, "reduce_scatter": 1e3 * float(et[1]) / KE}
+        for d in D.devs:
+            eev[3 * k][d][0].record(D.streams[d])
+        call(comm, ("ag",), bs)
+        for d in D.devs:
+            eev[3 * k][d][1].record(D.streams[d])
+            eev[3 * k + 1][d][0].record(D.streams[d])
+        call(comm, ("rs",), bs)
+        for d in D.devs:
+            eev[3 * k + 1][d][1].record(D.streams[d])
+    D.barrier()
+    ag_e = max(sum(eev[3 * k][d][0].elapsed_time(eev[3 * k][d][1]) for k in range(KE)) for d in D.devs)
+    rs_e = max(sum(eev[3 * k + 1][d][0].elapsed_time(eev[3 * k + 1][d][1]) for k in range(KE)) for d in D.devs)
+    ag_e, rs_e = max_over_ranks(torch, dist, dev0, [ag_e, rs_e])
+    eager_us = {"all_gather": 1e3 * ag_e / KE, "reduce_scatter": 1e3 * rs_e / KE}
 
     dbg("e2e")
-    # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region
+    # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region.
+    # Double-buffered per device: step k's inputs go up on a copy stream into device set k % 2
+    # while step k-1 runs, and step k-1's results come down on another copy stream (PCIe is full
+    # duplex); every step still copies all of its inputs in and its results out inside the
+    # timed region.
     h_ag_send = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(L)]
     h_rs_send = [torch.empty(n * elems, dtype=torch.float32).pin_memory() for _ in range(L)]
     h_ag_recv = [torch.empty(n * elems, dtype=torch.float32).pin_memory() for _ in range(L)]
     h_rs_recv = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(L)]
     for i in range(L):
-        h_ag_send[i].copy_(ag_send[i].cpu())
-        h_rs_send[i].copy_(rs_send[i].cpu())
-    # Double-buffered: step k's inputs go up on a copy stream into device set k % 2 while step
-    # k-1 runs, and step k-1's results come down on another copy stream (PCIe is full duplex, so
-    # the two directions overlap); every step still copies all of its inputs in and its results
-    # out inside the timed region.
+        h_ag_send[i].copy_(sets[0]["ag_send"][i].cpu())
+        h_rs_send[i].copy_(sets[0]["rs_send"][i].cpu())
     E = max(3, min(K, 20))
     dsets = [sets[j % len(sets)] for j in range(2)]
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    ev = lambda: torch.cuda.Event()  # noqa: E731
+    s_in = {d: torch.cuda.Stream(d) for d in D.devs}
+    s_out = {d: torch.cuda.Stream(d) for d in D.devs}
+    ev = lambda: {d: torch.cuda.Event() for d in D.devs}  # noqa: E731
     h2d_done, comp_done, d2h_done = [ev() for _ in range(E)], [ev() for _ in range(E)], [ev() for _ in range(E)]
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    s_in.wait_stream(stream)
-    s_out.wait_stream(stream)
+    e01 = D.events()
+    D.barrier()
+    for d in D.devs:
+        e01[d][0].record(D.streams[d])
+        s_in[d].wait_stream(D.streams[d])
+        s_out[d].wait_stream(D.streams[d])
     for k in range(E):
         bs = dsets[k % 2]
-        with torch.cuda.stream(s_in):
+        for d in D.devs:
+            with torch.cuda.device(d), torch.cuda.stream(s_in[d]):
+                if k >= 2:
+                    s_in[d].wait_event(comp_done[k - 2][d])  # set k % 2's inputs are free
+                for i, di in enumerate(devices):
+                    if di == d:
+                        bs["ag_send"][i].copy_(h_ag_send[i], non_blocking=True)
+                        bs["rs_send"][i].copy_(h_rs_send[i], non_blocking=True)
+                h2d_done[k][d].record(s_in[d])
+            D.streams[d].wait_event(h2d_done[k][d])
             if k >= 2:
-                s_in.wait_event(comp_done[k - 2])  # set k % 2's inputs are free
-            for i in range(L):
-                bs["ag_send"][i].copy_(h_ag_send[i], non_blocking=True)
-                bs["rs_send"][i].copy_(h_rs_send[i], non_blocking=True)
-            h2d_done[k].record(s_in)
-        stream.wait_event(h2d_done[k])
-        if k >= 2:
-            stream.wait_event(d2h_done[k - 2])  # set k % 2's outputs were read back
-        step(bs)
-        comp_done[k].record(stream)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(comp_done[k])
-            for i in range(L):
-                h_ag_recv[i].copy_(bs["ag_recv"][i], non_blocking=True)
-                h_rs_recv[i].copy_(bs["rs_recv"][i], non_blocking=True)
-            d2h_done[k].record(s_out)
-    stream.wait_event(d2h_done[E - 1])
-    stream.wait_event(h2d_done[E - 1])
-    e1.record(stream)
-    barrier()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1) / E], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_ms.item())
-    h2d = L * (elems + n * elems) * 4
-    d2h = L * (n * elems + elems) * 4
+                D.streams[d].wait_event(d2h_done[k - 2][d])  # set k % 2's outputs were read back
+        call(comm, ("ag", "rs"), bs)
+        for d in D.devs:
+            comp_done[k][d].record(D.streams[d])
+            with torch.cuda.device(d), torch.cuda.stream(s_out[d]):
+                s_out[d].wait_event(comp_done[k][d])
+                for i, di in enumerate(devices):
+                    if di == d:
+                        h_ag_recv[i].copy_(bs["ag_recv"][i], non_blocking=True)
+                        h_rs_recv[i].copy_(bs["rs_recv"][i], non_blocking=True)
+                d2h_done[k][d].record(s_out[d])
+    for d in D.devs:
+        D.streams[d].wait_event(d2h_done[E - 1][d])
+        D.streams[d].wait_event(h2d_done[E - 1][d])
+        e01[d][1].record(D.streams[d])
+    D.barrier()
+    e2e_ms = max_over_ranks(torch, dist, dev0, [max(e01[d][0].elapsed_time(e01[d][1]) for d in D.devs) / E])[0]
+    # bytes of the whole job per step (every rank's inputs up, every rank's outputs down)
+    ranks_total = n
+    h2d = ranks_total * (elems + n * elems) * 4
+    d2h = ranks_total * (n * elems + elems) * 4
 
-    # ---- NCCL Ring comparison (N > 1)
+    # ---- NCCL Ring comparison (torchrun), timed exactly like the PAT arm: CUDA graphs of K steps
     nccl = None
     dbg("nccl")
-    if world > 1 and not args.no_nccl:
+    if mode == "torchrun" and not args.no_nccl:
+        def nccl_call(kinds, bs):
+            if "ag" in kinds:
+                dist.all_gather_into_tensor(bs["ag_recv"][0], bs["ag_send"][0])
+            if "rs" in kinds:
+                dist.reduce_scatter_tensor(bs["rs_recv"][0], bs["rs_send"][0])
+
         for _ in range(args.warmup):
             for bs in sets:
-                dist.all_gather_into_tensor(bs["ag_recv"][0], bs["ag_send"][0])
-                dist.reduce_scatter_tensor(bs["rs_recv"][0], bs["rs_send"][0])
-        barrier()
-        # same timing method as the PAT arm: graph replay when NCCL captures, else eager
-        ngraphs, mode = [], "graph"
-        dbg("nccl-capture")
+                with torch.cuda.stream(streams[0]):
+                    nccl_call(("ag", "rs"), bs)
+        D.barrier()
+        timing = "graph"
         try:
-            if not os.environ.get("BENCH_NCCL_GRAPH"):  # capturing many NCCL graphs hung on 2.28.9
-                raise RuntimeError("eager")
-            cap2 = torch.cuda.Stream(dev)
-            cap2.wait_stream(stream)
-            with torch.cuda.stream(cap2):
-                for bs in sets:
-                    ga, gr = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(ga, stream=cap2):
-                        dist.all_gather_into_tensor(bs["ag_recv"][0], bs["ag_send"][0])
-                    with torch.cuda.graph(gr, stream=cap2):
-                        dist.reduce_scatter_tensor(bs["rs_recv"][0], bs["rs_send"][0])
-                    ngraphs.append((ga, gr))
-            stream.wait_stream(cap2)
-            for ga, gr in ngraphs:
-                ga.replay()
-                gr.replay()
-        except Exception:
-            mode, ngraphs = "eager", []
-        barrier()
-        KN = min(K, 1000)
-        nev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(KN)]
-        for k in range(KN):
-            bs = sets[k % S]
-            nev[k][0].record(stream)
-            if ngraphs:
-                ngraphs[k % S][0].replay()
-            else:
-                dist.all_gather_into_tensor(bs["ag_recv"][0], bs["ag_send"][0])
-            nev[k][1].record(stream)
-            if ngraphs:
-                ngraphs[k % S][1].replay()
-            else:
-                dist.reduce_scatter_tensor(bs["rs_recv"][0], bs["rs_send"][0])
-            nev[k][2].record(stream)
-        barrier()
-        nt = torch.tensor([sum(e[0].elapsed_time(e[2]) for e in nev), sum(e[0].elapsed_time(e[1]) for e in nev),
-                           sum(e[1].elapsed_time(e[2]) for e in nev)], dtype=torch.float64, device=dev)
-        dist.all_reduce(nt, op=dist.ReduceOp.MAX)
-        nt = nt.tolist()
-        nccl = {"algo": os.environ.get("NCCL_ALGO"), "ms_per_step": nt[0] / KN,
-                "busbw_gbs": busbw_gbs(n, C, nt[0] / KN / 1e3),
-                "ag_us": 1e3 * nt[1] / KN, "rs_us": 1e3 * nt[2] / KN,
-                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()), "timing": mode}
+            def nbody(kinds, count):
+                def run():
+                    for k in range(count):
+                        nccl_call(kinds, sets[k % S])
+                return run
+            ngraphs = {}
+            for kinds in (("ag", "rs"), ("ag",), ("rs",)):
+                ngraphs[kinds] = (D.capture(nbody(kinds, G)), D.capture(nbody(kinds, rem)) if rem else None)
+            for pair in ngraphs.values():
+                replay_k(pair)()
+            D.barrier()
+            nt = [D.time_ms(replay_k(ngraphs[kinds])) for kinds in (("ag", "rs"), ("ag",), ("rs",))]
+            del ngraphs
+        except Exception as e:  # eager fallback, labelled
+            dbg(f"nccl graph capture failed: {e}")
+            timing = f"eager (graph capture failed: {type(e).__name__})"
+            D.barrier()
+
+            def eager(kinds):
+                def run():
+                    with torch.cuda.stream(streams[0]):
+                        for k in range(K):
+                            nccl_call(kinds, sets[k % S])
+                return run
+            nt = [D.time_ms(eager(kinds)) for kinds in (("ag", "rs"), ("ag",), ("rs",))]
+        nt = max_over_ranks(torch, dist, dev0, nt)
+        nccl = {"algo": os.environ.get("NCCL_ALGO"), "ms_per_step": nt[0] / K,
+                "busbw_gbs": busbw_gbs(n, C, nt[0] / K / 1e3),
+                "ag_us": 1e3 * nt[1] / K, "rs_us": 1e3 * nt[2] / K,
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()), "timing": timing,
+                "pat_speedup_step": nt[0] / step_ms}
+
+    # ---- N = 1 extras: the same n = 8 workload through the PAT transport kernel (per-round
+    # messages through the inbox pools with flags), and the repo at the reference arm's dtypes
+    extras = {}
+    if mode == "local" and not args.no_extras:
+        dbg("transport_local")
+        tcomm = PatComm.init_all(n, devices, fused=-1)
+        for _ in range(max(3, args.warmup // 4)):
+            for bs in sets:
+                call(tcomm, ("ag", "rs"), bs)
+        D.barrier()
+        tg = {kinds: graphs_for(tcomm, kinds) for kinds in (("ag",), ("rs",))}
+        for pair in tg.values():
+            replay_k(pair)()
+        t_ag = D.time_ms(replay_k(tg[("ag",)]))
+        t_rs = D.time_ms(replay_k(tg[("rs",)]))
+        tcomm.raise_async_error()
+        pa, pr = tcomm.plan(0, elems, FLOAT32), tcomm.plan(1, elems, FLOAT32)
+        names = {1: "LL", 2: "SIMPLE", 3: "PULL", 5: "LL32"}
+        extras["transport_local"] = {
+            "kernel": "pat_kernel (fused = -1)", "all_gather_us": 1e3 * t_ag / K, "reduce_scatter_us": 1e3 * t_rs / K,
+            "protocol": {"all_gather": names.get(pa["protocol"]), "reduce_scatter": names.get(pr["protocol"])},
+            "channels": pa["channels"], "rounds": pa["rounds"], "pool_bytes_per_rank": pa["pool_bytes"],
+            "busbw_gbs": busbw_gbs(n, C, (t_ag + t_rs) / K / 1e3),
+            "timing": "CUDA graphs of K calls per collective, same buffer sets"}
+        del tg
+        tcomm.destroy()
+        # int64 all-gather + float64 reduce-scatter at equal bytes: the reference arm's dtypes
+        dbg("ref_dtypes")
+        e8 = C // 8
+        for _ in range(2):
+            for bs in sets:
+                call(comm, ("ag",), bs, dtype=INT64, count=e8)
+                call(comm, ("rs",), bs, dtype=FLOAT64, count=e8)
+        D.barrier()
+        rg_f = graphs_for(comm, ("rs",), dtype=FLOAT64, count=e8)
+        rg_a = graphs_for(comm, ("ag",), dtype=INT64, count=e8)
+        for pair in (rg_f, rg_a):
+            replay_k(pair)()
+        t_a = D.time_ms(replay_k(rg_a))
+        t_f = D.time_ms(replay_k(rg_f))
+        extras["ref_dtypes"] = {
+            "dtype": "int64 all-gather + f64 reduce-scatter(sum), equal bytes (the reference arm's dtypes)",
+            "ms_per_step": (t_a + t_f) / K, "value": busbw_gbs(n, C, (t_a + t_f) / K / 1e3), "unit": "GB/s",
+            "all_gather_us": 1e3 * t_a / K, "reduce_scatter_us": 1e3 * t_f / K,
+            "timing": "sum of CUDA-graph-timed K int64 all-gathers and K f64 reduce-scatters"}
+        del rg_f, rg_a
 
     # ---- roofline of the dominant kernel
     peaks, peak_src = load_peaks()
     dom = "reduce_scatter" if rs_ms >= ag_ms else "all_gather"
     dom_us = 1e3 * max(ag_ms, rs_ms) / K
-    if world == 1:
+    if mode == "local":
         algo_bytes = (n * n + n) * C  # local mode: read n*C + write n^2*C (AG) / read n^2*C + write n*C (RS)
         peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-        roof = {"bound": "hbm", "kernel": ("local_rs_kernel" if dom == "reduce_scatter" else "local_ag_tma_kernel"), "unit": "GB/s",
-                "algorithmic_bytes_per_launch": algo_bytes, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
+        roof = {"bound": "hbm", "kernel": ("local_rs_kernel" if dom == "reduce_scatter" else "local_ag_tma_kernel"),
+                "unit": "GB/s", "algorithmic_bytes_per_launch": algo_bytes,
+                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
+        achieved = algo_bytes / (dom_us * 1e-6) / 1e9
     else:
-        algo_bytes = (n - 1) * C  # per rank, received over NVLink
-        peak = NVLINK_MEASURED_GBS
+        # per GPU: every rank on it receives (n-1)*C over NVLink per launch (ranks sharing a GPU
+        # share its links, so the GPU's ingress is ranks_on_gpu * (n-1) * C minus what stays local)
+        algo_bytes = (n - 1) * C
+        peak = NVLINK_PEER_COPY_GBS
         roof = {"bound": "nvlink", "kernel": f"pat_kernel ({dom})", "unit": "GB/s",
                 "algorithmic_bytes_per_launch": algo_bytes,
-                "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"}
-    achieved = algo_bytes / (dom_us * 1e-6) / 1e9
+                "peak_source": "measured NVLink peer copy 770 GB/s per direction (B200_PROFILING.md)"}
+        achieved = algo_bytes / (dom_us * 1e-6) / 1e9
+        roof["frac_of_nominal_900"] = achieved / NVLINK_NOMINAL_GBS
+        roof["frac_of_sm_push_704"] = achieved / NVLINK_SM_PUSH_GBS
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
                  "launch_us": dom_us})
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath))
-            key = f"{'local' if world == 1 else 'nvlink'}_n{n}_{dom}"
+            key = f"{'local' if mode == 'local' else 'nvlink'}_n{n}_{dom}"
             if key in tr:
                 roof["traffic"] = tr[key]["dram_bytes_per_launch"]
                 roof["traffic_source"] = tr[key].get("source")
@@ -452,18 +593,18 @@ def run_pat(args, rank, world, local):
     # profiles/r01f_costmodel_fit.json) plus the payload on the wire with LL32's one flag word
     # per 28 bytes, at the measured two-way SM-push ceiling (profiles/r01_bidir_probe_g4.txt)
     lat_floor = None
-    if world > 1:
+    if mode != "local":
         plan = comm.plan(0, elems, FLOAT32)
         R = plan["rounds"]
         zero_us = 3.41 + 1.40 * R
-        wire_us = (32.0 / 28.0) * (n - 1) * C / (704.0 * 1e3)
+        wire_us = (32.0 / 28.0) * (n - 1) * C / (NVLINK_SM_PUSH_GBS * 1e3)
         lat_floor = {"rounds": R, "protocol": plan["protocol"], "zero_byte_us": zero_us,
                      "wire_us_at_704gbs": wire_us, "floor_us": zero_us + wire_us, "achieved_us": 1e3 * ag_ms / K,
                      "frac": (zero_us + wire_us) / (1e3 * ag_ms / K),
                      "source": "profiles/r01f_costmodel_fit.json (LL a, b), profiles/r01_bidir_probe_g4.txt"}
 
     clk = clocks.summary()
-    if world > 1:
+    if dist is not None:
         allc = [None] * world
         dist.all_gather_object(allc, clk)
         clk = {"sm_mhz": statistics.median([c["sm_mhz"] for c in allc if c["sm_mhz"]] or [0]),
@@ -472,45 +613,54 @@ def run_pat(args, rank, world, local):
 
     plan_ag = comm.plan(0, elems, FLOAT32)
     plan_rs = comm.plan(1, elems, FLOAT32)
+    pool_info = comm.pool_info()
     out = None
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
+        if n_gpus == 1 and not args.no_cpu_baseline:
             try:
                 sec, steps, thr = reference_time(n, C, args.cpu_seconds)
                 cpu = {"value": busbw_gbs(n, C, sec), "unit": "GB/s", "cores": thr, "kind": "reference",
                        "ms_per_step": sec * 1e3,
                        "sample": f"{steps} steps of the reference executor (oracle/_ref = /root/reference/proj/src "
-                                 f"compiled), n={n}, {C} B/rank, run_allgather(int64)+run_reduce_scatter(f64), "
-                                 f"ExecMode::Parallel x{thr} threads, {args.cpu_seconds:.0f} s budget"}
+                                 f"compiled), n={n}, {C} B/rank, run_allgather(int64)+run_reduce_scatter(f64) on "
+                                 f"payloads built once, ExecMode::Parallel x{thr} threads, {args.cpu_seconds:.0f} s budget"}
             except Exception as e:  # the reference library must be built in-tree
                 cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+        launches_per_gpu = 2 * K
         out = {
             "metric": "PAT all-gather + reduce-scatter(sum) aggregate bus bandwidth, 1 MiB fp32 per rank",
-            "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "value": value, "unit": "GB/s", "n_gpus": n_gpus, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.rand on device)",
-            "config": {"workload": "BASELINE configs[0]: PAT AG + RS(sum), 1 MiB fp32 per rank",
-                       "nranks": n, "placement": placement, "chunk_bytes": C, "trees": plan_ag["trees"],
-                       "rounds": plan_ag["rounds"], "l2": f"inputs larger than L2: {S} rotating buffer sets, {S * step_bytes / 2**20:.0f} MiB total",
-                       "timing": "CUDA events around CUDA-graph replays of exactly K steps (captured C-ABI calls)",
+            "config": {"workload": ("BASELINE configs[0]: PAT AG + RS(sum), n=8, 1 MiB fp32 per rank" if n == 8 else
+                                    f"BASELINE configs[0] shape at n={n}: PAT AG + RS(sum), 1 MiB fp32 per rank"),
+                       "nranks": n, "mode": mode, "placement": desc, "chunk_bytes": C, "trees": plan_ag["trees"],
+                       "rounds": plan_ag["rounds"],
+                       "l2": f"inputs larger than L2: {S} rotating buffer sets, {S * step_bytes / 2**20:.0f} MiB per GPU",
+                       "timing": "CUDA events around CUDA-graph replays of exactly K steps (captured C-ABI calls), "
+                                 "max over devices and ranks",
                        "plan_allgather": plan_ag, "plan_reduce_scatter": plan_rs},
             "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K,
                            "timing": "graph of K back-to-back calls per collective"},
             "latency_us_eager": dict(eager_us, timing="eager C-ABI calls, CUDA events per call"),
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host; double-buffered: step k+1 uploads while step k downloads (PCIe full duplex)"},
-            "gpu_launches": 2 * K,
+                    "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host; "
+                            "double-buffered: step k+1 uploads while step k downloads (PCIe full duplex)"},
+            "gpu_launches": launches_per_gpu * n_gpus,
+            "gpu_launches_per_gpu": launches_per_gpu,
             "roofline": roof,
             "latency_floor": lat_floor,
             "cpu_baseline": cpu,
             "clocks": clk,
+            "staging": pool_info,
         }
         if nccl:
             out["nccl_ring"] = nccl
+        out.update(extras)
     comm.destroy()
-    if world > 1:
+    if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return out
@@ -519,27 +669,27 @@ def run_pat(args, rank, world, local):
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    n = world if world > 1 else (args.ranks or 8)
+    n = world if world > 1 else (args.ranks or (8 if args.gpus == 1 else args.gpus))
     C = args.chunk_bytes
     # W warm-up steps (at most 3: each is the whole workload, ~90 ms), then exactly K timed steps
     # unless K steps would exceed ~2 minutes of host time: then as many as fit, reported in
     # "steps" and in the sample description
-    for _ in range(min(args.warmup, 3)):
-        reference_time(n, C, 0.0, max_steps=1)
-    est, _, _ = reference_time(n, C, 0.0, max_steps=1)
+    est, _, _ = reference_time(n, C, 0.0, max_steps=1, warmup=min(args.warmup, 3))
     timed = max(1, min(args.steps, int(120.0 / max(est, 1e-6))))
-    sec, steps, thr = reference_time(n, C, 1e9, max_steps=timed)
+    sec, steps, thr = reference_time(n, C, 1e9, max_steps=timed, warmup=0)
     budget = sec * steps
     value = busbw_gbs(n, C, sec)
     return {"impl": "reference", "metric": "PAT all-gather + reduce-scatter(sum) aggregate bus bandwidth, 1 MiB fp32 per rank",
-            "value": value, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "value": value, "unit": "GB/s", "n_gpus": world if world > 1 else args.gpus, "steps": steps,
+            "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "int64 AG + f64 RS (equal bytes)", "data": "synthetic (reference mt19937_64 payloads)",
-            "config": {"workload": "BASELINE configs[0]: PAT AG + RS(sum), 1 MiB per rank", "nranks": n,
-                       "chunk_bytes": C, "placement": "in-process ranks on host cores"},
+            "config": {"workload": ("BASELINE configs[0]: PAT AG + RS(sum), n=8, 1 MiB per rank" if n == 8 else
+                                    f"BASELINE configs[0] shape at n={n}: PAT AG + RS(sum), 1 MiB per rank"),
+                       "nranks": n, "chunk_bytes": C, "placement": "in-process ranks on host cores"},
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": thr, "kind": "reference",
                              "sample": f"{steps} timed steps (of --steps {args.steps}) of the whole workload, "
-                                       f"ExecMode::Parallel x{thr} threads, {budget:.1f} s"},
+                                       f"payloads built once (ref_prepare), ExecMode::Parallel x{thr} threads, {budget:.1f} s"},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -550,11 +700,20 @@ def main():
     os.dup2(2, 1)
     sys.stdout = os.fdopen(os.dup(2), "w")
     rank, world, local = dist_env()
-    if args.impl == "reference":
-        out = run_reference(args, rank, world)
-    else:
-        out = run_pat(args, rank, world, local)
+    try:
+        if args.impl == "reference":
+            out = run_reference(args, rank, world)
+        else:
+            out = run_pat(args, rank, world, local)
+    except SystemExit as e:
+        if isinstance(e.code, str):
+            print(e.code, file=sys.stderr, flush=True)
+            os._exit(2)
+        raise
     if rank == 0 and out is not None:
+        if args.impl == "pat" and out["n_gpus"] != args.gpus:  # never report a different GPU count
+            print(f"bench.py: measured n_gpus={out['n_gpus']} != --gpus {args.gpus}", file=sys.stderr)
+            os._exit(2)
         with os.fdopen(real_stdout, "w") as f:
             f.write(json.dumps(out) + "\n")
 

@@ -103,7 +103,10 @@ typedef enum { patAlgoRing = 0, patAlgoBruckNearest = 1, patAlgoBruckFarthest = 
    is set), then SIMPLE — except reduce-scatter
    below 128 MiB, which PULLs where possible (measured, profiles/r01_sp_simple_vs_pull.jsonl). */
 typedef enum { patProtoAuto = 0, patProtoLL = 1, patProtoSimple = 2, patProtoPull = 3,
-               patProtoLL32 = 5 } patProtocol_t;
+               patProtoLL32 = 5,
+               patProtoFused = 6  /* reported by patCommPlan only: every rank on one device, the
+                                     fused single-device executor runs the call (no transport) */
+} patProtocol_t;
 
 typedef struct {
   size_t size;              /* sizeof(patConfig_t) */
@@ -128,7 +131,7 @@ typedef struct {
 
 /* Plan the library would launch for one call (introspection / benchmarks). */
 typedef struct {
-  int protocol;             /* patProtocol_t actually chosen */
+  int protocol;             /* patProtocol_t actually chosen (patProtoFused: no transport) */
   int trees;
   int rounds;               /* PAT rounds (= sync steps) */
   int channels;             /* CTAs per rank */
@@ -141,7 +144,26 @@ typedef struct {
   int64_t bytes_sent_per_rank;   /* (n-1) * chunk bytes */
   int peak_intermediate_slots;   /* reference accounting (simulate.hpp:50) */
   double predicted_us;           /* the calibrated alpha-beta model's time for this call (comm.cpp) */
+  int staged_slots_per_step;     /* inbox slots a pipeline step occupies at the receiver: n-1 landing
+                                    slots (LL, LL32, SIMPLE), the schedule's accumulators (PULL
+                                    reduce-scatter), 0 (direct / PULL all-gather, fused) */
+  int depth;                     /* inbox buffers per channel for this protocol */
+  size_t staging_bytes_used;     /* bytes of the inbox this call touches per rank:
+                                    channels x depth x staged_slots_per_step x slot stride */
 } patPlanInfo_t;
+
+/* Memory the communicator holds (this process). */
+typedef struct {
+  size_t pool_bytes_per_rank;    /* flags + every protocol region of one rank's inbox pool */
+  size_t allocated_bytes;        /* inbox pool bytes allocated by this process (all its ranks);
+                                    0 while a one-device communicator only ran fused calls */
+  int pools_allocated;           /* 1 once this process's pools exist */
+  int depth;                     /* SIMPLE / PULL inbox buffers per channel */
+  int depth_poll;                /* LL / LL32 inbox buffers per channel */
+  int region_channels[4];        /* SIMPLE(+PULL), LL, LL32, (unused) */
+  size_t region_bytes[4];
+  size_t slot_bytes[4];          /* slot size per region (SIMPLE slice, LL slot, LL32 slot) */
+} patMemInfo_t;
 
 /* ExecStats (simulate.hpp:43-53) computed from a schedule; chunk_bytes as given. */
 typedef struct {
@@ -187,6 +209,7 @@ patResult_t patCommTraceRead(patComm_t comm, int group, void* host, size_t cap, 
 patResult_t patCommGetAsyncError(patComm_t comm, patResult_t* async_error);
 patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDataType_t dtype,
                         patPlanInfo_t* info);
+patResult_t patCommMemInfo(patComm_t comm, patMemInfo_t* info);
 
 /* ---- collectives (asynchronous on the given streams) ----------------------------------
  * Array arguments are indexed by local rank (patCommLocalRanks order): one entry per rank

@@ -145,6 +145,11 @@ def ref():
         R.ref_round_count_formula.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         R.ref_oracle_sweep.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, I64P]
         R.ref_last_error.restype = ctypes.c_char_p
+        R.ref_prepare.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int]
+        R.ref_prepare.restype = ctypes.c_void_p
+        R.ref_run_prepared.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        R.ref_free_prepared.argtypes = [ctypes.c_void_p]
+        R.ref_free_prepared.restype = None
         _ref = R
     return _ref
 

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -283,6 +284,45 @@ int64_t ref_trace_csv(const int32_t* s, int64_t len, int64_t chunk_bytes, char* 
     return -1;
   }
 }
+
+// Prepared workload for timing the reference's own CPU path (bench.py --impl reference and
+// cpu_baseline): the schedules and the seeded Payload<T>s (oracle.cpp:92-112) are built ONCE
+// here, so a timed step is exactly the reference's run_allgather(int64) +
+// run_reduce_scatter(double, FloatSum) — no marshalling from flat arrays, no copy-out (the
+// returned CollectiveResult is the reference's own allocation and is dropped).
+struct RefWorkload {
+  RelativeSchedule ag, rs;
+  Payload<std::int64_t> ag_in;
+  Payload<double> rs_in;
+  RunOptions opt;
+};
+
+void* ref_prepare(int n, int trees, int64_t elems, int mode, int threads) {
+  RefWorkload* w = nullptr;
+  guarded([&] {
+    auto p = std::make_unique<RefWorkload>();
+    p->ag = pat_allgather(n, trees);
+    p->rs = pat_reduce_scatter(n, trees);
+    p->ag_in = random_allgather_payload(n, static_cast<int>(elems), 0);
+    p->rs_in = random_reduce_scatter_payload_f64(n, static_cast<int>(elems), 1);
+    p->opt = options_of(mode, threads);
+    w = p.release();
+    return 0;
+  });
+  return w;
+}
+
+// which: bit 0 = all-gather, bit 1 = reduce-scatter
+int ref_run_prepared(void* h, int which) {
+  return guarded([&] {
+    auto* w = static_cast<RefWorkload*>(h);
+    if (which & 1) (void)run_allgather(w->ag, w->ag_in, w->opt);
+    if (which & 2) (void)run_reduce_scatter(w->rs, w->rs_in, ReduceOp::FloatSum, w->opt);
+    return 0;
+  });
+}
+
+void ref_free_prepared(void* h) { delete static_cast<RefWorkload*>(h); }
 
 // Acceptance-style sweep straight from the reference (oracle.cpp:237-282), for the record.
 int ref_oracle_sweep(int n_min, int n_max, int elems, int64_t* mismatches) {

@@ -28,7 +28,8 @@ RESULTS = {
 # datatypes (ncclDataType_t numbering) and ops (ncclRedOp_t numbering)
 INT8, UINT8, INT32, UINT32, INT64, UINT64, FLOAT16, FLOAT32, FLOAT64, BFLOAT16 = range(10)
 SUM, PROD, MAX, MIN = range(4)
-PROTO_AUTO, PROTO_LL, PROTO_SIMPLE, PROTO_PULL, PROTO_LL32 = 0, 1, 2, 3, 5
+PROTO_AUTO, PROTO_LL, PROTO_SIMPLE, PROTO_PULL, PROTO_LL32, PROTO_FUSED = 0, 1, 2, 3, 5, 6
+PROTO_NAMES = {PROTO_LL: "LL", PROTO_SIMPLE: "SIMPLE", PROTO_PULL: "PULL", PROTO_LL32: "LL32", PROTO_FUSED: "FUSED"}
 DTYPE_SIZE = {INT8: 1, UINT8: 1, INT32: 4, UINT32: 4, INT64: 8, UINT64: 8, FLOAT16: 2,
               FLOAT32: 4, FLOAT64: 8, BFLOAT16: 2}
 
@@ -76,10 +77,35 @@ class PlanInfo(ctypes.Structure):
         ("bytes_sent_per_rank", ctypes.c_int64),
         ("peak_intermediate_slots", ctypes.c_int),
         ("predicted_us", ctypes.c_double),
+        ("staged_slots_per_step", ctypes.c_int),
+        ("depth", ctypes.c_int),
+        ("staging_bytes_used", ctypes.c_size_t),
     ]
 
     def as_dict(self) -> dict:
-        return {f: getattr(self, f) for f, _ in self._fields_}
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["protocol_name"] = PROTO_NAMES.get(self.protocol, str(self.protocol))
+        return d
+
+
+class MemInfo(ctypes.Structure):
+    _fields_ = [
+        ("pool_bytes_per_rank", ctypes.c_size_t),
+        ("allocated_bytes", ctypes.c_size_t),
+        ("pools_allocated", ctypes.c_int),
+        ("depth", ctypes.c_int),
+        ("depth_poll", ctypes.c_int),
+        ("region_channels", ctypes.c_int * 4),
+        ("region_bytes", ctypes.c_size_t * 4),
+        ("slot_bytes", ctypes.c_size_t * 4),
+    ]
+
+    def as_dict(self) -> dict:
+        names = ("simple_pull", "ll", "ll32")
+        return {"pool_bytes_per_rank": self.pool_bytes_per_rank, "allocated_bytes": self.allocated_bytes,
+                "pools_allocated": bool(self.pools_allocated), "depth": self.depth, "depth_poll": self.depth_poll,
+                "regions": {names[i]: {"channels": self.region_channels[i], "bytes": self.region_bytes[i],
+                                       "slot_bytes": self.slot_bytes[i]} for i in range(3)}}
 
 
 class ExecStats(ctypes.Structure):
@@ -102,6 +128,7 @@ SYMBOLS = [
     "patReduceScatter", "patAllGatherSchedule", "patReduceScatterSchedule", "patScheduleBuild",
     "patScheduleMirror", "patScheduleValidate", "patScheduleStats", "patScheduleTraceCsv",
     "patMaxTrees", "patTreesFromBuffer", "patPatBufferSlots", "patRoundCountFormula", "patCommTraceRead",
+    "patCommMemInfo",
 ]
 
 _lib = None
@@ -148,6 +175,7 @@ def lib() -> ctypes.CDLL:
         L.patPatBufferSlots.argtypes = [ctypes.c_int, ctypes.c_int, IP]
         L.patRoundCountFormula.argtypes = [ctypes.c_int, ctypes.c_int, IP]
         L.patCommTraceRead.argtypes = [VP, ctypes.c_int, VP, ctypes.c_size_t, SZP, IP, IP]
+        L.patCommMemInfo.argtypes = [VP, ctypes.POINTER(MemInfo)]
         _lib = L
     return _lib
 

@@ -205,6 +205,12 @@ class PatComm:
                                 ctypes.byref(info)), "patCommPlan")
         return info.as_dict()
 
+    def pool_info(self) -> dict:
+        """Inbox pool layout and what this process has allocated (patCommMemInfo)."""
+        info = _lib.MemInfo()
+        check(lib().patCommMemInfo(self._h, ctypes.byref(info)), "patCommMemInfo")
+        return info.as_dict()
+
     def trace(self, group: int = 0):
         """Device event trace of the last transport launch (PAT_TRACE=<entries> at init).
         Returns a numpy array [ctas, 2 roles, entries, 2] of (globaltimer ns, code)."""

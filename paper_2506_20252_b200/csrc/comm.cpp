@@ -35,6 +35,9 @@ namespace pat {
 using KernelFn = void (*)(const KPlan);
 cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream);
 cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out);
+cudaError_t init_pool_state(char* pool, int64_t ll_off, int64_t ll_bytes, int64_t ll32_off, int64_t ll32_bytes,
+                            uint64_t start, cudaStream_t stream);
+cudaError_t fill_u64(uint64_t* p, int64_t n, uint64_t v, cudaStream_t stream);
 cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize, int64_t chunk_bytes,
                          const char* const* send_by_rank, char* const* recv_by_rank, int sm_count,
                          cudaStream_t stream);
@@ -48,7 +51,8 @@ namespace {
 constexpr size_t kFlagBytes = sizeof(uint64_t) * kMaxChannels * kFlagWords;  // 8 KiB
 constexpr uint32_t kMagic = 0x50415442;                                       // "PATB"
 constexpr size_t kDefaultPoolBytes = 512ull << 20;  // inbox pool budget per rank (all channels)
-constexpr size_t kMinSlice = 64 << 10, kMaxSlice = 256 << 10;
+constexpr size_t kMaxSlice = 256 << 10;
+constexpr size_t kCapMinSlice = 32 << 10;  // smallest bulk slice a staging cap shrinks to before channels
 constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
 // LL32 vs bulk is chosen by the calibrated cost model below (choose_slicing).
 constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
@@ -85,9 +89,9 @@ struct DevGroup {
 
 struct Handle {
   uint32_t magic, version;
-  int32_t nranks, rank, device, channels;
+  int32_t nranks, rank, device, channels, pid, pad;
   uint64_t pool_bytes, slot_bytes;
-  int32_t pid, pad;
+  uint64_t config_hash;  // every resolved setting that decides a call's protocol, slicing or layout
   cudaIpcMemHandle_t ipc;
 };
 static_assert(sizeof(Handle) <= PAT_HANDLE_BYTES, "handle too large");
@@ -114,9 +118,20 @@ struct patComm {
   size_t ll_slot_bytes = 0;                // LL inbox slot (own region, common_init)
   size_t ll32_slot_bytes = 0;              // LL32 inbox slot (own region)
   size_t region_off[kNumProtoSlots] = {};  // inbox region of each protocol within a pool
+  size_t region_bytes[kNumProtoSlots] = {};
+  int region_channels[kNumProtoSlots] = {};  // channels each protocol region is laid out for
+  int depth_poll = 0;                        // inbox buffers per channel of the LL / LL32 regions
+  // Pools are allocated lazily for one-process communicators: a communicator whose ranks all
+  // sit on one device runs PAT calls through the fused executor (local.cu), which needs no
+  // inbox, so its pools appear only if a transport launch ever happens.
+  bool pools_ready = false;
+  size_t pools_allocated = 0;  // bytes of inbox pool this process allocated (all its ranks)
   int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
   int skew = 1;            // SIMPLE / PULL sender skew distance (PAT_SKEW; 0 = rounds in order)
+  uint64_t epoch_mask = (1ull << 31) - 1;  // LL / LL32 flag epochs (PAT_EPOCH_SHIFT, tests)
+  uint64_t iter_start = 0;                 // first pipeline step of every channel (PAT_ITER_START, tests)
   int channels = 0;
+  uint64_t config_hash = 0;  // config_fingerprint(): must be equal on every process of a comm
   int* err_host = nullptr;
   int* err_dev = nullptr;
   std::map<std::vector<int32_t>, Compiled> compiled;  // keyed by schedule encoding
@@ -178,16 +193,80 @@ size_t dtype_size(int dt) {
   }
 }
 
-// Bytes of an explicit staging budget (patConfig_t::staging_bytes) per slot triple (one
-// SIMPLE/PULL slot + one LL slot + one LL32 slot for each of channels * depth * (n-1) slots).
-size_t budget_per_slot(const patConfig_t& c, int n) {
-  const size_t slots = static_cast<size_t>(c.max_channels) * c.depth * std::max(n - 1, 1);
-  return c.staging_bytes > 8192 ? (c.staging_bytes - 8192) / slots : 0;
+// Pool layout. Each protocol has its own inbox region, laid out [channel][buffer][slot]:
+//   SIMPLE  channels x depth x (n-1) landing slots x slice     (one slot per arrival of a step)
+//   PULL    the SIMPLE region re-cut as channels x depth x A x pslice, A = accumulators of the
+//           schedule (internal nodes of the PAT reduction tree: 3 at n = 8) — the reference's
+//           intermediate slots; leaves are read straight from the peers' sendbufs
+//   LL      ll_channels x depth x (n-1) x 32 KiB              (16-byte lines, half payload)
+//   LL32    channels x depth x (n-1) x 32 KiB                 (32-byte lines, 28/32 payload)
+// The polling protocols poll their lines, so each has its own memory: a stale payload word left
+// by another protocol could otherwise pass for a flag. Without a cap the bulk region takes
+// kDefaultPoolBytes; under patConfig_t::staging_bytes (the whole pool, flags aside) the polling
+// regions get at most a quarter and the bulk region the rest, with fewer channels rather than
+// slices below kCapMinSlice (large slices amortise the per-round fence and flag).
+constexpr int kLLChannels = 32;  // LL runs to 256 KiB chunks: 32 x 16 KiB payload per step covers them
+struct Layout {
+  int ch[kNumProtoSlots] = {};
+  size_t slot[kNumProtoSlots] = {};
+  size_t bytes[kNumProtoSlots] = {};
+};
+
+// Channels and slot size for a region of `budget` bytes: `slot_pref` per slot if it fits with
+// `ch_max` channels, else smaller slots down to `slot_min`, then fewer channels.
+void fit_region(size_t budget, int ch_max, size_t per_ch_slots, size_t slot_pref, size_t slot_min, size_t align,
+                int* ch, size_t* slot) {
+  size_t s = budget / (static_cast<size_t>(ch_max) * per_ch_slots);
+  s = std::min(s, slot_pref) / align * align;
+  if (s >= slot_min) {
+    *ch = ch_max;
+    *slot = s;
+    return;
+  }
+  const size_t c = budget / (per_ch_slots * slot_min);
+  if (c >= 1) {
+    *ch = static_cast<int>(std::min<size_t>(c, ch_max));
+    *slot = std::min(slot_pref, budget / (static_cast<size_t>(*ch) * per_ch_slots)) / align * align;
+    return;
+  }
+  *ch = 1;
+  *slot = std::max(align, budget / per_ch_slots / align * align);
 }
-// A polling protocol's slot under a budget of b bytes per triple: at most a sixth of it, so a
-// tight budget goes to the bulk slices that carry the large calls (ZeRO-3 shape at a 64 MiB
-// cap: 19 -> 38 KiB slices).
-size_t polling_slot(size_t def, size_t b) { return std::max<size_t>(1024, std::min(def, b / 6) & ~size_t(1023)); }
+
+Layout plan_layout(const patConfig_t& c, int n, int depth_poll, bool explicit_slice) {
+  Layout L;
+  const size_t slots = static_cast<size_t>(std::max(n - 1, 1));
+  const size_t ll_pref = kLLSlotBytes, ll32_pref = ll32_slot_default();
+  const int ch_ll = std::min(c.max_channels, kLLChannels);
+  const size_t poll_default = static_cast<size_t>(ch_ll) * depth_poll * slots * ll_pref +
+                              static_cast<size_t>(c.max_channels) * depth_poll * slots * ll32_pref;
+  size_t bulk_budget = kDefaultPoolBytes, poll_budget = poll_default;
+  if (c.staging_bytes != 0) {
+    const size_t B = c.staging_bytes > kFlagBytes + 3 * 4096 ? c.staging_bytes - kFlagBytes - 3 * 4096 : 0;
+    poll_budget = std::min(poll_default, B / 4);
+    bulk_budget = B - poll_budget;
+  }
+  // LL gets a quarter of the polling budget, LL32 the rest (LL32 carries up to 48 MiB per call)
+  fit_region(poll_budget / 4, ch_ll, depth_poll * slots, ll_pref, 1024, 1024, &L.ch[kProtoLL], &L.slot[kProtoLL]);
+  fit_region(poll_budget - poll_budget / 4, c.max_channels, depth_poll * slots, ll32_pref, 1024, 1024,
+             &L.ch[kProtoLL32], &L.slot[kProtoLL32]);
+  if (explicit_slice && c.staging_bytes == 0) {
+    L.ch[kProtoSimple] = c.max_channels;
+    L.slot[kProtoSimple] = c.slice_bytes;
+  } else {
+    // under a cap, slices shrink to kCapMinSlice before channels are dropped (PAT_MIN_SLICE)
+    long long ms = 0;
+    const size_t min_slice = env_int("PAT_MIN_SLICE", &ms) && ms >= 1024 ? static_cast<size_t>(ms) : kCapMinSlice;
+    fit_region(bulk_budget, c.max_channels, c.depth * slots, kMaxSlice, std::min(min_slice, kMaxSlice), 128,
+               &L.ch[kProtoSimple], &L.slot[kProtoSimple]);
+  }
+  L.ch[kProtoPull] = L.ch[kProtoSimple];
+  L.slot[kProtoPull] = L.slot[kProtoSimple];  // re-cut per call by the schedule's accumulator count
+  L.bytes[kProtoSimple] = L.bytes[kProtoPull] = static_cast<size_t>(L.ch[kProtoSimple]) * c.depth * slots * L.slot[kProtoSimple];
+  for (int p : {kProtoLL, kProtoLL32})
+    L.bytes[p] = static_cast<size_t>(L.ch[p]) * depth_poll * slots * L.slot[p];
+  return L;
+}
 
 void fill_defaults(patConfig_t* c, int n) {
   long long v;
@@ -199,25 +278,11 @@ void fill_defaults(patConfig_t* c, int n) {
   // at least 2: the polling protocols publish a call's last done(step) only when the next call
   // starts (transport.cuh), which a first step waiting for step base - depth + 1 must not need
   c->depth = std::min(std::max(c->depth, 2), 16);
-  const size_t slots = static_cast<size_t>(c->max_channels) * c->depth * std::max(n - 1, 1);
-  if (c->slice_bytes == 0) {
-    // large slices amortise the per-round fence + flag (measured: 85 KiB -> 256 KiB slices
-    // lift n=4 all-gather from ~460 to ~660 GB/s); the pool stays within kDefaultPoolBytes
-    c->slice_bytes = env_int("PAT_SLICE_BYTES", &v)
-                         ? (size_t)v
-                         : std::min(kMaxSlice, std::max(kMinSlice, kDefaultPoolBytes / slots));
-  }
-  c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(15));
-  if (c->staging_bytes != 0) {
-    // explicit budget for the whole pool (flags aside): channels * depth * (n-1) slot triples,
-    // one SIMPLE/PULL slot plus the LL and LL32 slots (polling_slot)
-    const size_t b = budget_per_slot(*c, n);
-    const size_t ll = polling_slot(kLLSlotBytes, b) + polling_slot(ll32_slot_default(), b);
-    size_t s = b > ll ? b - ll : 0;
-    s &= ~size_t(127);
-    if (s < 256) s = 256;
-    c->slice_bytes = s;
-  }
+  // SIMPLE slice: explicit (config or PAT_SLICE_BYTES), else sized from the pool budget by
+  // plan_layout (large slices amortise the per-round fence + flag: 85 KiB -> 256 KiB slices
+  // lifted n=4 all-gather from ~460 to ~660 GB/s)
+  if (c->slice_bytes == 0 && env_int("PAT_SLICE_BYTES", &v) && v > 0) c->slice_bytes = (size_t)v;
+  if (c->slice_bytes) c->slice_bytes = std::max<size_t>(256, c->slice_bytes & ~size_t(127));
   if (c->ll_threshold == 0 && env_int("PAT_LL_THRESHOLD", &v)) c->ll_threshold = (size_t)v;  // 0: cost model
   if (c->timeout_ms <= 0) c->timeout_ms = env_int("PAT_TIMEOUT_MS", &v) ? (int)v : kDefaultTimeoutMs;
   if (c->protocol == patProtoAuto && env_int("PAT_PROTOCOL", &v)) c->protocol = (int)v;
@@ -366,6 +431,23 @@ patResult_t compile_schedule(patComm* comm, const Schedule& given, Compiled** ou
       }
     }
   }
+  // PULL staging holds accumulators only (fold of a forwarded offset's arrivals, finalised with
+  // the own contribution): number them compactly, one slot per forwarded offset with arrivals
+  // (the internal nodes of the reduction tree, the reference's intermediate slots). Ids are not
+  // reused within a step: a reader may still be pulling an accumulator while its owner opens the
+  // next one, and slots return only with done(step).
+  {
+    int8_t id_of[kMaxSlots];
+    for (int j = 0; j < kMaxSlots; ++j) id_of[j] = -1;
+    int na = 0;
+    for (int j = 0; j < p.nslots; ++j) {
+      const int d = p.pull_dst[j];
+      if (d < 0) continue;
+      if (id_of[d] < 0) id_of[d] = static_cast<int8_t>(na++);
+      p.pull_dst[j] = id_of[d];
+    }
+    p.pull_nacc = static_cast<int8_t>(na);
+  }
   for (int t = 0; t < p.nrounds; ++t) {
     bool seen = false;
     for (int k = 0; k < p.npeers; ++k) seen |= p.peers[k] == p.rounds[t].peer;
@@ -429,9 +511,19 @@ double predict_us(int proto, int n, int rounds, int64_t chunk_bytes, int iters) 
 // 8-byte reductions.
 int64_t ll32_group(int kind, int64_t es) { return kind == kRS && es == 8 ? 768 : 896; }
 
-Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int channels, int64_t es) {
+// PULL staging slot for a schedule with `nacc` accumulators per step: the bulk region re-cut
+// into region_channels x depth x nacc slots (at most kMaxSlice x 4 each)
+int64_t pull_slot_bytes(const patComm* comm, int nacc) {
+  const int64_t per = static_cast<int64_t>(comm->region_bytes[kProtoPull]) /
+                      (int64_t{comm->region_channels[kProtoPull]} * comm->cfg.depth * std::max(nacc, 1));
+  return std::min<int64_t>(per, 4 * kMaxSlice) & ~int64_t(127);
+}
+
+Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int max_channels, int64_t es,
+              int nacc) {
   Slicing s{};
   s.proto = proto;
+  const int channels = std::max(1, std::min(comm->region_channels[proto], max_channels));
   int64_t cap = static_cast<int64_t>(comm->slot_bytes);
   int64_t minslice = 16 << 10;
   if (proto == kProtoLL) {
@@ -440,8 +532,10 @@ Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int
   } else if (proto == kProtoLL32) {
     cap = static_cast<int64_t>(comm->ll32_slot_bytes / 1024) * ll32_group(kind, es);
     minslice = ll32_group(kind, es);
+  } else if (proto == kProtoPull) {
+    // RS stages only accumulators; AG pull stages nothing
+    cap = kind == kAG ? std::max<int64_t>(cap, comm->pull_slice) : pull_slot_bytes(comm, nacc);
   }
-  if (proto == kProtoPull && kind == kAG) cap = std::max<int64_t>(cap, comm->pull_slice);  // AG pull stages nothing
   int64_t per = (chunk_bytes + channels - 1) / channels;
   per = (per + 15) & ~int64_t(15);
   per = std::max<int64_t>(per, std::min<int64_t>(minslice, cap));
@@ -459,7 +553,7 @@ Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int
 }
 
 Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int max_channels, bool pull_ok,
-                       int rounds, int64_t es) {
+                       int rounds, int64_t es, int nacc) {
   const int channels = std::max(1, std::min(comm->channels, max_channels));
   int proto = comm->cfg.protocol;
   if (proto == patProtoAuto) {
@@ -474,7 +568,7 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
       for (const int cand : std::array<int, 3>{kProtoLL, kProtoLL32, bulk}) {
         if (cand == kProtoLL32 && static_cast<int64_t>(comm->n - 1) * chunk_bytes > kLL32MaxPayload) continue;
         const double t = predict_us(cand, comm->n, rounds, chunk_bytes,
-                                    shape(comm, cand, kind, chunk_bytes, channels, es).iters);
+                                    shape(comm, cand, kind, chunk_bytes, channels, es, nacc).iters);
         if (cand == kProtoLL || t < best) {
           best = t;
           proto = cand;
@@ -483,7 +577,7 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
     }
   }
   if (proto == kProtoPull && !pull_ok) proto = kProtoSimple;
-  return shape(comm, proto, kind, chunk_bytes, channels, es);
+  return shape(comm, proto, kind, chunk_bytes, channels, es, nacc);
 }
 
 // Channels per rank such that every device's launch stays co-resident (cooperative launch).
@@ -509,6 +603,33 @@ patResult_t alloc_pool(patComm* comm, int device, char** pool) {
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaMalloc(pool, comm->pool_bytes));
   CUDA_TRY(cudaMemset(*pool, 0, comm->pool_bytes));
+  comm->pools_allocated += comm->pool_bytes;
+  return patSuccess;
+}
+
+// One-process communicators allocate every rank's pool on the first transport launch. A
+// launch may be under stream capture: the allocation is not a stream operation, so it runs in
+// relaxed capture mode for this thread and zeroes the pools synchronously before returning.
+patResult_t ensure_pools(patComm* comm) {
+  if (comm->pools_ready) return patSuccess;
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  CUDA_TRY(cudaThreadExchangeStreamCaptureMode(&mode));
+  patResult_t rc = patSuccess;
+  for (size_t l = comm->owned_pool.size(); l < comm->ldevs.size() && rc == patSuccess; ++l) {
+    char* pool = nullptr;
+    rc = alloc_pool(comm, comm->ldevs[l], &pool);
+    if (rc == patSuccess) comm->owned_pool.push_back(pool);
+  }
+  if (rc == patSuccess)
+    for (size_t l = 0; l < comm->ldevs.size(); ++l) {  // the memsets ran on the legacy stream
+      cudaSetDevice(comm->ldevs[l]);
+      if (cudaDeviceSynchronize() != cudaSuccess) rc = patUnhandledCudaError;
+    }
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (rc != patSuccess) return rc;
+  for (DevGroup& g : comm->groups)
+    for (int r = 0; r < comm->n; ++r) g.pool_view[r] = comm->owned_pool[r];
+  comm->pools_ready = true;
   return patSuccess;
 }
 
@@ -527,28 +648,30 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
     return patInvalidArgument;
   comm->cfg = c;
   comm->channels = c.max_channels;
-  comm->slot_bytes = c.slice_bytes;
   {
     long long v = 0;
     comm->pull_slice = env_int("PAT_PULL_SLICE", &v) && v >= 256 ? (v & ~15LL) : (512 << 10);
     comm->skew = env_int("PAT_SKEW", &v) ? static_cast<int>(std::max(0LL, v)) : 1;
+    // the polling protocols need depth >= 2 (deferred credit, transport.cuh); they do not skew
+    comm->depth_poll = env_int("PAT_POLL_DEPTH", &v) ? static_cast<int>(v) : c.depth;
+    comm->depth_poll = std::min(std::max(comm->depth_poll, 2), c.depth);
+    if (env_int("PAT_EPOCH_SHIFT", &v) && v >= 3 && v <= 31 && (1ll << v) > 2 * comm->depth_poll)
+      comm->epoch_mask = (1ull << v) - 1;
+    if (env_int("PAT_ITER_START", &v) && v > 0) comm->iter_start = static_cast<uint64_t>(v);
   }
-  const size_t slots = static_cast<size_t>(std::max(nranks - 1, 1));
-  // Inbox regions: SIMPLE/PULL slots, then LL slots. LL polls its lines, so it gets its own
-  // memory: a stale payload word left by a bulk protocol could otherwise pass for a flag.
-  size_t llb = kLLSlotBytes, ll32b = ll32_slot_default();
-  if (c.staging_bytes != 0) {  // as fill_defaults sized the bulk slots
-    llb = polling_slot(llb, budget_per_slot(c, nranks));
-    ll32b = polling_slot(ll32b, budget_per_slot(c, nranks));
+  const Layout lay = plan_layout(c, nranks, comm->depth_poll, c.slice_bytes != 0);
+  for (int p = 0; p < kNumProtoSlots; ++p) {
+    comm->region_channels[p] = lay.ch[p];
+    comm->region_bytes[p] = lay.bytes[p];
   }
-  comm->ll_slot_bytes = std::max<size_t>(1024, std::min<size_t>(llb, comm->slot_bytes) & ~size_t(1023));
-  comm->ll32_slot_bytes = std::max<size_t>(1024, std::min<size_t>(ll32b, comm->slot_bytes) & ~size_t(1023));
-  const size_t nslots = static_cast<size_t>(comm->channels) * c.depth * slots;
+  comm->slot_bytes = lay.slot[kProtoSimple];
+  comm->ll_slot_bytes = lay.slot[kProtoLL];
+  comm->ll32_slot_bytes = lay.slot[kProtoLL32];
   auto align = [](size_t x) { return (x + 4095) & ~size_t(4095); };
   comm->region_off[kProtoSimple] = comm->region_off[kProtoPull] = 0;
-  comm->region_off[kProtoLL] = align(nslots * comm->slot_bytes);
-  comm->region_off[kProtoLL32] = comm->region_off[kProtoLL] + align(nslots * comm->ll_slot_bytes);
-  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL32] + nslots * comm->ll32_slot_bytes;
+  comm->region_off[kProtoLL] = align(lay.bytes[kProtoSimple]);
+  comm->region_off[kProtoLL32] = comm->region_off[kProtoLL] + align(lay.bytes[kProtoLL]);
+  comm->pool_bytes = kFlagBytes + comm->region_off[kProtoLL32] + lay.bytes[kProtoLL32];
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&comm->err_host), sizeof(int),
                          cudaHostAllocMapped | cudaHostAllocPortable));
   *comm->err_host = 0;
@@ -575,6 +698,10 @@ patResult_t setup_groups(patComm* comm) {
     const size_t bytes = sizeof(uint64_t) * kMaxChannels * g.lidx.size();
     CUDA_TRY(cudaMalloc(&g.iter_state, bytes));
     CUDA_TRY(cudaMemset(g.iter_state, 0, bytes));
+    if (comm->iter_start) {
+      CUDA_TRY(fill_u64(g.iter_state, static_cast<int64_t>(kMaxChannels * g.lidx.size()), comm->iter_start, nullptr));
+      CUDA_TRY(cudaDeviceSynchronize());
+    }
     long long tcap = 0;
     if (env_int("PAT_TRACE", &tcap) && tcap > 0) {  // device event trace for tools/trace.py
       g.trace_cap = static_cast<int>(std::min<long long>(tcap, 4096));
@@ -594,6 +721,45 @@ patResult_t setup_groups(patComm* comm) {
 patResult_t check_async(patComm* comm) {
   const int e = *reinterpret_cast<volatile int*>(comm->err_host);
   return e ? static_cast<patResult_t>(e) : patSuccess;
+}
+
+// FNV-1a over every resolved setting that decides a call's protocol, slicing, channel count or
+// pool layout. The processes of a multi-process communicator each resolve their own config (env
+// knobs included); one that differs would slice differently or read another region, so
+// patCommInitRankFinish refuses the communicator instead of hanging or corrupting data.
+uint64_t config_fingerprint(const patComm* comm) {
+  const patConfig_t& c = comm->cfg;
+  const uint64_t v[] = {c.staging_bytes, c.slice_bytes, c.ll_threshold, uint64_t(c.trees), uint64_t(c.max_channels),
+                        uint64_t(c.protocol), uint64_t(c.threads), uint64_t(c.depth), uint64_t(c.direct),
+                        uint64_t(c.send_warps), uint64_t(c.fused), uint64_t(comm->skew), uint64_t(comm->pull_slice),
+                        comm->slot_bytes, comm->ll_slot_bytes, comm->ll32_slot_bytes, comm->pool_bytes,
+                        comm->region_off[kProtoLL], comm->region_off[kProtoLL32], comm->epoch_mask,
+                        comm->iter_start, uint64_t(comm->depth_poll)};
+  uint64_t h = 1469598103934665603ull;
+  for (uint64_t x : v)
+    for (int b = 0; b < 8; ++b) h = (h ^ ((x >> (8 * b)) & 0xff)) * 1099511628211ull;
+  return h;
+}
+
+// Every rank on one device and the compiled schedule is the tree local.cu evaluates: the
+// fused single-device executor runs the call, no transport.
+bool fused_path(const patComm* comm, const Compiled* cp) {
+  return !comm->multiprocess && comm->groups.size() == 1 && comm->cfg.fused >= 0 && cp->fused_ok &&
+         static_cast<int>(comm->groups[0].lidx.size()) == comm->n;
+}
+
+// Inbox slots one pipeline step occupies at a receiver.
+int staged_slots(int proto, int kind, bool direct, const KPlan& p) {
+  if (proto == kProtoPull) return kind == kRS ? p.pull_nacc : 0;
+  if (direct) return 0;
+  return p.nslots;
+}
+
+int64_t proto_slot_stride(const patComm* comm, int proto, int nacc) {
+  return static_cast<int64_t>(proto == kProtoLL     ? comm->ll_slot_bytes
+                              : proto == kProtoLL32 ? comm->ll32_slot_bytes
+                              : proto == kProtoPull ? pull_slot_bytes(comm, nacc)
+                                                    : comm->slot_bytes);
 }
 
 patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs, void* const* recvbuffs,
@@ -628,7 +794,8 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
                  (comm->cfg.protocol == patProtoPull || (kind == kRS && chunk_bytes > kPullMinRS));
   for (size_t l = 0; l < comm->lranks.size() && pull_ok && !single_device; ++l)
     pull_ok = legacy_ipc_capable(sendbuffs[l]) && (kind == kRS || legacy_ipc_capable(recvbuffs[l]));
-  const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es));
+  const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es),
+                                    cp->proto.pull_nacc);
   int vec = 16;
   bool aligned4 = (chunk_bytes % 4) == 0, aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
   for (size_t l = 0; l < comm->lranks.size(); ++l) {
@@ -641,8 +808,9 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   vec = aligned16 ? 16 : (aligned8 ? 8 : 0);
   if (sl.proto == kProtoLL32 && vec == 0 && aligned4) vec = 4;  // LL32 moves 4-byte units
   if (sl.proto == kProtoSimple && vec == 8) vec = 0;  // SIMPLE vectors are 16 bytes
-  const bool fused = single_device && comm->cfg.fused >= 0 && cp->fused_ok &&
-                     static_cast<int>(comm->groups[0].lidx.size()) == n;
+  const bool fused = fused_path(comm, cp);
+  if (!fused)
+    if (patResult_t e = ensure_pools(comm)) return e;
   bool direct = false;
   if (kind == kAG && sl.proto == kProtoSimple && !comm->multiprocess && comm->cfg.direct >= 0) {
     direct = single_device || comm->cfg.direct > 0;
@@ -664,10 +832,9 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.iters = sl.iters;
     p.chunk_bytes = chunk_bytes;
     p.slice_bytes = sl.slice;
-    p.slot_stride = static_cast<int64_t>(sl.proto == kProtoLL     ? comm->ll_slot_bytes
-                                         : sl.proto == kProtoLL32 ? comm->ll32_slot_bytes
-                                                                  : comm->slot_bytes);
-    p.depth = comm->cfg.depth;
+    p.slot_stride = proto_slot_stride(comm, sl.proto, p.pull_nacc);
+    const bool polling = sl.proto == kProtoLL || sl.proto == kProtoLL32;
+    p.depth = polling ? comm->depth_poll : comm->cfg.depth;
     {
       // skew distance L: the sender keeps (nrounds-1)*L+1 steps in flight -> needs that many buffers
       const int L = comm->skew;
@@ -679,7 +846,9 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
                      ? L
                      : 0;
     }
-    p.chan_stride = static_cast<int64_t>(p.depth) * std::max(n - 1, 1) * p.slot_stride;
+    // region layout [channel][buffer][slot]: n-1 landing slots per step, PULL's accumulators
+    p.chan_stride = static_cast<int64_t>(p.depth) * (sl.proto == kProtoPull ? std::max<int>(p.pull_nacc, 1) : std::max(n - 1, 1)) *
+                    p.slot_stride;
     p.send_warps = comm->cfg.send_warps;
     p.gpu_scope = single_device ? 1 : 0;
     p.direct = direct && sl.proto != kProtoPull ? 1 : 0;
@@ -691,6 +860,14 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     if (direct)
       for (size_t l = 0; l < comm->lranks.size(); ++l) p.peer_recv[comm->lranks[l]] = static_cast<char*>(recvbuffs[l]);
     p.timeout_ns = static_cast<uint64_t>(comm->cfg.timeout_ms) * 1000000ull;
+    p.epoch_mask = comm->epoch_mask;
+    p.depth_poll = comm->depth_poll;
+    p.poll_channels[0] = comm->region_channels[kProtoLL];
+    p.poll_channels[1] = comm->region_channels[kProtoLL32];
+    p.poll_off[0] = static_cast<int64_t>(kFlagBytes + comm->region_off[kProtoLL]);
+    p.poll_off[1] = static_cast<int64_t>(kFlagBytes + comm->region_off[kProtoLL32]);
+    p.poll_slot[0] = static_cast<int64_t>(comm->ll_slot_bytes);
+    p.poll_slot[1] = static_cast<int64_t>(comm->ll32_slot_bytes);
     p.err = comm->err_dev;
     p.trace = g.trace;
     p.trace_cap = g.trace_cap;
@@ -835,11 +1012,6 @@ patResult_t patCommInitAll(patComm_t* out, int nranks, const int* devlist, const
     comm->lranks.push_back(r);
     comm->ldevs.push_back(d);
   }
-  for (int r = 0; r < nranks; ++r) {
-    char* pool = nullptr;
-    if (patResult_t e = alloc_pool(comm.get(), comm->ldevs[r], &pool)) return e;
-    comm->owned_pool.push_back(pool);
-  }
   // peer access between every pair of distinct devices
   std::vector<int> devs(comm->ldevs);
   std::sort(devs.begin(), devs.end());
@@ -859,8 +1031,10 @@ patResult_t patCommInitAll(patComm_t* out, int nranks, const int* devlist, const
       else if (e != cudaSuccess) return patSystemError;
     }
   if (patResult_t e = setup_groups(comm.get())) return e;
-  for (DevGroup& g : comm->groups)
-    for (int r = 0; r < nranks; ++r) g.pool_view[r] = comm->owned_pool[r];
+  // every rank on one device: calls run in the fused executor unless asked not to, so the
+  // pools wait for the first transport launch (ensure_pools); otherwise allocate them now
+  if (!(comm->groups.size() == 1 && comm->cfg.fused >= 0))
+    if (patResult_t e = ensure_pools(comm.get())) return e;
   long long lt = 1;
   env_int("PAT_LAUNCH_THREADS", &lt);  // 0: one thread submits to every device in turn
   if (lt != 0)
@@ -893,6 +1067,7 @@ patResult_t patCommInitRankPrepare(patComm_t* out, int nranks, int rank, int dev
   char* pool = nullptr;
   if (patResult_t e = alloc_pool(comm.get(), device, &pool)) return e;
   comm->owned_pool.push_back(pool);
+  comm->pools_ready = true;  // mapped by the peers at patCommInitRankFinish
   Handle h{};
   h.magic = kMagic;
   h.version = PAT_B200_VERSION;
@@ -902,6 +1077,7 @@ patResult_t patCommInitRankPrepare(patComm_t* out, int nranks, int rank, int dev
   h.channels = comm->channels;
   h.pool_bytes = comm->pool_bytes;
   h.slot_bytes = comm->slot_bytes;
+  h.config_hash = comm->config_hash = config_fingerprint(comm.get());
   h.pid = static_cast<int32_t>(getpid());
   CUDA_TRY(cudaIpcGetMemHandle(&h.ipc, pool));
   std::memset(handle_out, 0, PAT_HANDLE_BYTES);
@@ -920,9 +1096,13 @@ patResult_t patCommInitRankFinish(patComm_t comm, const void* all_handles) {
     Handle h;
     std::memcpy(&h, static_cast<const char*>(all_handles) + static_cast<size_t>(r) * PAT_HANDLE_BYTES, sizeof(h));
     if (h.magic != kMagic || h.version != PAT_B200_VERSION || h.nranks != comm->n || h.rank != r ||
-        h.pool_bytes != comm->pool_bytes || h.slot_bytes != comm->slot_bytes || h.channels != comm->channels) {
-      std::fprintf(stderr, "pat_b200: handle %d inconsistent (rank %d, pool %llu vs %llu)\n", r, h.rank,
-                   (unsigned long long)h.pool_bytes, (unsigned long long)comm->pool_bytes);
+        h.pool_bytes != comm->pool_bytes || h.slot_bytes != comm->slot_bytes || h.channels != comm->channels ||
+        h.config_hash != comm->config_hash) {
+      std::fprintf(stderr,
+                   "pat_b200: handle %d inconsistent (rank %d, pool %llu vs %llu, config %016llx vs %016llx): every "
+                   "process must resolve the same patConfig_t and PAT_* environment\n",
+                   r, h.rank, (unsigned long long)h.pool_bytes, (unsigned long long)comm->pool_bytes,
+                   (unsigned long long)h.config_hash, (unsigned long long)comm->config_hash);
       return patInvalidUsage;
     }
     if (r == comm->lranks[0]) {
@@ -1021,21 +1201,57 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   // as run_collective decides, assuming cudaMalloc'd (peer-reachable) buffers
   const bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple &&
                        (comm->cfg.protocol == patProtoPull || (static_cast<int>(kind) == kRS && cb > kPullMinRS));
-  const Slicing sl = choose_slicing(comm, kind, cb, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es));
+  const Slicing sl = choose_slicing(comm, kind, cb, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es),
+                                    cp->proto.pull_nacc);
   std::memset(info, 0, sizeof(*info));
-  info->protocol = sl.proto;
   info->trees = trees;
   info->rounds = cp->proto.nrounds;
-  info->channels = sl.channels;
-  info->iterations = sl.iters;
   info->threads = comm->cfg.threads;
   info->launches = static_cast<int>(comm->groups.size());
   info->slots_per_step = cp->proto.nslots;
-  info->slice_bytes = static_cast<size_t>(sl.slice);
   info->pool_bytes = comm->pool_bytes;  // the whole per-rank pool: flags + every protocol region
   info->bytes_sent_per_rank = static_cast<int64_t>(comm->n - 1) * cb;
   info->peak_intermediate_slots = cp->peak_slots;
+  if (fused_path(comm, cp)) {  // as run_collective: local.cu, one launch, no inbox
+    info->protocol = patProtoFused;
+    info->channels = 0;
+    info->iterations = 1;
+    info->threads = 0;
+    info->predicted_us = 0;
+    return patSuccess;
+  }
+  // direct all-gather as run_collective decides it for cudaMalloc'd buffers in one process
+  const bool direct = static_cast<int>(kind) == kAG && sl.proto == kProtoSimple && !comm->multiprocess &&
+                      comm->cfg.direct >= 0;
+  const bool polling = sl.proto == kProtoLL || sl.proto == kProtoLL32;
+  info->protocol = sl.proto;
+  info->channels = sl.channels;
+  info->iterations = sl.iters;
+  info->slice_bytes = static_cast<size_t>(sl.slice);
   info->predicted_us = predict_us(sl.proto, comm->n, cp->proto.nrounds, cb, sl.iters);
+  info->depth = polling ? comm->depth_poll : comm->cfg.depth;
+  info->staged_slots_per_step = staged_slots(sl.proto, kind, direct, cp->proto);
+  info->staging_bytes_used = static_cast<size_t>(sl.channels) * info->depth * info->staged_slots_per_step *
+                             static_cast<size_t>(proto_slot_stride(comm, sl.proto, cp->proto.pull_nacc));
+  return patSuccess;
+}
+
+patResult_t patCommMemInfo(patComm_t comm, patMemInfo_t* info) {
+  if (!comm || !info) return patInvalidArgument;
+  std::lock_guard<std::mutex> lock(comm->mu);
+  std::memset(info, 0, sizeof(*info));
+  info->pool_bytes_per_rank = comm->pool_bytes;
+  info->allocated_bytes = comm->pools_allocated;
+  info->pools_allocated = comm->pools_ready ? 1 : 0;
+  info->depth = comm->cfg.depth;
+  info->depth_poll = comm->depth_poll;
+  const int order[3] = {kProtoSimple, kProtoLL, kProtoLL32};
+  const size_t slot[3] = {comm->slot_bytes, comm->ll_slot_bytes, comm->ll32_slot_bytes};
+  for (int i = 0; i < 3; ++i) {
+    info->region_channels[i] = comm->region_channels[order[i]];
+    info->region_bytes[i] = comm->region_bytes[order[i]];
+    info->slot_bytes[i] = slot[i];
+  }
   return patSuccess;
 }
 

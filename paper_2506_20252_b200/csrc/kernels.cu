@@ -24,6 +24,43 @@ cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out
 
 bool pdl_enabled();  // local.cu
 
+// Pool state for a communicator whose step counters start at `start` instead of 0
+// (PAT_ITER_START, tests of the 32-bit flag wrap): every done/credit flag = start, and the LL /
+// LL32 lines stamped as epoch_clean leaves them (complete for value uint32(start + 1) - 2^30,
+// zero data), which a zeroed pool equals for start = 0.
+__global__ void init_pool_kernel(char* pool, int64_t ll_off, int64_t ll_bytes, int64_t ll32_off, int64_t ll32_bytes,
+                                 uint64_t start) {
+  const uint32_t V = static_cast<uint32_t>(start + 1) - 0x40000000u;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  uint64_t* flags = reinterpret_cast<uint64_t*>(pool);
+  for (int64_t i = tid; i < int64_t{kMaxChannels} * kFlagWords; i += nthr) {
+    const int w = static_cast<int>(i % kFlagWords);
+    if (w >= 8 && w < 16) flags[i] = start;
+  }
+  uint4* ll = reinterpret_cast<uint4*>(pool + ll_off);
+  for (int64_t i = tid; i < ll_bytes / 16; i += nthr) ll[i] = make_uint4(0, V, 0, V);
+  uint4* l32 = reinterpret_cast<uint4*>(pool + ll32_off);
+  for (int64_t i = tid; i < ll32_bytes / 16; i += nthr) l32[i] = (i & 1) ? make_uint4(0, 0, 0, V) : make_uint4(0, 0, 0, 0);
+}
+
+__global__ void fill_u64_kernel(uint64_t* p, int64_t n, uint64_t v) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+cudaError_t init_pool_state(char* pool, int64_t ll_off, int64_t ll_bytes, int64_t ll32_off, int64_t ll32_bytes,
+                            uint64_t start, cudaStream_t stream) {
+  init_pool_kernel<<<256, 256, 0, stream>>>(pool, ll_off, ll_bytes, ll32_off, ll32_bytes, start);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_u64(uint64_t* p, int64_t n, uint64_t v, cudaStream_t stream) {
+  fill_u64_kernel<<<64, 256, 0, stream>>>(p, n, v);
+  return cudaGetLastError();
+}
+
 cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.nlocal * plan.channels);

@@ -33,8 +33,12 @@ struct LaunchWorker {
       while (posted.load(std::memory_order_acquire) == seen && !stop.load(std::memory_order_relaxed)) {
         if ((++spins & 255u) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
           std::unique_lock<std::mutex> lk(m);
+          // store-buffering pair with post(): sleeping.store / posted.load here against
+          // posted.fetch_add / sleeping.load there. Both loads must be seq_cst, or each side may
+          // read the other's stale value (an acquire load may be LDAPR on armv8.3+) and the
+          // worker sleeps through a post.
           sleeping.store(true, std::memory_order_seq_cst);
-          cv.wait(lk, [&] { return posted.load(std::memory_order_acquire) != seen || stop.load(); });
+          cv.wait(lk, [&] { return posted.load(std::memory_order_seq_cst) != seen || stop.load(); });
           sleeping.store(false, std::memory_order_relaxed);
           t0 = std::chrono::steady_clock::now();
         }

@@ -60,7 +60,7 @@ struct KPlan {
   int64_t chunk_bytes;   // bytes of one rank chunk (AG sendcount*esize, RS recvcount*esize)
   int64_t slice_bytes;   // payload bytes per slot per pipeline step
   int64_t slot_stride;   // inbox bytes per slot
-  int64_t chan_stride;   // inbox bytes per channel (2 buffers * nslots * slot_stride)
+  int64_t chan_stride;   // inbox bytes per channel (depth buffers x slots per buffer x slot_stride)
   uint64_t timeout_ns;
   KRound rounds[kMaxRounds];
   int8_t slot_round[kMaxSlots];    // round whose arrival fills slot j
@@ -71,7 +71,8 @@ struct KPlan {
   int8_t peers[kMaxRounds];
   // PULL protocol (receiver reads the upstream's buffers): per arrival slot j
   int8_t pull_act[kMaxSlots];      // RS: PullAct
-  int8_t pull_dst[kMaxSlots];      // RS: local staging slot accumulating offset slot_offset[j]
+  int8_t pull_dst[kMaxSlots];      // RS: accumulator (staging slot) id folding the arrival of slot j
+  int8_t pull_nacc;                // RS: accumulators per step (staging slots per buffer)
   int8_t round_dep[kMaxRounds];    // upstream round whose arrivals round t reads; -1 = own data only
   uint8_t sig_after[kMaxRounds];   // reader rounds (bitmask) that become ready when round t completes
   uint8_t stage_rounds;            // RS: bitmask of rounds that write the local staging (need credits)
@@ -89,6 +90,13 @@ struct KPlan {
   // optional device trace (PAT_TRACE=1): per (CTA, role) ring of {globaltimer ns, event code}
   uint64_t* trace;
   int trace_cap;                    // entries per (CTA, role)
+  // 32-bit line flags (LL, LL32) repeat every 2^32 steps: every kernel's receiver re-stamps its
+  // own polling buffers once per epoch (epoch_clean), so no line can hold a flag 2^32 steps old
+  uint64_t epoch_mask;              // (1 << 31) - 1; PAT_EPOCH_SHIFT overrides (tests)
+  int depth_poll;                   // LL / LL32 inbox buffers per channel
+  int poll_channels[2];             // channels of the LL / LL32 regions
+  int64_t poll_off[2];              // LL / LL32 region offsets from a pool's base (= flags[rank])
+  int64_t poll_slot[2];             // LL / LL32 slot bytes
 };
 
 }  // namespace pat

@@ -283,8 +283,43 @@ __device__ __forceinline__ char* slot_ptr(const KPlan& p, int rank, int c, int b
   return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j) * p.slot_stride;
 }
 
+// PULL staging: accumulator `a` of buffer `buf` (pull_nacc accumulators per buffer)
+__device__ __forceinline__ char* acc_ptr(const KPlan& p, int rank, int c, int buf, int a) {
+  return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.pull_nacc + a) * p.slot_stride;
+}
+
 __device__ __forceinline__ uint64_t* chan_flags(const KPlan& p, int rank, int c) {
   return p.flags[rank] + c * kFlagWords;
+}
+
+// ------------------------------------------------------------------------- flag epochs
+// LL and LL32 lines carry the 32-bit value uint32(g + 1) of a 64-bit step counter, so a line
+// last written 2^32 steps ago (or never written, at g + 1 = 2^32) would pass for the current
+// step. The owner of an inbox therefore re-stamps its polling buffers once per 2^31 steps: the
+// receiver of step g, when g + 1 is within depth_poll of an epoch start, rewrites buffer
+// g % depth_poll of channel c in its LL and LL32 regions with lines that are complete for step
+// value V = uint32(g + 1) - 2^30 and zero data — a value no step polls in the next 3 * 2^30
+// steps — after consuming step g and before publishing done(g). A sender writes that buffer
+// again only for step g + depth_poll, after done(g), so the re-stamp cannot race a write.
+// (NCCL's LL protocol cleans its buffers near the flag wrap the same way.)
+__device__ __forceinline__ bool epoch_clean_due(const KPlan& p, uint64_t g) {
+  return ((g + 1) & p.epoch_mask) < static_cast<uint64_t>(p.depth_poll);
+}
+// by threads [tid, nthr) of the receiver; the caller fences before publishing done(g)
+static __device__ __noinline__ void epoch_clean(const KPlan& p, int R, int c, uint64_t g, int tid, int nthr) {
+  const uint32_t V = static_cast<uint32_t>(g + 1) - 0x40000000u;
+  const int b = static_cast<int>(g % static_cast<uint64_t>(p.depth_poll));
+  const int64_t per_buf[2] = {static_cast<int64_t>(p.nslots) * p.poll_slot[0],
+                              static_cast<int64_t>(p.nslots) * p.poll_slot[1]};
+  char* pool = reinterpret_cast<char*>(p.flags[R]);
+  if (c < p.poll_channels[0]) {  // LL lines {data, flag, data, flag}
+    uint4* q = reinterpret_cast<uint4*>(pool + p.poll_off[0] + (static_cast<int64_t>(c) * p.depth_poll + b) * per_buf[0]);
+    for (int64_t i = tid; i < per_buf[0] / 16; i += nthr) q[i] = make_uint4(0, V, 0, V);
+  }
+  if (c < p.poll_channels[1]) {  // LL32 lines {7 zero words, V ^ hash(0) = V}
+    uint4* q = reinterpret_cast<uint4*>(pool + p.poll_off[1] + (static_cast<int64_t>(c) * p.depth_poll + b) * per_buf[1]);
+    for (int64_t i = tid; i < per_buf[1] / 16; i += nthr) q[i] = (i & 1) ? make_uint4(0, 0, 0, V) : make_uint4(0, 0, 0, 0);
+  }
 }
 
 // Credits: before pushing step g into a peer's inbox buffer g % depth, the peer must have
@@ -457,7 +492,10 @@ __device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int
     }
   }
   tr.rec(kEvDelivered, s.g, 0);
+  const bool clean = epoch_clean_due(p, s.g);
+  if (clean) epoch_clean(p, s.R, s.c, s.g, tid, nthr);
   named_bar(2, nthr);
+  if (clean && tid < n) fence_acq_rel(gpu);
   if (tid < n && tid != s.R) st_release(chan_flags(p, tid, s.c) + 8 + s.R, s.g + 1, gpu);
 }
 
@@ -533,12 +571,16 @@ __device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
 }
 
 // ------------------------------------------------------------------------- LL32 protocol
-// 32-byte lines {payload, flag} written with ONE st.volatile.v8 (STG.256) and polled with one
-// ld.volatile.v8: a single flag word per line. This relies on a 32-byte vector store landing
-// whole at the peer, which tools/atomicity_probe.cu measured on this fabric (0 torn lines of
-// 7.3e9 per GPU pair, 2 and 4 GPUs, every GPU sending and receiving; profiles/r01f_*). LL
-// assumes only 8-byte atomicity and spends half of every line on flags; LL32 carries 28
-// payload bytes per 32 (87.5%).
+// 32-byte lines {7 payload words, check word} written with ONE st.volatile.v8 (STG.256) and
+// polled with one ld.volatile.v8. The check word is the step's flag XOR a hash of the 7 payload
+// words, so a line counts as arrived only when the flag AND the data it was written with are
+// both visible: a line that lands in pieces (the flag's 16-byte sector before the data sector —
+// PTX promises single-copy atomicity per element, not per 32-byte vector, and LL128's one flag
+// per 128 bytes was observed to tear on this fabric) fails the check and is
+// polled again instead of being consumed. tools/atomicity_probe.cu never saw a 32-byte store
+// land torn (0 of 7.3e9 lines, profiles/r01f_atomicity_g*.txt); the check makes correctness
+// independent of that observation. The reference's executor consumes a message only when it is
+// complete (Mailbox::incoming, simulate.cpp:131-149); this is that rule per line.
 //
 // Payload units: a line holds R units of U bytes (U = 4, R = 7; U = 8 for 8-byte reductions so
 // every unit is a whole element, R = 3). Lines go in groups of 32 (one per lane): unit r of
@@ -546,13 +588,25 @@ __device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
 // loads and stores is one contiguous 32 U-byte access. Lines whose first unit lies past the
 // slice end are empty; sender and receiver skip the same ones.
 struct Line32 {
-  uint32_t w[8];  // w[7] = flag
+  uint32_t w[8];  // w[7] = check word
 };
+
+// Hash of a line's payload words: a sum of distinct odd multiples (7 IMADs), so a change of any
+// single word always changes it and the all-zero line (a zeroed or re-stamped pool) hashes to 0.
+__host__ __device__ __forceinline__ uint32_t line_hash(const Line32& v) {
+  return v.w[0] * 0x9E3779B1u + v.w[1] * 0x85EBCA77u + v.w[2] * 0xC2B2AE3Du + v.w[3] * 0x27D4EB2Fu +
+         v.w[4] * 0x165667B1u + v.w[5] * 0xD3A2646Du + v.w[6] * 0xFD7046C5u;
+}
 
 __device__ __forceinline__ void st_line32(void* p, const Line32& v) {
   asm volatile("st.volatile.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
                "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
                : "memory");
+}
+// Seal a line for step flag `flag` and store it.
+__device__ __forceinline__ void put_line32(void* p, Line32& v, uint32_t flag) {
+  v.w[7] = flag ^ line_hash(v);
+  st_line32(p, v);
 }
 __device__ __forceinline__ Line32 ld_volatile32(const void* p) {
   Line32 v;
@@ -563,15 +617,16 @@ __device__ __forceinline__ Line32 ld_volatile32(const void* p) {
                : "memory");
   return v;
 }
-// Poll one line until its flag word carries `flag`.
+__device__ __forceinline__ bool line32_ok(const Line32& v, uint32_t flag) { return v.w[7] == (flag ^ line_hash(v)); }
+// Poll one line until it is complete for step flag `flag` (check word matches its payload).
 __device__ __forceinline__ Line32 ld_line32(const char* line, uint32_t flag, Waiter& w) {
   Line32 v = ld_volatile32(line);
-  if (v.w[7] == flag) return v;
+  if (line32_ok(v, flag)) return v;
   uint64_t start = 0;
   uint32_t spins = 0;
   while (!w.aborted) {
     v = ld_volatile32(line);
-    if (v.w[7] == flag) break;
+    if (line32_ok(v, flag)) break;
     if ((++spins & 1023u) == 0) {
       const uint64_t now = globaltimer();
       if (start == 0) start = now;
@@ -701,8 +756,7 @@ __device__ void ll32_phase(const KPlan& p, const Step& s, int t, Waiter& w) {
         const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
         PAT_LL32_LINES {
           Line32 v = fwd ? ld_line32(fwd + 32 * q, flag, w) : load_units<U>(snd, gb, lane, s.len, p);
-          v.w[7] = flag;
-          st_line32(dst + 32 * q, v);
+          put_line32(dst + 32 * q, v, flag);
         }
       } else {
         const char* own = snd + ((s.R - r.chunk[pos] + n) % n) * Cb;
@@ -718,8 +772,7 @@ __device__ void ll32_phase(const KPlan& p, const Step& s, int t, Waiter& w) {
               fold_line32<DT, OP, U>(v, ld_line32(slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][a]) + 32 * q, flag, w));
             fold_line32<DT, OP, U>(v, mine);
           }
-          v.w[7] = flag;
-          st_line32(dst + 32 * q, v);
+          put_line32(dst + 32 * q, v, flag);
         }
       }
     }
@@ -773,11 +826,11 @@ __device__ __forceinline__ void pull_task(const KPlan& p, const Step& s, int t, 
       grp_fold<DT, OP>(out + at * Cb + s.off, srcs, 1, s.len, p, tid, nthr);
     } else {
       const char* m = r.narr[pos] == 0 ? p.peer_send[Q] + at * Cb + s.off
-                                       : slot_ptr(p, Q, s.c, s.buf, r.arr[pos][r.narr[pos] - 1]);
+                                       : acc_ptr(p, Q, s.c, s.buf, p.pull_dst[r.arr[pos][r.narr[pos] - 1]]);
       const int j = r.slot_base + pos;
       const int kr = p.slot_offset[j];                  // received offset at R
       const char* mine = own + ((s.R - kr + n) % n) * Cb + s.off;
-      char* stage = slot_ptr(p, s.R, s.c, s.buf, p.pull_dst[j]);
+      char* stage = p.pull_dst[j] >= 0 ? acc_ptr(p, s.R, s.c, s.buf, p.pull_dst[j]) : nullptr;
       char* dst = stage;
       int cnt = 2;
       switch (p.pull_act[j]) {
@@ -831,10 +884,15 @@ __device__ void pull_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
       for (int q = 0; q < n; ++q)
         if (q != R) st_relaxed(chan_flags(p, q, c) + 8 + R, g1, gpu);
   };
+  // before done(step i) (signal of the last round): the step's epoch re-stamp, if due
+  auto clean = [&](int i) {
+    if (epoch_clean_due(p, base + i)) epoch_clean(p, R, c, base + i, tid, nthr);
+  };
   if (L > 0) {  // skewed: round t of step k - t*L in iteration k, one fence per iteration
     for (int k = 0; k < p.iters + (NR - 1) * L; ++k) {
       for (int t = 0; t < NR; ++t)
         if (k - t * L >= 0 && k - t * L < p.iters) task(k - t * L, t);
+      if (k - (NR - 1) * L >= 0 && k - (NR - 1) * L < p.iters) clean(k - (NR - 1) * L);
       __syncthreads();
       if (tid == 0) {
         fence_acq_rel(gpu);
@@ -846,6 +904,7 @@ __device__ void pull_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
     for (int i = 0; i < p.iters; ++i)
       for (int t = 0; t < NR; ++t) {
         task(i, t);
+        if (t == NR - 1) clean(i);
         __syncthreads();
         if (tid == 0) {
           fence_acq_rel(gpu);
@@ -908,7 +967,13 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
       } else {
         for (int t = 0; t <= p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w);
       }
+      const bool clean = epoch_clean_due(p, s.g);
+      if (clean) {  // every load of this step's lines returned before the barrier above it
+        __syncthreads();
+        epoch_clean(p, R, c, s.g, threadIdx.x, blockDim.x);
+      }
       __syncthreads();
+      if (clean && threadIdx.x < p.n) fence_acq_rel(w.gpu);
       // done(step): every load of this step's inbox has returned (its value was consumed before
       // the barrier), so a relaxed store suffices to hand the buffers back. The last step's is
       // published by the next call's kernel (above): a remote store at exit would hold the
