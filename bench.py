@@ -57,6 +57,7 @@ def parse(argv=None):
                     help="ranks without torchrun (default: 8 at --gpus 1, else --gpus), placed round-robin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--nccl-graph", action="store_true", help="time NCCL Ring from CUDA graphs (hangs on some boxes)")
     ap.add_argument("--no-extras", action="store_true", help="skip transport_local / ref_dtypes records")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args(argv)
@@ -207,6 +208,7 @@ class Devices:
 
     def __init__(self, torch, devs, dist=None):
         self.torch, self.devs, self.dist = torch, list(devs), dist
+        self.pre = None  # enqueued on the timing streams before the start events (time_ms)
         self.streams = {d: torch.cuda.Stream(d) for d in self.devs}
 
     def sync(self):
@@ -247,9 +249,13 @@ class Devices:
         return {d: (E(enable_timing=True), E(enable_timing=True)) for d in self.devs}
 
     def time_ms(self, run):
-        """barrier; start events; run(); end events; barrier -> max over devices (ms)."""
+        """barrier; device barrier; start events; run(); end events; barrier -> max over devices (ms).
+        The device barrier (patCommBarrier on the timing streams, outside the timed region) lines
+        the GPUs up, so host jitter in leaving the host barrier is not timed as collective time."""
         ev = self.events()
         self.barrier()
+        if self.pre is not None:
+            self.pre()
         for d in self.devs:
             ev[d][0].record(self.streams[d])
         run()
@@ -296,6 +302,23 @@ def run_pat(args, rank, world, local):
     L = len(devices)  # ranks this process drives
     D = Devices(torch, sorted(set(devices)), dist)
     streams = [D.streams[d] for d in devices]
+
+    # 2x L2 of scratch per GPU, read before every timed region (leaves L2 clean: the dirty output
+    # lines of the previous region are written back before the clock starts, not inside it)
+    flush = {d: torch.empty(2 * L2_BYTES // 4, device=f"cuda:{d}") for d in D.devs}
+
+    def pre():
+        # L2 flush by reads, device barrier (GPUs aligned), then a ~100 us spin on each timing
+        # stream so the graph replays are queued behind it before the start events: neither host
+        # jitter between ranks nor the host's graph-launch latency is timed as collective time
+        for d in D.devs:
+            with torch.cuda.device(d), torch.cuda.stream(D.streams[d]):
+                flush[d].sum()
+        comm.barrier(streams)
+        for d in D.devs:
+            with torch.cuda.device(d), torch.cuda.stream(D.streams[d]):
+                torch.cuda._sleep(int(os.environ.get("BENCH_SLEEP_CYCLES", "200000")))
+    D.pre = pre
     g = {d: torch.Generator(device=f"cuda:{d}").manual_seed(1234 + 17 * rank + d) for d in D.devs}
 
     def rnd(numel, d):
@@ -373,7 +396,15 @@ def run_pat(args, rank, world, local):
     ms_per_step = step_ms / K
     value = busbw_gbs(n, C, ms_per_step / 1e3)
 
-    # ---- the same steps launched eagerly through the C ABI (events per call)
+    # ---- the same calls launched eagerly (no graphs) through the Python binding: K back-to-back
+    # calls per collective, events around the K (as the NCCL comparison is timed)
+    def eager_k(kinds):
+        def run():
+            for k in range(K):
+                call(comm, kinds, sets[k % S])
+        return run
+    eager_bb = max_over_ranks(torch, dist, dev0, [D.time_ms(eager_k(("ag",))), D.time_ms(eager_k(("rs",)))])
+    # ---- isolated eager calls (events per call on an idle stream: host submission included)
     KE = min(K, 100)
     eev = [D.events() for _ in range(3 * KE)]
     D.barrier()
@@ -392,7 +423,11 @@ def run_pat(args, rank, world, local):
     ag_e = max(sum(eev[3 * k][d][0].elapsed_time(eev[3 * k][d][1]) for k in range(KE)) for d in D.devs)
     rs_e = max(sum(eev[3 * k + 1][d][0].elapsed_time(eev[3 * k + 1][d][1]) for k in range(KE)) for d in D.devs)
     ag_e, rs_e = max_over_ranks(torch, dist, dev0, [ag_e, rs_e])
-    eager_us = {"all_gather": 1e3 * ag_e / KE, "reduce_scatter": 1e3 * rs_e / KE}
+    eager_iso_us = {"all_gather": 1e3 * ag_e / KE, "reduce_scatter": 1e3 * rs_e / KE,
+                    "timing": "one eager call at a time on an idle GPU, events around each call: includes the "
+                              "host's submission time (Python binding + C ABI)"}
+    eager_us = {"all_gather": 1e3 * eager_bb[0] / K, "reduce_scatter": 1e3 * eager_bb[1] / K,
+                "timing": "K back-to-back eager calls through the Python binding, events around the K"}
 
     dbg("e2e")
     # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region.
@@ -471,6 +506,8 @@ def run_pat(args, rank, world, local):
         D.barrier()
         timing = "graph"
         try:
+            if not args.nccl_graph:  # capturing NCCL inside this process hangs (r02, 2 GPUs): eager
+                raise RuntimeError("eager")
             def nbody(kinds, count):
                 def run():
                     for k in range(count):
@@ -485,8 +522,10 @@ def run_pat(args, rank, world, local):
             nt = [D.time_ms(replay_k(ngraphs[kinds])) for kinds in (("ag", "rs"), ("ag",), ("rs",))]
             del ngraphs
         except Exception as e:  # eager fallback, labelled
-            dbg(f"nccl graph capture failed: {e}")
-            timing = f"eager (graph capture failed: {type(e).__name__})"
+            dbg(f"nccl graph capture skipped/failed: {e}")
+            timing = ("eager: K back-to-back calls on one stream (GPU-bound: NCCL's host launch is shorter than "
+                      "its kernel); CUDA graphs of NCCL calls hang inside bench.py, see --nccl-graph"
+                      if str(e) == "eager" else f"eager (graph capture failed: {type(e).__name__})")
             D.barrier()
 
             def eager(kinds):
@@ -557,9 +596,12 @@ def run_pat(args, rank, world, local):
     if mode == "local":
         algo_bytes = (n * n + n) * C  # local mode: read n*C + write n^2*C (AG) / read n^2*C + write n*C (RS)
         peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-        roof = {"bound": "hbm", "kernel": ("local_rs_kernel" if dom == "reduce_scatter" else "local_ag_tma_kernel"),
+        roof = {"bound": "hbm", "kernel": ("local_rs_flat_kernel" if dom == "reduce_scatter" else "local_ag32_kernel"),
                 "unit": "GB/s", "algorithmic_bytes_per_launch": algo_bytes,
-                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
+                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
+                "write_ceiling_note": "the all-gather is (n^2 C writes + n C reads): a write-only kernel of the same "
+                                      "72 MiB takes 12.2 us = 0.94 of hbm_gbs (profiles/r02_local_tune.jsonl, "
+                                      "ceil_write_only), so ~0.94 bounds the all-gather's frac"}
         achieved = algo_bytes / (dom_us * 1e-6) / 1e9
     else:
         # per GPU: every rank on it receives (n-1)*C over NVLink per launch (ranks sharing a GPU
@@ -643,7 +685,8 @@ def run_pat(args, rank, world, local):
                        "plan_allgather": plan_ag, "plan_reduce_scatter": plan_rs},
             "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K,
                            "timing": "graph of K back-to-back calls per collective"},
-            "latency_us_eager": dict(eager_us, timing="eager C-ABI calls, CUDA events per call"),
+            "latency_us_eager": eager_us,
+            "latency_us_eager_isolated": eager_iso_us,
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host; "

@@ -211,6 +211,25 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
                         patPlanInfo_t* info);
 patResult_t patCommMemInfo(patComm_t comm, patMemInfo_t* info);
 
+/* Device-side barrier on the given streams (one entry per local rank; the first stream of each
+ * device is used): returns once enqueued; the kernels complete when every rank reached its
+ * barrier. Every rank calls it the same number of times. A no-op with one device. */
+patResult_t patCommBarrier(patComm_t comm, const patStream_t* streams);
+
+/* ---- symmetric user-buffer windows (one process per rank; zero copy) -------------------
+ * The paper's way around staging is to register the user buffers (NCCL's
+ * ncclCommRegister / symmetric windows). Collective over a multi-process communicator: every
+ * rank calls Prepare with a window of the same byte size (cudaMalloc memory, e.g. PyTorch's
+ * caching allocator), all-gathers the PAT_HANDLE_BYTES blobs (like init) and calls Finish with
+ * them, rank-ordered; windows are matched by registration order. Afterwards, a call whose
+ * all-gather recvbuf (direct push) or reduce-scatter sendbuf (PULL) lies inside a window runs
+ * zero copy, provided every rank passes its buffer at the SAME offset of its window — the
+ * kernels check that at entry (a mismatch is the asynchronous error patInvalidUsage).
+ * Deregister is local and must follow the completion of every call that used the window. */
+patResult_t patCommRegisterPrepare(patComm_t comm, void* buf, size_t bytes, void* handle_out);
+patResult_t patCommRegisterFinish(patComm_t comm, void* buf, const void* all_handles);
+patResult_t patCommDeregister(patComm_t comm, void* buf);
+
 /* ---- collectives (asynchronous on the given streams) ----------------------------------
  * Array arguments are indexed by local rank (patCommLocalRanks order): one entry per rank
  * this communicator drives. Ranks sharing a device are launched as one kernel on the stream

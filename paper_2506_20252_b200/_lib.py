@@ -128,7 +128,7 @@ SYMBOLS = [
     "patReduceScatter", "patAllGatherSchedule", "patReduceScatterSchedule", "patScheduleBuild",
     "patScheduleMirror", "patScheduleValidate", "patScheduleStats", "patScheduleTraceCsv",
     "patMaxTrees", "patTreesFromBuffer", "patPatBufferSlots", "patRoundCountFormula", "patCommTraceRead",
-    "patCommMemInfo",
+    "patCommMemInfo", "patCommRegisterPrepare", "patCommRegisterFinish", "patCommDeregister", "patCommBarrier",
 ]
 
 _lib = None
@@ -176,8 +176,32 @@ def lib() -> ctypes.CDLL:
         L.patRoundCountFormula.argtypes = [ctypes.c_int, ctypes.c_int, IP]
         L.patCommTraceRead.argtypes = [VP, ctypes.c_int, VP, ctypes.c_size_t, SZP, IP, IP]
         L.patCommMemInfo.argtypes = [VP, ctypes.POINTER(MemInfo)]
+        L.patCommRegisterPrepare.argtypes = [VP, VP, ctypes.c_size_t, VP]
+        L.patCommRegisterFinish.argtypes = [VP, VP, VP]
+        L.patCommDeregister.argtypes = [VP, VP]
+        L.patCommBarrier.argtypes = [VP, PP]
         _lib = L
     return _lib
+
+
+_fast = None
+
+
+def fast():
+    """The CPython fast-call module (csrc/pyfast.c, built in-tree next to libpatb200.so), bound
+    to this library's patAllGather / patReduceScatter. None if it was not built."""
+    global _fast
+    if _fast is None:
+        L = lib()
+        try:
+            from . import _patfast as F
+        except ImportError:
+            _fast = False
+            return None
+        F.bind(ctypes.cast(L.patAllGather, ctypes.c_void_p).value,
+               ctypes.cast(L.patReduceScatter, ctypes.c_void_p).value)
+        _fast = F
+    return _fast or None
 
 
 def check(rc: int, where: str = "") -> None:

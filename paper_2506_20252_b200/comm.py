@@ -84,12 +84,16 @@ class PatComm:
         n = ctypes.c_int()
         check(lib().patCommCount(self._h, ctypes.byref(n)), "patCommCount")
         self.nranks = n.value
+        self._hv = int(handle.value) if handle.value else 0
         nl = ctypes.c_int()
         ranks = (ctypes.c_int * _lib.MAX_RANKS)()
         devs = (ctypes.c_int * _lib.MAX_RANKS)()
         check(lib().patCommLocalRanks(self._h, ctypes.byref(nl), ranks, devs), "patCommLocalRanks")
         self.local_ranks = list(ranks[: nl.value])
         self.devices = list(devs[: nl.value])
+        self._fast = _lib.fast()
+        self._raw_stream = (getattr(torch._C, "_cuda_getCurrentRawStream", None)
+                            if torch is not None and torch.cuda.is_available() else None)
 
     # ------------------------------------------------------------------ construction
     @classmethod
@@ -117,7 +121,9 @@ class PatComm:
         except BaseException:
             lib().patCommDestroy(h)
             raise
-        return cls(h)
+        c = cls(h)
+        c._exchange = exchange
+        return c
 
     @classmethod
     def from_process_group(cls, group=None, device: Optional[int] = None, **config) -> "PatComm":
@@ -152,11 +158,29 @@ class PatComm:
                 streams = [0] * len(self.local_ranks)
         return ptr_array([int(getattr(s, "cuda_stream", s)) for s in streams])
 
+    def _fast_streams(self, streams):
+        """Stream handles as plain ints for _patfast (one current-stream lookup per device)."""
+        if streams is None:
+            if self._raw_stream is not None:
+                if len(self.devices) == 1:
+                    return self._raw_stream(self.devices[0])
+                cur = {}
+                for d in self.devices:
+                    if d not in cur:
+                        cur[d] = self._raw_stream(d)
+                return [cur[d] for d in self.devices]
+            return [0] * len(self.local_ranks)
+        return [int(getattr(s, "cuda_stream", s)) for s in streams]
+
     def all_gather(self, sendbufs, recvbufs, count: Optional[int] = None, dtype=None, streams=None, schedule=None):
         """sendbufs[l] -> recvbufs[l] (n*count, origin order) for every local rank l."""
         dt = _dtype(dtype, sendbufs[0])
         if count is None:
             count = sendbufs[0].numel()
+        if schedule is None and self._fast is not None and self._h:
+            check(self._fast.all_gather(self._hv, [_ptr(x) for x in sendbufs], [_ptr(x) for x in recvbufs], count, dt,
+                                        self._fast_streams(streams)), "patAllGather")
+            return
         sb, rb = ptr_array([_ptr(x) for x in sendbufs]), ptr_array([_ptr(x) for x in recvbufs])
         if schedule is not None:
             enc = schedule.encode()
@@ -171,6 +195,10 @@ class PatComm:
         dt = _dtype(dtype, sendbufs[0])
         if count is None:
             count = recvbufs[0].numel()
+        if schedule is None and self._fast is not None and self._h:
+            check(self._fast.reduce_scatter(self._hv, [_ptr(x) for x in sendbufs], [_ptr(x) for x in recvbufs], count,
+                                            dt, int(op), self._fast_streams(streams)), "patReduceScatter")
+            return
         sb, rb = ptr_array([_ptr(x) for x in sendbufs]), ptr_array([_ptr(x) for x in recvbufs])
         if schedule is not None:
             enc = schedule.encode()
@@ -188,6 +216,12 @@ class PatComm:
             raise PatError(5, "all_gather_into_tensor needs a one-rank-per-process communicator")
         if output.numel() != self.nranks * input.numel() or output.dtype != input.dtype:
             raise PatError(31, "all_gather_into_tensor: output must hold nranks * input.numel() of input's dtype")
+        if self._fast is not None and self._h:
+            st = self._fast_streams(None if stream is None else [stream])
+            check(self._fast.all_gather(self._hv, input.data_ptr(), output.data_ptr(), input.numel(),
+                                        TORCH_DTYPES[input.dtype], st if isinstance(st, int) else st[0]),
+                  "patAllGather")
+            return
         self.all_gather([input], [output], input.numel(), None, None if stream is None else [stream])
 
     def reduce_scatter_tensor(self, output, input, op: int = _lib.SUM, stream=None):
@@ -197,7 +231,38 @@ class PatComm:
             raise PatError(5, "reduce_scatter_tensor needs a one-rank-per-process communicator")
         if input.numel() != self.nranks * output.numel() or output.dtype != input.dtype:
             raise PatError(31, "reduce_scatter_tensor: input must hold nranks * output.numel() of output's dtype")
+        if self._fast is not None and self._h:
+            st = self._fast_streams(None if stream is None else [stream])
+            check(self._fast.reduce_scatter(self._hv, input.data_ptr(), output.data_ptr(), output.numel(),
+                                            TORCH_DTYPES[output.dtype], int(op), st if isinstance(st, int) else st[0]),
+                  "patReduceScatter")
+            return
         self.reduce_scatter([input], [output], output.numel(), None, op, None if stream is None else [stream])
+
+    def barrier(self, streams=None) -> None:
+        """Device-side barrier over every rank on `streams` (default: the current streams)."""
+        check(lib().patCommBarrier(self._h, self._streams(streams)), "patCommBarrier")
+
+    # ---- symmetric windows (one rank per process): zero-copy all-gather / PULL reduce-scatter
+    def register(self, buf, nbytes: Optional[int] = None) -> None:
+        """Collective: every rank registers a window of the same size (a cudaMalloc'd tensor or
+        pointer), in the same order. Calls whose all-gather recvbuf / reduce-scatter sendbuf lie
+        inside a window at the same offset on every rank then run zero copy
+        (patCommRegisterPrepare/Finish)."""
+        exchange = getattr(self, "_exchange", None)
+        if exchange is None:
+            raise PatError(5, "register needs a one-rank-per-process communicator (init_rank)")
+        if nbytes is None:
+            nbytes = buf.numel() * buf.element_size()
+        blob = ctypes.create_string_buffer(_lib.HANDLE_BYTES)
+        check(lib().patCommRegisterPrepare(self._h, _ptr(buf), int(nbytes), blob), "patCommRegisterPrepare")
+        handles = exchange(bytes(blob.raw))
+        allh = ctypes.create_string_buffer(b"".join(handles), self.nranks * _lib.HANDLE_BYTES)
+        check(lib().patCommRegisterFinish(self._h, _ptr(buf), allh), "patCommRegisterFinish")
+
+    def deregister(self, buf) -> None:
+        """Local; only after every call that used the window has completed."""
+        check(lib().patCommDeregister(self._h, _ptr(buf)), "patCommDeregister")
 
     def plan(self, kind: int, count: int, dtype) -> dict:
         info = PlanInfo()

@@ -34,6 +34,7 @@
 namespace pat {
 using KernelFn = void (*)(const KPlan);
 cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream);
+cudaError_t launch_barrier(const BPlan& b, cudaStream_t stream);
 cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out);
 cudaError_t init_pool_state(char* pool, int64_t ll_off, int64_t ll_bytes, int64_t ll32_off, int64_t ll32_bytes,
                             uint64_t start, cudaStream_t stream);
@@ -48,7 +49,11 @@ using namespace pat;
 
 namespace {
 
-constexpr size_t kFlagBytes = sizeof(uint64_t) * kMaxChannels * kFlagWords;  // 8 KiB
+// per pool: channel flags (8 KiB), then the barrier words (patCommBarrier), padded so the
+// inbox regions stay 4 KiB aligned
+constexpr size_t kChanFlagBytes = sizeof(uint64_t) * kMaxChannels * kFlagWords;  // 8 KiB
+constexpr size_t kBarrierOff = kChanFlagBytes;
+constexpr size_t kFlagBytes = kChanFlagBytes + 4096;
 constexpr uint32_t kMagic = 0x50415442;                                       // "PATB"
 constexpr size_t kDefaultPoolBytes = 512ull << 20;  // inbox pool budget per rank (all channels)
 constexpr size_t kMaxSlice = 256 << 10;
@@ -96,6 +101,17 @@ struct Handle {
 };
 static_assert(sizeof(Handle) <= PAT_HANDLE_BYTES, "handle too large");
 
+// Registration blob of one symmetric window (patCommRegisterPrepare).
+struct RegHandle {
+  uint32_t magic, version;
+  int32_t nranks, rank;
+  uint64_t bytes;   // window size (equal on every rank)
+  uint64_t offset;  // window start within its allocation (the IPC handle names the allocation)
+  uint64_t config_hash;
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(RegHandle) <= PAT_HANDLE_BYTES, "registration handle too large");
+
 bool env_int(const char* name, long long* out) {
   const char* v = std::getenv(name);
   if (!v || !*v) return false;
@@ -114,6 +130,17 @@ struct patComm {
   std::vector<char*> owned_pool;     // per local index
   std::vector<DevGroup> groups;
   std::vector<void*> ipc_opened;
+  // symmetric windows (multi-process zero copy): local range, the peers' matching ranges
+  struct Window {
+    char* local = nullptr;
+    size_t bytes = 0;
+    uint32_t id = 0;
+    std::array<char*, kMaxRanks> peer{};
+    std::array<std::string, kMaxRanks> key{};  // ipc_cache key of each peer's mapping
+  };
+  std::vector<Window> windows;
+  uint32_t next_window = 1;
+  std::map<std::string, std::pair<char*, int>> ipc_cache;  // IPC handle bytes -> (base, refs)
   size_t slot_bytes = 0, pool_bytes = 0;
   size_t ll_slot_bytes = 0;                // LL inbox slot (own region, common_init)
   size_t ll32_slot_bytes = 0;              // LL32 inbox slot (own region)
@@ -128,8 +155,10 @@ struct patComm {
   size_t pools_allocated = 0;  // bytes of inbox pool this process allocated (all its ranks)
   int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
   int skew = 1;            // SIMPLE / PULL sender skew distance (PAT_SKEW; 0 = rounds in order)
+  int leaves_first = 1;    // push senders send every round's leaf chunks first (PAT_LEAVES_FIRST)
   uint64_t epoch_mask = (1ull << 31) - 1;  // LL / LL32 flag epochs (PAT_EPOCH_SHIFT, tests)
   uint64_t iter_start = 0;                 // first pipeline step of every channel (PAT_ITER_START, tests)
+  uint64_t barrier_seq = 0;                // patCommBarrier calls so far
   int channels = 0;
   uint64_t config_hash = 0;  // config_fingerprint(): must be equal on every process of a comm
   int* err_host = nullptr;
@@ -181,6 +210,26 @@ bool legacy_ipc_capable(const void* ptr) {
   constexpr int kIsLegacyIpcCapable = 10;  // CU_POINTER_ATTRIBUTE_IS_LEGACY_CUDA_IPC_CAPABLE
   if (fn(&v, kIsLegacyIpcCapable, reinterpret_cast<unsigned long long>(ptr)) != 0) return false;
   return v != 0;
+}
+
+// Base of the allocation holding `ptr` (cuMemGetAddressRange through the runtime's driver
+// entry point, so the library links no libcuda).
+bool allocation_base(const void* ptr, char** base, size_t* size) {
+  using Fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<Fn>(nullptr);
+    return reinterpret_cast<Fn>(f);
+  }();
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (!fn || fn(&b, &sz, reinterpret_cast<unsigned long long>(ptr)) != 0) return false;
+  *base = reinterpret_cast<char*>(b);
+  *size = sz;
+  return true;
 }
 
 size_t dtype_size(int dt) {
@@ -652,6 +701,7 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
     long long v = 0;
     comm->pull_slice = env_int("PAT_PULL_SLICE", &v) && v >= 256 ? (v & ~15LL) : (512 << 10);
     comm->skew = env_int("PAT_SKEW", &v) ? static_cast<int>(std::max(0LL, v)) : 1;
+    comm->leaves_first = env_int("PAT_LEAVES_FIRST", &v) ? static_cast<int>(v != 0) : 1;
     // the polling protocols need depth >= 2 (deferred credit, transport.cuh); they do not skew
     comm->depth_poll = env_int("PAT_POLL_DEPTH", &v) ? static_cast<int>(v) : c.depth;
     comm->depth_poll = std::min(std::max(comm->depth_poll, 2), c.depth);
@@ -731,7 +781,7 @@ uint64_t config_fingerprint(const patComm* comm) {
   const patConfig_t& c = comm->cfg;
   const uint64_t v[] = {c.staging_bytes, c.slice_bytes, c.ll_threshold, uint64_t(c.trees), uint64_t(c.max_channels),
                         uint64_t(c.protocol), uint64_t(c.threads), uint64_t(c.depth), uint64_t(c.direct),
-                        uint64_t(c.send_warps), uint64_t(c.fused), uint64_t(comm->skew), uint64_t(comm->pull_slice),
+                        uint64_t(c.send_warps), uint64_t(c.fused), uint64_t(comm->skew), uint64_t(comm->leaves_first), uint64_t(comm->pull_slice),
                         comm->slot_bytes, comm->ll_slot_bytes, comm->ll32_slot_bytes, comm->pool_bytes,
                         comm->region_off[kProtoLL], comm->region_off[kProtoLL32], comm->epoch_mask,
                         comm->iter_start, uint64_t(comm->depth_poll)};
@@ -746,6 +796,14 @@ uint64_t config_fingerprint(const patComm* comm) {
 bool fused_path(const patComm* comm, const Compiled* cp) {
   return !comm->multiprocess && comm->groups.size() == 1 && comm->cfg.fused >= 0 && cp->fused_ok &&
          static_cast<int>(comm->groups[0].lidx.size()) == comm->n;
+}
+
+// The symmetric window holding [ptr, ptr + bytes), if any.
+const patComm::Window* find_window(const patComm* comm, const void* ptr, int64_t bytes) {
+  const char* q = static_cast<const char*>(ptr);
+  for (const auto& w : comm->windows)
+    if (q >= w.local && q + bytes <= w.local + w.bytes) return &w;
+  return nullptr;
 }
 
 // Inbox slots one pipeline step occupies at a receiver.
@@ -790,9 +848,18 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   const bool single_device = !comm->multiprocess && comm->groups.size() == 1;
   // PULL reads the peers' user buffers: they must be mapped into every device of this process.
   // Auto mode only pulls mid-size reduce-scatters, so small calls skip the pointer queries.
-  bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple &&
+  // One process per rank: zero copy needs the user buffers inside symmetric windows
+  // (patCommRegister*); the peers' buffers are then at the same window offset.
+  const patComm::Window* wsend = nullptr;
+  const patComm::Window* wrecv = nullptr;
+  if (comm->multiprocess && !comm->windows.empty()) {
+    const int64_t sb = kind == kAG ? chunk_bytes : n * chunk_bytes, rb = kind == kAG ? n * chunk_bytes : chunk_bytes;
+    wsend = find_window(comm, sendbuffs[0], sb);
+    wrecv = find_window(comm, recvbuffs[0], rb);
+  }
+  bool pull_ok = (!comm->multiprocess || (wsend && (kind == kRS || wrecv))) && comm->cfg.protocol != patProtoSimple &&
                  (comm->cfg.protocol == patProtoPull || (kind == kRS && chunk_bytes > kPullMinRS));
-  for (size_t l = 0; l < comm->lranks.size() && pull_ok && !single_device; ++l)
+  for (size_t l = 0; l < comm->lranks.size() && pull_ok && !single_device && !comm->multiprocess; ++l)
     pull_ok = legacy_ipc_capable(sendbuffs[l]) && (kind == kRS || legacy_ipc_capable(recvbuffs[l]));
   const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es),
                                     cp->proto.pull_nacc);
@@ -812,12 +879,27 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   if (!fused)
     if (patResult_t e = ensure_pools(comm)) return e;
   bool direct = false;
-  if (kind == kAG && sl.proto == kProtoSimple && !comm->multiprocess && comm->cfg.direct >= 0) {
-    direct = single_device || comm->cfg.direct > 0;
-    if (!direct) {  // auto: cudaMalloc'd recvbufs are reachable through the enabled peer access
-      direct = true;
-      for (size_t l = 0; l < comm->lranks.size() && direct; ++l) direct = legacy_ipc_capable(recvbuffs[l]);
+  if (kind == kAG && sl.proto == kProtoSimple && comm->cfg.direct >= 0) {
+    if (comm->multiprocess) {
+      direct = wrecv != nullptr;  // the peers' recvbufs: same offset of their windows
+    } else {
+      direct = single_device || comm->cfg.direct > 0;
+      if (!direct) {  // auto: cudaMalloc'd recvbufs are reachable through the enabled peer access
+        direct = true;
+        for (size_t l = 0; l < comm->lranks.size() && direct; ++l) direct = legacy_ipc_capable(recvbuffs[l]);
+      }
     }
+  }
+  // window tag the kernels compare at entry (transport.cuh: sym_check)
+  uint64_t sym_tag = 0;
+  if (comm->multiprocess && (direct || sl.proto == kProtoPull)) {
+    auto mix = [](uint64_t h, uint64_t x) { return (h ^ x) * 0x100000001B3ull + (h >> 29); };
+    uint64_t h = 0xcbf29ce484222325ull;
+    if (sl.proto == kProtoPull)
+      h = mix(mix(h, wsend->id), static_cast<uint64_t>(static_cast<const char*>(sendbuffs[0]) - wsend->local));
+    if (direct || (sl.proto == kProtoPull && kind == kAG))
+      h = mix(mix(h, wrecv->id + 0x10000ull), static_cast<uint64_t>(static_cast<char*>(recvbuffs[0]) - wrecv->local));
+    sym_tag = h | 1;
   }
   std::vector<KPlan> plans(comm->groups.size());
   for (size_t gi = 0; gi < comm->groups.size(); ++gi) {
@@ -850,6 +932,7 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.chan_stride = static_cast<int64_t>(p.depth) * (sl.proto == kProtoPull ? std::max<int>(p.pull_nacc, 1) : std::max(n - 1, 1)) *
                     p.slot_stride;
     p.send_warps = comm->cfg.send_warps;
+    p.leaves_first = sl.proto != kProtoPull ? comm->leaves_first : 0;
     p.gpu_scope = single_device ? 1 : 0;
     p.direct = direct && sl.proto != kProtoPull ? 1 : 0;
     if (sl.proto == kProtoPull)
@@ -859,6 +942,17 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       }
     if (direct)
       for (size_t l = 0; l < comm->lranks.size(); ++l) p.peer_recv[comm->lranks[l]] = static_cast<char*>(recvbuffs[l]);
+    p.sym_tag = sym_tag;
+    if (sym_tag) {  // the peers' buffers through their windows
+      const int me = comm->lranks[0];
+      for (int r = 0; r < n; ++r) {
+        if (r == me) continue;
+        if (wsend && sl.proto == kProtoPull)
+          p.peer_send[r] = wsend->peer[r] + (static_cast<const char*>(sendbuffs[0]) - wsend->local);
+        if (wrecv && (direct || kind == kAG))
+          p.peer_recv[r] = wrecv->peer[r] + (static_cast<char*>(recvbuffs[0]) - wrecv->local);
+      }
+    }
     p.timeout_ns = static_cast<uint64_t>(comm->cfg.timeout_ms) * 1000000ull;
     p.epoch_mask = comm->epoch_mask;
     p.depth_poll = comm->depth_poll;
@@ -1132,6 +1226,8 @@ patResult_t patCommDestroy(patComm_t comm) {
       cudaSetDevice(g.device);
       for (void* p : comm->ipc_opened) cudaIpcCloseMemHandle(p);
       comm->ipc_opened.clear();
+      for (auto& kv : comm->ipc_cache) cudaIpcCloseMemHandle(kv.second.first);
+      comm->ipc_cache.clear();
       if (g.iter_state) cudaFree(g.iter_state);
       if (g.trace) cudaFree(g.trace);
     }
@@ -1251,6 +1347,130 @@ patResult_t patCommMemInfo(patComm_t comm, patMemInfo_t* info) {
     info->region_channels[i] = comm->region_channels[order[i]];
     info->region_bytes[i] = comm->region_bytes[order[i]];
     info->slot_bytes[i] = slot[i];
+  }
+  return patSuccess;
+}
+
+patResult_t patCommRegisterPrepare(patComm_t comm, void* buf, size_t bytes, void* handle_out) {
+  if (!comm || !buf || !bytes || !handle_out) return patInvalidArgument;
+  if (!comm->multiprocess || !comm->finished) return patInvalidUsage;
+  std::lock_guard<std::mutex> lock(comm->mu);
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(comm->ldevs[0]));
+  char* base = nullptr;
+  size_t size = 0;
+  if (!allocation_base(buf, &base, &size) || static_cast<char*>(buf) + bytes > base + size) return patInvalidArgument;
+  if (!legacy_ipc_capable(buf)) {
+    std::fprintf(stderr, "pat_b200: patCommRegisterPrepare needs cudaMalloc memory (CUDA IPC)\n");
+    return patInvalidUsage;
+  }
+  RegHandle h{};
+  h.magic = kMagic;
+  h.version = PAT_B200_VERSION;
+  h.nranks = comm->n;
+  h.rank = comm->lranks[0];
+  h.bytes = bytes;
+  h.offset = static_cast<uint64_t>(static_cast<char*>(buf) - base);
+  h.config_hash = comm->config_hash;
+  CUDA_TRY(cudaIpcGetMemHandle(&h.ipc, base));
+  std::memset(handle_out, 0, PAT_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  return patSuccess;
+}
+
+patResult_t patCommRegisterFinish(patComm_t comm, void* buf, const void* all_handles) {
+  if (!comm || !buf || !all_handles) return patInvalidArgument;
+  if (!comm->multiprocess || !comm->finished) return patInvalidUsage;
+  std::lock_guard<std::mutex> lock(comm->mu);
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(comm->ldevs[0]));
+  const int me = comm->lranks[0];
+  std::vector<RegHandle> hs(comm->n);
+  for (int r = 0; r < comm->n; ++r) {
+    std::memcpy(&hs[r], static_cast<const char*>(all_handles) + static_cast<size_t>(r) * PAT_HANDLE_BYTES,
+                sizeof(RegHandle));
+    const RegHandle& h = hs[r];
+    if (h.magic != kMagic || h.version != PAT_B200_VERSION || h.nranks != comm->n || h.rank != r ||
+        h.bytes != hs[0].bytes || h.config_hash != comm->config_hash)
+      return patInvalidUsage;  // every rank registers a window of the same size, in the same order
+  }
+  patComm::Window w;
+  w.local = static_cast<char*>(buf);
+  w.bytes = hs[me].bytes;
+  w.id = comm->next_window++;
+  for (int r = 0; r < comm->n; ++r) {
+    if (r == me) {
+      w.peer[r] = w.local;
+      continue;
+    }
+    std::string key(reinterpret_cast<const char*>(&hs[r].ipc), sizeof(cudaIpcMemHandle_t));
+    auto it = comm->ipc_cache.find(key);
+    if (it == comm->ipc_cache.end()) {  // an allocation is opened once per process, refcounted
+      void* ptr = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&ptr, hs[r].ipc, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (int q = 0; q < r; ++q)  // undo this window's references
+          if (q != me) {
+            auto& ent = comm->ipc_cache[w.key[q]];
+            if (--ent.second == 0) {
+              cudaIpcCloseMemHandle(ent.first);
+              comm->ipc_cache.erase(w.key[q]);
+            }
+          }
+        std::fprintf(stderr, "pat_b200: cudaIpcOpenMemHandle (window of rank %d): %s\n", r, cudaGetErrorString(e));
+        return patUnhandledCudaError;
+      }
+      it = comm->ipc_cache.emplace(key, std::make_pair(static_cast<char*>(ptr), 0)).first;
+    }
+    ++it->second.second;
+    w.key[r] = key;
+    w.peer[r] = it->second.first + hs[r].offset;
+  }
+  comm->windows.push_back(w);
+  return patSuccess;
+}
+
+patResult_t patCommDeregister(patComm_t comm, void* buf) {
+  if (!comm || !buf) return patInvalidArgument;
+  std::lock_guard<std::mutex> lock(comm->mu);
+  DeviceGuard guard;
+  for (size_t i = 0; i < comm->windows.size(); ++i) {
+    if (comm->windows[i].local != buf) continue;
+    CUDA_TRY(cudaSetDevice(comm->ldevs[0]));
+    for (int r = 0; r < comm->n; ++r) {
+      auto it = comm->ipc_cache.find(comm->windows[i].key[r]);
+      if (r == comm->lranks[0] || it == comm->ipc_cache.end()) continue;
+      if (--it->second.second == 0) {
+        cudaIpcCloseMemHandle(it->second.first);
+        comm->ipc_cache.erase(it);
+      }
+    }
+    comm->windows.erase(comm->windows.begin() + static_cast<std::ptrdiff_t>(i));
+    return patSuccess;
+  }
+  return patInvalidArgument;
+}
+
+patResult_t patCommBarrier(patComm_t comm, const patStream_t* streams) {
+  if (!comm || !comm->finished) return patInvalidUsage;
+  if (patResult_t e = check_async(comm)) return e;
+  std::lock_guard<std::mutex> lock(comm->mu);
+  DeviceGuard guard;
+  ++comm->barrier_seq;
+  if (comm->groups.size() == 1 && !comm->multiprocess) return patSuccess;  // one device: stream order
+  if (patResult_t e = ensure_pools(comm)) return e;
+  for (const DevGroup& g : comm->groups) {
+    BPlan b{};
+    for (int r = 0; r < comm->n; ++r) b.bar[r] = reinterpret_cast<uint64_t*>(g.pool_view[r] + kBarrierOff);
+    b.nlocal = static_cast<int>(g.lidx.size());
+    for (size_t i = 0; i < g.lidx.size(); ++i) b.rank[i] = comm->lranks[g.lidx[i]];
+    b.n = comm->n;
+    b.gpu = 0;
+    b.seq = comm->barrier_seq;
+    b.timeout_ns = static_cast<uint64_t>(comm->cfg.timeout_ms) * 1000000ull;
+    b.err = comm->err_dev;
+    CUDA_TRY(cudaSetDevice(g.device));
+    CUDA_TRY(launch_barrier(b, streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr));
   }
   return patSuccess;
 }

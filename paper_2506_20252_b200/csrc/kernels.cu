@@ -61,6 +61,25 @@ cudaError_t fill_u64(uint64_t* p, int64_t n, uint64_t v, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// Device-side barrier over the ranks of a communicator (patCommBarrier): every local rank
+// stores the call's sequence number into word `rank` of every peer's barrier words (release),
+// then waits until every peer's word in its own pool reached it (acquire). One CTA per device.
+__global__ void barrier_kernel(const __grid_constant__ BPlan b) {
+  const int i = threadIdx.x;
+  if (i >= b.nlocal * b.n) return;
+  const int R = b.rank[i / b.n], q = i % b.n;
+  if (q == R) return;
+  if (b.gpu) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(b.bar[q] + R), "l"(b.seq) : "memory");
+  else asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(b.bar[q] + R), "l"(b.seq) : "memory");
+  Waiter w{b.timeout_ns, b.err, false, b.gpu != 0};
+  wait_flag(b.bar[R] + q, b.seq, w);
+}
+
+cudaError_t launch_barrier(const BPlan& b, cudaStream_t stream) {
+  barrier_kernel<<<1, 64, 0, stream>>>(b);
+  return cudaGetLastError();
+}
+
 cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.nlocal * plan.channels);

@@ -117,6 +117,59 @@ __global__ void __launch_bounds__(kLocalThreads, 2) local_ag_kernel(const __grid
   }
 }
 
+// All-gather, 32-byte units, one wave: global unit g in [0, n * Cb/32) is unit g % nu of origin
+// g / nu; each thread loads kAgU units (256-bit loads) before storing each to the n outputs
+// (256-bit stores). The broadcast writes n^2 C and reads n C, so it is bound by HBM write
+// bandwidth: tools/local_tune.cu measured 12.5 us at n = 8, 1 MiB against 12.2 us for a
+// write-only kernel of the same byte count (the bulk-copy kernel below: 13.0 us).
+struct V8 {
+  uint32_t w[8];
+};
+__device__ __forceinline__ V8 ld_nc32(const void* p) {
+  V8 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
+                 "=r"(v.w[7])
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st32(void* p, const V8& v) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]),
+               "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+               : "memory");
+}
+constexpr int kFlatThreads = 256;  // flat kernels: 4 CTAs of 256 threads per SM, one wave
+constexpr int kFlatCtasPerSm = 4;
+constexpr int kAgU = 2;
+
+__global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) local_ag32_kernel(const __grid_constant__ LPlan p) {
+  pdl_enter();
+  const int n = p.n;
+  const int64_t Cb = p.chunk_bytes;
+  const int64_t nu = Cb >> 5;
+  const int64_t total = n * nu;
+  const int64_t TT = static_cast<int64_t>(gridDim.x) * kFlatThreads;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kFlatThreads + threadIdx.x; g < total; g += kAgU * TT) {
+    V8 v[kAgU];
+    int o[kAgU];
+    int64_t u[kAgU];
+#pragma unroll
+    for (int k = 0; k < kAgU; ++k) {
+      const int64_t gg = g + k * TT;
+      o[k] = gg < total ? static_cast<int>(gg / nu) : -1;
+      u[k] = gg - static_cast<int64_t>(o[k]) * nu;
+      if (o[k] >= 0) v[k] = ld_nc32(p.send[o[k]] + 32 * u[k]);
+    }
+    for (int r = 0; r < n; ++r)
+#pragma unroll
+      for (int k = 0; k < kAgU; ++k) {
+        if (o[k] < 0) continue;
+        char* dst = p.recv[r] + o[k] * Cb + 32 * u[k];
+        if (dst != p.send[o[k]] + 32 * u[k]) st32(dst, v[k]);  // in place: rank o's own block is there
+      }
+  }
+}
+
 // All-gather through the tensor memory accelerator: one elected thread per CTA streams tiles of
 // the inputs into shared memory with 1-D bulk copies (cp.async.bulk, mbarrier completion) and
 // writes each tile to the n outputs with n bulk stores, NS stages deep. Full-line writes and no
@@ -221,6 +274,30 @@ __device__ __forceinline__ void local_rs_body(const LPlan& p) {
   }
 }
 
+// Reduce-scatter, 16-byte units, one wave: global unit g in [0, n * Cb/16) is unit g % nu of
+// output rank g / nu, its N loads in flight before the tree (tools/local_tune.cu: 11.5 us at
+// n = 8, 1 MiB fp32, against 11.3-12.3 us for the per-rank two-wave grid, which varies with the
+// box; a bulk-copy-staged variant reached only 12.7 us).
+template <int DT, int OP, int N>
+__device__ __forceinline__ void local_rs_flat(const LPlan& p) {
+  const int64_t Cb = p.chunk_bytes;
+  const int64_t nu = Cb >> 4;
+  const int64_t total = N * nu;
+  const int64_t TT = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += TT) {
+    const int r = static_cast<int>(g / nu);
+    const int64_t off = r * Cb + 16 * (g - r * nu);
+    uint4 x[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      int s = r + j;
+      s = s >= N ? s - N : s;
+      x[j] = ld_nc16(p.send[s] + off);
+    }
+    st_cs16(p.recv[r] + (off - r * Cb), tree<DT, OP, N>(x));
+  }
+}
+
 template <int DT, int OP>
 __global__ void __launch_bounds__(kLocalThreads, 2) local_rs_kernel(const __grid_constant__ LPlan p) {
   pdl_enter();
@@ -236,12 +313,35 @@ __global__ void __launch_bounds__(kLocalThreads, 2) local_rs_kernel(const __grid
   }
 }
 
+template <int DT, int OP>
+__global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) local_rs_flat_kernel(const __grid_constant__ LPlan p) {
+  pdl_enter();
+  switch (p.n) {
+    case 1: local_rs_flat<DT, OP, 1>(p); break;
+    case 2: local_rs_flat<DT, OP, 2>(p); break;
+    case 3: local_rs_flat<DT, OP, 3>(p); break;
+    case 4: local_rs_flat<DT, OP, 4>(p); break;
+    case 5: local_rs_flat<DT, OP, 5>(p); break;
+    case 6: local_rs_flat<DT, OP, 6>(p); break;
+    case 7: local_rs_flat<DT, OP, 7>(p); break;
+    default: local_rs_flat<DT, OP, 8>(p); break;
+  }
+}
+
 using LocalFn = void (*)(const LPlan);
 #define PAT_LRS_ROW(DT) \
   { local_rs_kernel<DT, kSum>, local_rs_kernel<DT, kProd>, local_rs_kernel<DT, kMax>, local_rs_kernel<DT, kMin> }
 static const LocalFn kLocalRs[10][4] = {
     PAT_LRS_ROW(kI8), PAT_LRS_ROW(kU8), PAT_LRS_ROW(kI32), PAT_LRS_ROW(kU32), PAT_LRS_ROW(kI64),
     PAT_LRS_ROW(kU64), PAT_LRS_ROW(kF16), PAT_LRS_ROW(kF32), PAT_LRS_ROW(kF64), PAT_LRS_ROW(kBF16)};
+#define PAT_LRSF_ROW(DT)                                                                             \
+  {                                                                                                  \
+    local_rs_flat_kernel<DT, kSum>, local_rs_flat_kernel<DT, kProd>, local_rs_flat_kernel<DT, kMax>, \
+        local_rs_flat_kernel<DT, kMin>                                                               \
+  }
+static const LocalFn kLocalRsFlat[10][4] = {
+    PAT_LRSF_ROW(kI8), PAT_LRSF_ROW(kU8), PAT_LRSF_ROW(kI32), PAT_LRSF_ROW(kU32), PAT_LRSF_ROW(kI64),
+    PAT_LRSF_ROW(kU64), PAT_LRSF_ROW(kF16), PAT_LRSF_ROW(kF32), PAT_LRSF_ROW(kF64), PAT_LRSF_ROW(kBF16)};
 
 // The tree the fused reduce-scatter evaluates, in the symbolic form comm.cpp produces.
 const char* local_tree_string(int n) {
@@ -300,6 +400,23 @@ cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  // PAT_LOCAL_FLAT=0: the previous kernels (bulk-copy all-gather, per-rank reduce-scatter grid)
+  static const bool flat = [] {
+    const char* e = std::getenv("PAT_LOCAL_FLAT");
+    return !e || std::atoi(e) != 0;
+  }();
+  bool aligned32 = (chunk_bytes % 32) == 0;
+  for (int r = 0; r < n && aligned32; ++r)
+    aligned32 = ((reinterpret_cast<uintptr_t>(p.send[r]) | reinterpret_cast<uintptr_t>(p.recv[r])) % 32) == 0;
+  const int64_t units = n * (chunk_bytes >> (kind == 0 ? 5 : 4));
+  const int flat_grid = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(int64_t{kFlatCtasPerSm} * sm_count, (units + kFlatThreads - 1) / kFlatThreads)));
+  if (flat && vec == 16 && (kind == 1 || aligned32)) {
+    cfg.gridDim = dim3(flat_grid);
+    cfg.blockDim = dim3(kFlatThreads);
+    if (kind == 0) return cudaLaunchKernelEx(&cfg, local_ag32_kernel, p);
+    return cudaLaunchKernelEx(&cfg, kLocalRsFlat[dtype][op], p);
+  }
   if (kind == 0 && tma_piece && vec == 16) {
     const int smem = kTmaStages * tma_piece;
     if (smem > 48 * 1024)  // per device; only for tiles set above the default through the env

@@ -17,7 +17,8 @@ constexpr int kMaxLocal = 8;    // ranks driven by one kernel (local mode)
 constexpr int kMaxChannels = 128;
 constexpr int kMaxThreads = 512;  // per CTA: 128 registers per thread for the unrolled SIMPLE loops
 constexpr int kFlagWords = 32;  // per channel: data flag per round [0,8), done-from per rank [8,16),
-                                // ready-from per rank [16,24) (direct mode entry handshake)
+                                // ready-from per rank [16,24) (direct mode entry handshake),
+                                // window tag from each rank [24,32) (symmetric windows)
 
 // (4 is retired: LL128, 128-byte lines with one flag word, was measured to tear over NVLink —
 // a line's flag sector can land before its data sectors — and was removed. LL32's lines are
@@ -57,6 +58,7 @@ struct KPlan {
   int gpu_scope;    // all ranks on this device: flags and fences at .gpu scope instead of .sys
   int direct;       // AG: push straight into the peers' recvbufs (peer_recv), no inbox
   int skew;         // SIMPLE sender runs round t of step k - t in iteration k (needs depth >= nrounds)
+  int leaves_first; // SIMPLE: a step's first task pushes the leaf chunks (no arrivals) of every round
   int64_t chunk_bytes;   // bytes of one rank chunk (AG sendcount*esize, RS recvcount*esize)
   int64_t slice_bytes;   // payload bytes per slot per pipeline step
   int64_t slot_stride;   // inbox bytes per slot
@@ -97,6 +99,19 @@ struct KPlan {
   int poll_channels[2];             // channels of the LL / LL32 regions
   int64_t poll_off[2];              // LL / LL32 region offsets from a pool's base (= flags[rank])
   int64_t poll_slot[2];             // LL / LL32 slot bytes
+  // symmetric windows (multi-process zero copy): the tag (window id, offsets) of the user
+  // buffers this call reads or writes at its peers; 0 = not windowed. Published to the peers
+  // with the entry handshake and compared there (kernels: sym_check)
+  uint64_t sym_tag;
+};
+
+// Device barrier (patCommBarrier): every rank's barrier words, as seen from the launching device.
+struct BPlan {
+  uint64_t* bar[kMaxRanks];  // [kMaxRanks] words of each rank's pool, word q = last seq from rank q
+  int rank[kMaxLocal];
+  int nlocal, n, gpu;
+  uint64_t seq, timeout_ns;
+  int* err;
 };
 
 }  // namespace pat

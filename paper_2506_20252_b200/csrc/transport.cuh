@@ -322,6 +322,21 @@ static __device__ __noinline__ void epoch_clean(const KPlan& p, int R, int c, ui
   }
 }
 
+// Symmetric windows: a rank publishes its call's window tag to every peer before its entry
+// handshake (release) flag; after acquiring peer Q's handshake it checks Q's tag against its own,
+// so a zero-copy access never uses a peer buffer at a different window offset. On a mismatch the
+// call reports patInvalidUsage (5) and moves no data.
+__device__ __forceinline__ void sym_publish(const KPlan& p, int R, int c, int q, bool gpu) {
+  if (p.sym_tag) st_relaxed(p.flags[q] + c * kFlagWords + 24 + R, p.sym_tag, gpu);
+}
+__device__ __forceinline__ bool sym_check(const KPlan& p, int R, int c, int q, Waiter& w) {
+  if (!p.sym_tag || w.aborted) return !w.aborted;
+  if (ld_acquire(p.flags[R] + c * kFlagWords + 24 + q, w.gpu) == p.sym_tag) return true;
+  atomicCAS_system(w.err, 0, 5 /* patInvalidUsage */);
+  w.aborted = true;
+  return false;
+}
+
 // Credits: before pushing step g into a peer's inbox buffer g % depth, the peer must have
 // finished step g - depth (published as done_from[peer] >= g - depth + 1).
 __device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Waiter& w) {
@@ -331,10 +346,13 @@ __device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Wait
 }
 
 // SIMPLE sender role, one PAT round of step s (warps [0, send_warps)). `waited` caches which
-// rounds' arrivals of this step were already acquired.
+// rounds' arrivals of this step were already acquired. `part` selects the round's positions:
+// kAllPos, kLeafPos (chunks that carry no arrival: the own chunk in all-gather, a bare own
+// contribution in reduce-scatter) or kFwdPos (the rest).
+enum : int { kAllPos = 0, kLeafPos = 1, kFwdPos = 2 };
 template <int DT, int OP, int KIND>
 __device__ void send_round(const KPlan& p, const Step& s, int t, uint32_t& waited, Waiter& w, int tid, int nthr,
-                           bool signal) {
+                           bool signal, int part = kAllPos) {
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const char* snd = p.send[s.lr];
@@ -353,6 +371,7 @@ __device__ void send_round(const KPlan& p, const Step& s, int t, uint32_t& waite
     const KRound& r = p.rounds[t];
     const int P = (s.R + r.peer) % n;
     for (int pos = 0; pos < r.nchunks; ++pos) {
+      if (part != kAllPos && (r.narr[pos] == 0) != (part == kLeafPos)) continue;
       int m = 0;
       char* dst;
       if constexpr (KIND == kAG) {
@@ -407,8 +426,13 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
       if (tid == 0 && !p.direct) wait_credits(p, s, w);
       tr.rec(kEvCredit, s.g, 0);
       named_bar(1, nthr);
+      // leaves first: every round's dependency-free chunks go out now, so the link is busy while
+      // the forwards of later rounds wait for their arrivals (each round's flag still follows
+      // all of its positions: it is published after a later fence)
+      if (p.leaves_first)
+        for (int t2 = 0; t2 < NR; ++t2) send_round<DT, OP, KIND>(p, s, t2, wm, w, tid, nthr, false, kLeafPos);
     }
-    send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr, signal);
+    send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr, signal, p.leaves_first ? kFwdPos : kAllPos);
     tr.rec(kEvPushed, s.g, t);
     if (signal && t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
   };
@@ -503,6 +527,9 @@ __device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int
 // only ever waits on lines it polls itself — no CTA barrier inside the step.
 template <int DT, int OP, int KIND>
 __device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
+  // leaves first (p.leaves_first): pass 0 pushes every round's chunks that carry no arrival,
+  // pass 1 the forwards; otherwise one pass over all positions in round order
+  const int passes = p.leaves_first ? 2 : 1;
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const char* snd = p.send[s.lr];
@@ -518,10 +545,12 @@ __device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
         store_word(out + s.R * Cb + s.off + 8 * q, load_word(snd + s.off + 8 * q, valid, p), valid, p);
       }
   }
+  for (int pass = 0; pass < passes; ++pass)
   for (int t = 0; t < p.nrounds; ++t) {
     const KRound& r = p.rounds[t];
     const int P = (s.R + r.peer) % n;
     for (int pos = 0; pos < r.nchunks; ++pos) {
+      if (passes == 2 && (r.narr[pos] == 0) != (pass == 0)) continue;
       char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
       if constexpr (KIND == kAG) {
         const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
@@ -594,6 +623,9 @@ struct Line32 {
 // Hash of a line's payload words: a sum of distinct odd multiples (7 IMADs), so a change of any
 // single word always changes it and the all-zero line (a zeroed or re-stamped pool) hashes to 0.
 __host__ __device__ __forceinline__ uint32_t line_hash(const Line32& v) {
+#ifdef PAT_LL32_NOHASH  // A/B builds only (tools/build_variant.sh): the flag alone, no integrity check
+  return 0 * v.w[0];
+#endif
   return v.w[0] * 0x9E3779B1u + v.w[1] * 0x85EBCA77u + v.w[2] * 0xC2B2AE3Du + v.w[3] * 0x27D4EB2Fu +
          v.w[4] * 0x165667B1u + v.w[5] * 0xD3A2646Du + v.w[6] * 0xFD7046C5u;
 }
@@ -732,7 +764,7 @@ __device__ __forceinline__ void fold_line32(Line32& a, const Line32& b) {
 // finishes the step (all-gather: own chunk placement and delivery of every slot; reduce-scatter:
 // the output fold). The same rounds, slots and fold order as step_ll.
 template <int DT, int OP, int KIND, int U>
-__device__ void ll32_phase(const KPlan& p, const Step& s, int t, Waiter& w) {
+__device__ void ll32_phase(const KPlan& p, const Step& s, int t, Waiter& w, int part = kAllPos) {
   constexpr int G = LL32Shape<U>::G;
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
@@ -751,6 +783,7 @@ __device__ void ll32_phase(const KPlan& p, const Step& s, int t, Waiter& w) {
     const KRound& r = p.rounds[t];
     const int P = (s.R + r.peer) % n;
     for (int pos = 0; pos < r.nchunks; ++pos) {
+      if (part != kAllPos && (r.narr[pos] == 0) != (part == kLeafPos)) continue;
       char* dst = slot_ptr(p, P, s.c, s.buf, r.slot_base + pos);
       if constexpr (KIND == kAG) {
         const char* fwd = r.narr[pos] ? slot_ptr(p, s.R, s.c, s.buf, r.arr[pos][0]) : nullptr;
@@ -852,11 +885,23 @@ __device__ void pull_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
   const int tid = threadIdx.x, nthr = blockDim.x;
   const bool gpu = p.gpu_scope != 0;
   uint64_t* myflags = chan_flags(p, R, c);
+  __shared__ int s_abort;
   // entry: my sendbuf (and, for AG, recvbuf) are final once this stream reached the call
-  if (tid < n && tid != R) st_release(chan_flags(p, tid, c) + 16 + R, base + 1, gpu);
-  if (tid == 0)
-    for (int t = 0; t < NR; ++t) wait_flag(myflags + 16 + (R - p.rounds[t].peer + n) % n, base + 1, w);
+  if (tid < n && tid != R) {
+    sym_publish(p, R, c, tid, gpu);
+    st_release(chan_flags(p, tid, c) + 16 + R, base + 1, gpu);
+  }
+  if (tid == 0) {
+    bool ok = true;
+    for (int t = 0; t < NR; ++t) {
+      const int Q = (R - p.rounds[t].peer + n) % n;
+      wait_flag(myflags + 16 + Q, base + 1, w);
+      ok = sym_check(p, R, c, Q, w) && ok;
+    }
+    s_abort = !ok;
+  }
   __syncthreads();
+  if (s_abort) return;
   auto task = [&](int i, int t) {
     const Step s = make_step(p, base, i, R, lr, c);
     if (tid == 0) {
@@ -938,12 +983,22 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
 
   if (p.direct && KIND == kAG) {
     // entry handshake: a peer may be written directly only once it entered this call
-    if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
+    __shared__ int s_abort;
+    if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R) {
+      sym_publish(p, R, c, threadIdx.x, w.gpu);
       st_release(chan_flags(p, threadIdx.x, c) + 16 + R, base + 1, w.gpu);
-    if (threadIdx.x == 0)
-      for (int k = 0; k < p.npeers; ++k)
-        wait_flag(chan_flags(p, R, c) + 16 + (R + p.peers[k]) % p.n, base + 1, w);
+    }
+    if (threadIdx.x == 0) {
+      bool ok = true;
+      for (int k = 0; k < p.npeers; ++k) {
+        const int P = (R + p.peers[k]) % p.n;
+        wait_flag(chan_flags(p, R, c) + 16 + P, base + 1, w);
+        ok = sym_check(p, R, c, P, w) && ok;
+      }
+      s_abort = !ok;
+    }
     __syncthreads();
+    if (s_abort) return;
   }
 
   if (p.proto == kProtoPull) {
@@ -965,7 +1020,13 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
       if (p.proto == kProtoLL) {
         step_ll<DT, OP, KIND>(p, s, w);
       } else {
-        for (int t = 0; t <= p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w);
+        if (p.leaves_first) {  // every round's leaf lines, then the forwards, then the finish
+          for (int t = 0; t < p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w, kLeafPos);
+          for (int t = 0; t < p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w, kFwdPos);
+          ll32_phase<DT, OP, KIND, U>(p, s, p.nrounds, w);
+        } else {
+          for (int t = 0; t <= p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w);
+        }
       }
       const bool clean = epoch_clean_due(p, s.g);
       if (clean) {  // every load of this step's lines returned before the barrier above it

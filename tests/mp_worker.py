@@ -14,6 +14,62 @@ import oracle as O  # noqa: E402
 from paper_2506_20252_b200 import PatComm  # noqa: E402
 
 
+def windows_section(rank, n, dev):
+    """Symmetric windows (patCommRegister*): zero-copy direct all-gather, PULL reduce-scatter and
+    PULL all-gather across processes, bit-exact; then a rank-dependent offset must be refused."""
+    fails = 0
+    elems = (1 << 20) + 7
+    pad = 4096  # buffers sit at byte offset `pad` inside their windows, equal on every rank
+    win_s = torch.zeros(n * elems * 4 + 2 * pad, dtype=torch.uint8, device=dev)
+    win_r = torch.zeros(n * elems * 4 + 2 * pad, dtype=torch.uint8, device=dev)
+    for proto in (0, 2, 3):  # auto, SIMPLE (direct all-gather), PULL
+        comm = PatComm.from_process_group(device=local_of(dev), protocol=proto)
+        comm.register(win_s)
+        comm.register(win_r)
+        for dt in (O.FLOAT32, O.INT32):
+            p = O.random_payload(dt, n, elems, 77 + proto + dt)
+            mine = p[rank * elems:(rank + 1) * elems]
+            s = win_s[pad:pad + elems * 4]
+            s.copy_(torch.from_numpy(mine.copy().view(np.uint8)))
+            r = win_r[pad:pad + n * elems * 4]
+            comm.all_gather([s], [r], elems, dt)
+            torch.cuda.synchronize(dev)
+            want, _ = O.run_allgather(O.pat_allgather(n, O.max_trees(n)), dt, p, elems)
+            if r.cpu().numpy().tobytes() != want[rank].tobytes():
+                fails += 1
+                print(f"rank {rank} windowed AG mismatch proto={proto} dt={dt}", flush=True)
+            q = O.random_payload(dt, n * n, elems, 99 + proto + dt)
+            s = win_s[pad:pad + n * elems * 4]
+            s.copy_(torch.from_numpy(q[rank * n * elems:(rank + 1) * n * elems].copy().view(np.uint8)))
+            r = win_r[pad:pad + elems * 4]
+            comm.reduce_scatter([s], [r], elems, dt, O.SUM)
+            torch.cuda.synchronize(dev)
+            want, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, O.max_trees(n)), dt, O.SUM, q, elems)
+            if r.cpu().numpy().tobytes() != want[rank].tobytes():
+                fails += 1
+                print(f"rank {rank} windowed RS mismatch proto={proto} dt={dt}", flush=True)
+        comm.raise_async_error()
+        comm.deregister(win_r)
+        comm.deregister(win_s)
+        comm.destroy()
+    # rank-dependent offsets: the entry check refuses the zero-copy call on the ranks that see it
+    comm = PatComm.from_process_group(device=local_of(dev), protocol=2, timeout_ms=3000)
+    comm.register(win_r)
+    off = pad + 16 * rank
+    s = torch.zeros(elems * 4, dtype=torch.uint8, device=dev)
+    comm.all_gather([s], [win_r[off:off + n * elems * 4]], elems, O.FLOAT32)
+    torch.cuda.synchronize(dev)
+    if comm.async_error() == 0:
+        fails += 1
+        print(f"rank {rank} mismatched window offsets were not refused", flush=True)
+    comm.destroy()
+    return fails
+
+
+def local_of(dev):
+    return dev.index
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
@@ -84,6 +140,7 @@ def main():
             print(f"rank {rank} reduce_scatter_tensor differs from the oracle elems={elems}", flush=True)
     comm.raise_async_error()
     comm.destroy()
+    fails += windows_section(rank, n, dev)
     t = torch.tensor([fails], device=dev)
     dist.all_reduce(t)
     if rank == 0:
