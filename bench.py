@@ -183,14 +183,14 @@ class ClockSampler:
             time.sleep(0.002)
 
     def __enter__(self):
-        if self.ok:
+        if self.ok and not os.environ.get("BENCH_NO_CLOCKS"):
             self._sample()  # at least one sample inside a short timed region
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         return self
 
     def __exit__(self, *a):
-        if self.ok:
+        if self.ok and hasattr(self, "_t"):
             self._stop.set()
             self._t.join()
 
@@ -319,6 +319,8 @@ def run_pat(args, rank, world, local):
             with torch.cuda.device(d), torch.cuda.stream(D.streams[d]):
                 torch.cuda._sleep(int(os.environ.get("BENCH_SLEEP_CYCLES", "200000")))
     D.pre = pre
+    pre()  # loads the flush / spin kernels' modules now (lazy loading), not inside a timed region's prologue
+    D.barrier()
     g = {d: torch.Generator(device=f"cuda:{d}").manual_seed(1234 + 17 * rank + d) for d in D.devs}
 
     def rnd(numel, d):
@@ -388,6 +390,9 @@ def run_pat(args, rank, world, local):
     dbg("timed")
     with ClockSampler(D.devs) as clocks:
         step_ms = D.time_ms(replay_k(graphs[("ag", "rs")]))
+        if os.environ.get("BENCH_TRIALS"):  # diagnostics: more timed regions of the same K steps
+            extra = [D.time_ms(replay_k(graphs[("ag", "rs")])) for _ in range(int(os.environ["BENCH_TRIALS"]))]
+            dbg(f"step trials (us/step): {[round(1e3 * x / K, 2) for x in [step_ms] + extra]}")
         ag_ms = D.time_ms(replay_k(graphs[("ag",)]))
         rs_ms = D.time_ms(replay_k(graphs[("rs",)]))
     comm.raise_async_error()

@@ -33,6 +33,10 @@ def main():
     ap.add_argument("--ranks", type=int, default=8, help="logical ranks when run without torchrun")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--protocol", type=int, default=0)
+    ap.add_argument("--algos", default="pat", help="pat,ring: schedules run on the PAT transport "
+                    "(ring = ring_allgather / its mirror through the generic executor, impl 'pat-ring')")
+    ap.add_argument("--windows", action="store_true",
+                    help="torchrun: user buffers inside registered symmetric windows (zero copy)")
     ap.add_argument("--trials", type=int, default=5, help="graph mode: timed replays per point (median)")
     ap.add_argument("--mode", default="loop", choices=["loop", "events", "graph"],
                     help="loop: K back-to-back calls between two events (nccl-tests style); events: one "
@@ -43,6 +47,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2506_20252_b200 import BFLOAT16, FLOAT32, SUM, PatComm
+    from paper_2506_20252_b200 import schedule as S
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -62,6 +67,18 @@ def main():
         L = n
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    win = None
+    if args.windows and world > 1:  # one pair of windows for every size, buffers at offset 0
+        wbytes = (n + 1) * args.max_bytes + 4096
+        win = (torch.empty(wbytes, dtype=torch.uint8, device=dev), torch.empty(wbytes, dtype=torch.uint8, device=dev))
+        comm.register(win[0])
+        comm.register(win[1])
+    scheds = {}
+    for a in args.algos.split(","):
+        if a == "ring":
+            scheds["pat-ring"] = (S.ring_allgather(n), S.mirror_schedule(S.ring_allgather(n)))
+        else:
+            scheds["pat"] = (None, None)
     dts = {"f32": (torch.float32, FLOAT32), "bf16": (torch.bfloat16, BFLOAT16)}
     out = open(args.out, "w") if rank == 0 else None
 
@@ -139,22 +156,31 @@ def main():
                 break
             big = C >= (1 << 20)
             for coll in args.colls.split(","):
-                if coll == "ag":
+                if win is not None:
+                    sn, rn = (elems, n * elems) if coll == "ag" else (n * elems, elems)
+                    s = [win[0][:sn * es].view(tdt)]
+                    r = [win[1][:rn * es].view(tdt)]
+                    s[0].fill_(1)
+                elif coll == "ag":
                     s = [torch.ones(elems, dtype=tdt, device=dev) for _ in range(L)]
                     r = [torch.empty(n * elems, dtype=tdt, device=dev) for _ in range(L)]
-                    fn = lambda: comm.all_gather(s, r, elems, pdt)
                 else:
                     s = [torch.ones(n * elems, dtype=tdt, device=dev) for _ in range(L)]
                     r = [torch.empty(elems, dtype=tdt, device=dev) for _ in range(L)]
-                    fn = lambda: comm.reduce_scatter(s, r, elems, pdt, SUM)
-                us = timed(fn, big)
-                rec = {"coll": coll, "impl": "pat", "n": n, "gpus": world, "dtype": dname,
-                       "bytes_per_rank": elems * es, "us": us,
-                       "busbw_gbs": (n - 1) * elems * es / (us * 1e-6) / 1e9,
-                       "plan": comm.plan(0 if coll == "ag" else 1, elems, pdt), "forced": args.protocol}
-                if out:
-                    out.write(json.dumps(rec) + "\n")
-                    out.flush()
+                for impl, (sag, srs) in scheds.items():
+                    if coll == "ag":
+                        fn = lambda sc=sag: comm.all_gather(s, r, elems, pdt, schedule=sc)
+                    else:
+                        fn = lambda sc=srs: comm.reduce_scatter(s, r, elems, pdt, SUM, schedule=sc)
+                    us = timed(fn, big)
+                    rec = {"coll": coll, "impl": impl + ("-win" if win is not None else ""), "n": n, "gpus": world,
+                           "dtype": dname, "bytes_per_rank": elems * es, "us": us,
+                           "busbw_gbs": (n - 1) * elems * es / (us * 1e-6) / 1e9,
+                           "plan": comm.plan(0 if coll == "ag" else 1, elems, pdt) if impl == "pat" else None,
+                           "forced": args.protocol}
+                    if out:
+                        out.write(json.dumps(rec) + "\n")
+                        out.flush()
                 if world > 1 and not args.no_nccl:
                     if coll == "ag":
                         nfn = lambda: dist.all_gather_into_tensor(r[0], s[0])

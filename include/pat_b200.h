@@ -205,6 +205,11 @@ patResult_t patCommLocalRanks(patComm_t comm, int* nlocal, int* ranks, int* devi
  * 32..39 round. Synchronises the device. */
 patResult_t patCommTraceRead(patComm_t comm, int group, void* host, size_t cap, size_t* out_bytes, int* ctas,
                              int* entries);
+/* Intermediate-slot occupancy after every round, counted by the device during the last SIMPLE
+ * launch (first pipeline step, channel 0) of a communicator created with PAT_STATS=1 in the
+ * environment: occupancy[l * 8 + t] for local rank l, round t < *nrounds — the reference's
+ * ExecStats.occupancy_per_round (simulate.hpp:43-53), measured instead of replayed. Synchronises. */
+patResult_t patCommStatsRead(patComm_t comm, int32_t* occupancy, int* nlocal, int* nrounds);
 /* Device-reported asynchronous error (timeouts); readable without synchronising. */
 patResult_t patCommGetAsyncError(patComm_t comm, patResult_t* async_error);
 patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDataType_t dtype,

@@ -128,7 +128,7 @@ SYMBOLS = [
     "patReduceScatter", "patAllGatherSchedule", "patReduceScatterSchedule", "patScheduleBuild",
     "patScheduleMirror", "patScheduleValidate", "patScheduleStats", "patScheduleTraceCsv",
     "patMaxTrees", "patTreesFromBuffer", "patPatBufferSlots", "patRoundCountFormula", "patCommTraceRead",
-    "patCommMemInfo", "patCommRegisterPrepare", "patCommRegisterFinish", "patCommDeregister", "patCommBarrier",
+    "patCommMemInfo", "patCommRegisterPrepare", "patCommRegisterFinish", "patCommDeregister", "patCommBarrier", "patCommStatsRead",
 ]
 
 _lib = None
@@ -180,6 +180,7 @@ def lib() -> ctypes.CDLL:
         L.patCommRegisterFinish.argtypes = [VP, VP, VP]
         L.patCommDeregister.argtypes = [VP, VP]
         L.patCommBarrier.argtypes = [VP, PP]
+        L.patCommStatsRead.argtypes = [VP, I32P, IP, IP]
         _lib = L
     return _lib
 

@@ -288,6 +288,14 @@ class PatComm:
                                      ctypes.byref(ctas), ctypes.byref(ent)), "patCommTraceRead")
         return buf.reshape(ctas.value, 2, ent.value, 2)
 
+    def device_occupancy(self) -> list:
+        """Per local rank: intermediate slots held after every round, as counted by the device in
+        the last SIMPLE launch (communicator created with PAT_STATS=1; patCommStatsRead)."""
+        buf = (ctypes.c_int32 * (_lib.MAX_RANKS * 8))()
+        nl, nr = ctypes.c_int(), ctypes.c_int()
+        check(lib().patCommStatsRead(self._h, buf, ctypes.byref(nl), ctypes.byref(nr)), "patCommStatsRead")
+        return [list(buf[l * 8:l * 8 + nr.value]) for l in range(nl.value)] if nr.value >= 0 else []
+
     def async_error(self) -> int:
         e = ctypes.c_int()
         check(lib().patCommGetAsyncError(self._h, ctypes.byref(e)), "patCommGetAsyncError")

@@ -88,6 +88,8 @@ struct DevGroup {
   uint64_t* trace = nullptr;       // PAT_TRACE: [lidx.size() * kMaxChannels][2 roles][cap][2]
   int trace_cap = 0;
   int trace_ctas = 0;              // CTAs of the last traced launch
+  int* occ = nullptr;              // PAT_STATS: [lidx.size()][2][kMaxRounds] live occupancy counters
+  int occ_rounds = -1;             // rounds of the last SIMPLE launch that filled them
   int sm_count = 0;
   std::array<char*, kMaxRanks> pool_view{};  // every rank's pool as seen from this device
 };
@@ -155,7 +157,8 @@ struct patComm {
   size_t pools_allocated = 0;  // bytes of inbox pool this process allocated (all its ranks)
   int64_t pull_slice = 0;  // all-gather PULL slice (no staging, so not bounded by the slots)
   int skew = 1;            // SIMPLE / PULL sender skew distance (PAT_SKEW; 0 = rounds in order)
-  int leaves_first = 1;    // push senders send every round's leaf chunks first (PAT_LEAVES_FIRST)
+  int leaves_first = -1;   // push senders send every round's leaf chunks first (PAT_LEAVES_FIRST:
+                           // 1 always, 0 never, default: single-step SIMPLE calls only)
   uint64_t epoch_mask = (1ull << 31) - 1;  // LL / LL32 flag epochs (PAT_EPOCH_SHIFT, tests)
   uint64_t iter_start = 0;                 // first pipeline step of every channel (PAT_ITER_START, tests)
   uint64_t barrier_seq = 0;                // patCommBarrier calls so far
@@ -701,7 +704,7 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
     long long v = 0;
     comm->pull_slice = env_int("PAT_PULL_SLICE", &v) && v >= 256 ? (v & ~15LL) : (512 << 10);
     comm->skew = env_int("PAT_SKEW", &v) ? static_cast<int>(std::max(0LL, v)) : 1;
-    comm->leaves_first = env_int("PAT_LEAVES_FIRST", &v) ? static_cast<int>(v != 0) : 1;
+    comm->leaves_first = env_int("PAT_LEAVES_FIRST", &v) ? static_cast<int>(v != 0) : -1;
     // the polling protocols need depth >= 2 (deferred credit, transport.cuh); they do not skew
     comm->depth_poll = env_int("PAT_POLL_DEPTH", &v) ? static_cast<int>(v) : c.depth;
     comm->depth_poll = std::min(std::max(comm->depth_poll, 2), c.depth);
@@ -751,6 +754,12 @@ patResult_t setup_groups(patComm* comm) {
     if (comm->iter_start) {
       CUDA_TRY(fill_u64(g.iter_state, static_cast<int64_t>(kMaxChannels * g.lidx.size()), comm->iter_start, nullptr));
       CUDA_TRY(cudaDeviceSynchronize());
+    }
+    long long stats = 0;
+    if (env_int("PAT_STATS", &stats) && stats > 0) {  // device-counted occupancy (patCommStatsRead)
+      const size_t ob = sizeof(int) * 2 * kMaxRounds * g.lidx.size();
+      CUDA_TRY(cudaMalloc(&g.occ, ob));
+      CUDA_TRY(cudaMemset(g.occ, 0, ob));
     }
     long long tcap = 0;
     if (env_int("PAT_TRACE", &tcap) && tcap > 0) {  // device event trace for tools/trace.py
@@ -932,7 +941,12 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.chan_stride = static_cast<int64_t>(p.depth) * (sl.proto == kProtoPull ? std::max<int>(p.pull_nacc, 1) : std::max(n - 1, 1)) *
                     p.slot_stride;
     p.send_warps = comm->cfg.send_warps;
-    p.leaves_first = sl.proto != kProtoPull ? comm->leaves_first : 0;
+    // leaves first (r02 A/B, n = 4 all-gather, profiles/r02_leaves_first_n4.jsonl): +7% for a
+    // one-step SIMPLE call (32 MiB), -1 to -5% for LL32 and multi-step SIMPLE (the skewed
+    // wavefront already keeps the link busy), so by default only single-step SIMPLE calls
+    p.leaves_first = sl.proto == kProtoPull ? 0
+                     : comm->leaves_first >= 0 ? comm->leaves_first
+                                                : (sl.proto == kProtoSimple && sl.iters == 1 ? 1 : 0);
     p.gpu_scope = single_device ? 1 : 0;
     p.direct = direct && sl.proto != kProtoPull ? 1 : 0;
     if (sl.proto == kProtoPull)
@@ -963,6 +977,14 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.poll_slot[0] = static_cast<int64_t>(comm->ll_slot_bytes);
     p.poll_slot[1] = static_cast<int64_t>(comm->ll32_slot_bytes);
     p.err = comm->err_dev;
+    p.occ = nullptr;
+    if (g.occ && sl.proto == kProtoSimple) {
+      p.occ = g.occ;
+      g.occ_rounds = p.nrounds;
+      CUDA_TRY(cudaSetDevice(g.device));
+      CUDA_TRY(cudaMemsetAsync(g.occ, 0, sizeof(int) * 2 * kMaxRounds * g.lidx.size(),
+                               streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr));
+    }
     p.trace = g.trace;
     p.trace_cap = g.trace_cap;
     if (g.trace) {
@@ -1230,6 +1252,7 @@ patResult_t patCommDestroy(patComm_t comm) {
       comm->ipc_cache.clear();
       if (g.iter_state) cudaFree(g.iter_state);
       if (g.trace) cudaFree(g.trace);
+      if (g.occ) cudaFree(g.occ);
     }
     for (size_t l = 0; l < comm->owned_pool.size(); ++l) {
       cudaSetDevice(comm->ldevs[l]);
@@ -1273,6 +1296,31 @@ patResult_t patCommTraceRead(patComm_t comm, int group, void* host, size_t cap, 
   CUDA_TRY(cudaSetDevice(g.device));
   CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemcpy(host, g.trace, bytes, cudaMemcpyDeviceToHost));
+  return patSuccess;
+}
+
+patResult_t patCommStatsRead(patComm_t comm, int32_t* occupancy, int* nlocal, int* nrounds) {
+  if (!comm || !occupancy || !nlocal || !nrounds) return patInvalidArgument;
+  std::lock_guard<std::mutex> lock(comm->mu);
+  DeviceGuard guard;
+  *nlocal = static_cast<int>(comm->lranks.size());
+  *nrounds = -1;
+  for (const DevGroup& g : comm->groups) {
+    if (!g.occ) return patInvalidUsage;  // communicator created without PAT_STATS
+    if (g.occ_rounds < 0) continue;
+    std::vector<int> h(2 * kMaxRounds * g.lidx.size());
+    CUDA_TRY(cudaSetDevice(g.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(h.data(), g.occ, sizeof(int) * h.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < g.lidx.size(); ++i) {
+      int live = 0;
+      for (int t = 0; t < kMaxRounds; ++t) {
+        live += h[(i * 2 + 0) * kMaxRounds + t] - h[(i * 2 + 1) * kMaxRounds + t];
+        occupancy[static_cast<size_t>(g.lidx[i]) * kMaxRounds + t] = t < g.occ_rounds ? live : 0;
+      }
+    }
+    *nrounds = g.occ_rounds;
+  }
   return patSuccess;
 }
 

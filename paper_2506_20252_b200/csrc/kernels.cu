@@ -1,5 +1,7 @@
 // kernels.cu — dispatch and launch of the transport kernel (transport.cuh). The kernel
 // templates are instantiated per dtype group in rs_*.cu so the build compiles in parallel.
+#include <cstdlib>
+
 #include "transport.cuh"
 
 namespace pat {
@@ -86,9 +88,16 @@ cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = stream;
+  // Cooperative launch (every CTA co-resident) is needed when several ranks share this grid:
+  // their CTAs wait on each other. With one rank per device a CTA waits only on CTAs of other
+  // devices, so a plain launch is safe and cheaper on the host (PAT_COOP=1 forces cooperative).
+  static const int force_coop = [] {
+    const char* e = std::getenv("PAT_COOP");
+    return e ? std::atoi(e) : -1;
+  }();
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  attr[0].val.cooperative = force_coop >= 0 ? (force_coop != 0) : (plan.nlocal > 1);
   // programmatic dependent launch: scheduled while the stream's previous kernel drains; the
   // kernel waits (griddepcontrol.wait) before touching memory. tools/launch_probe.cu: a
   // cooperative launch in a graph costs 0.99 us back to back, 0.68 us with this attribute.

@@ -103,6 +103,10 @@ struct KPlan {
   // buffers this call reads or writes at its peers; 0 = not windowed. Published to the peers
   // with the entry handshake and compared there (kernels: sym_check)
   uint64_t sym_tag;
+  // PAT_STATS: live intermediate-slot counts of the call's first SIMPLE step on channel 0,
+  // [nlocal][2][kMaxRounds]: slots that became held in round t / were released by round t
+  // (the reference's StatsBuilder occupancy, simulate.cpp:109-129, brute_force.hpp:25-54)
+  int* occ;
 };
 
 // Device barrier (patCommBarrier): every rank's barrier words, as seen from the launching device.

@@ -345,6 +345,45 @@ __device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Wait
   for (int k = 0; k < p.npeers; ++k) wait_flag(mine + 8 + (s.R + p.peers[k]) % p.n, s.g - p.depth + 1, w);
 }
 
+// ------------------------------------------------------------------------- live occupancy
+// (PAT_STATS) Counted by the device as the step runs: the receiver role, once round t's flag is
+// acquired, counts the slots of round t that stay held — all-gather: an arrival a later round
+// forwards (brute_force.hpp occupancy_allgather); reduce-scatter: the first arrival toward an
+// offset opens its accumulator (occupancy_reduce_scatter). The sender role, after pushing round
+// t, counts the slots it released — the last forward of an arrival / the forward that closes an
+// accumulator. Occupancy after round t = sum over rounds <= t of held - released (host).
+__device__ __forceinline__ bool ag_forwarded_after(const KPlan& p, int j, int t) {
+  for (int t2 = t + 1; t2 < p.nrounds; ++t2)
+    for (int q = 0; q < p.rounds[t2].nchunks; ++q)
+      if (p.rounds[t2].narr[q] && p.rounds[t2].arr[q][0] == j) return true;
+  return false;
+}
+static __device__ __noinline__ void occ_arrived(const KPlan& p, int lr, int t) {
+  const KRound& r = p.rounds[t];
+  int held = 0;
+  for (int pos = 0; pos < r.nchunks; ++pos) {
+    const int j = r.slot_base + pos, k = p.slot_offset[j];
+    if (k == 0) continue;
+    if (p.kind == kAG) {
+      held += ag_forwarded_after(p, j, t);
+    } else {
+      bool first = true;
+      for (int j2 = 0; j2 < j; ++j2) first &= p.slot_offset[j2] != k;
+      held += first;
+    }
+  }
+  atomicAdd(p.occ + (lr * 2 + 0) * kMaxRounds + t, held);
+}
+static __device__ __noinline__ void occ_sent(const KPlan& p, int lr, int t) {
+  const KRound& r = p.rounds[t];
+  int released = 0;
+  for (int pos = 0; pos < r.nchunks; ++pos) {
+    if (!r.narr[pos]) continue;
+    released += p.kind == kAG ? !ag_forwarded_after(p, r.arr[pos][0], t) : 1;
+  }
+  atomicAdd(p.occ + (lr * 2 + 1) * kMaxRounds + t, released);
+}
+
 // SIMPLE sender role, one PAT round of step s (warps [0, send_warps)). `waited` caches which
 // rounds' arrivals of this step were already acquired. `part` selects the round's positions:
 // kAllPos, kLeafPos (chunks that carry no arrival: the own chunk in all-gather, a bare own
@@ -433,6 +472,7 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
         for (int t2 = 0; t2 < NR; ++t2) send_round<DT, OP, KIND>(p, s, t2, wm, w, tid, nthr, false, kLeafPos);
     }
     send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr, signal, p.leaves_first ? kFwdPos : kAllPos);
+    if (p.occ && i == 0 && c == 0 && tid == 0) occ_sent(p, lr, t);
     tr.rec(kEvPushed, s.g, t);
     if (signal && t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
   };
@@ -468,7 +508,7 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
 // sender role is also done with this step's inbox — publishes done(g) to every rank.
 template <int DT, int OP, int KIND>
 __device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int nthr,
-                          volatile uint64_t* sent_steps, Tracer& tr) {
+                          volatile uint64_t* sent_steps, Tracer& tr, bool first_step) {
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const char* snd = p.send[s.lr];
@@ -483,7 +523,10 @@ __device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int
     }
   }
   for (int t = 0; t < p.nrounds; ++t) {
-    if (tid == 0) wait_flag(myflags + t, s.g + 1, w);
+    if (tid == 0) {
+      wait_flag(myflags + t, s.g + 1, w);
+      if (p.occ && first_step && s.c == 0) occ_arrived(p, s.lr, t);
+    }
     tr.rec(kEvArrived, s.g, t);
     named_bar(2, nthr);
     if constexpr (KIND == kAG) {
@@ -1054,7 +1097,7 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
       tr.rec(kEvStart, base, 0);
       for (int i = 0; i < p.iters; ++i) {
         const Step s = make_step(p, base, i, R, lr, c);
-        recv_step<DT, OP, KIND>(p, s, w, tid, nrecv, &s_sent, tr);
+        recv_step<DT, OP, KIND>(p, s, w, tid, nrecv, &s_sent, tr, i == 0);
       }
       tr.rec(kEvEnd, base + p.iters, 0);
     }
