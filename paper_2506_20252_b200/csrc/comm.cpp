@@ -941,6 +941,7 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.chan_stride = static_cast<int64_t>(p.depth) * (sl.proto == kProtoPull ? std::max<int>(p.pull_nacc, 1) : std::max(n - 1, 1)) *
                     p.slot_stride;
     p.send_warps = comm->cfg.send_warps;
+    p.region_bytes = static_cast<int64_t>(comm->region_bytes[sl.proto]);
     // leaves first (r02 A/B, n = 4 all-gather, profiles/r02_leaves_first_n4.jsonl): +7% for a
     // one-step SIMPLE call (32 MiB), -1 to -5% for LL32 and multi-step SIMPLE (the skewed
     // wavefront already keeps the link busy), so by default only single-step SIMPLE calls

@@ -107,6 +107,7 @@ struct KPlan {
   // [nlocal][2][kMaxRounds]: slots that became held in round t / were released by round t
   // (the reference's StatsBuilder occupancy, simulate.cpp:109-129, brute_force.hpp:25-54)
   int* occ;
+  int64_t region_bytes;  // bytes of the inbox region this launch uses (bounds checks, PAT_BOUNDS_CHECK builds)
 };
 
 // Device barrier (patCommBarrier): every rank's barrier words, as seen from the launching device.

@@ -39,10 +39,28 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <type_traits>
 
 #include "fold.cuh"
 #include "plan.hpp"
+
+// PAT_BOUNDS_CHECK builds (tools/build_variant.sh bounds -DPAT_BOUNDS_CHECK=1) trap on any inbox
+// slot or user-buffer range outside its allocation: the stand-in for compute-sanitizer's memcheck,
+// which is closed on this GPU pool (profiles/r02_sanitizer.txt).
+#ifdef PAT_BOUNDS_CHECK
+#define PAT_BOUND(cond)                                                                              \
+  do {                                                                                               \
+    if (!(cond)) {                                                                                   \
+      printf("pat bounds: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x, threadIdx.x); \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#else
+#define PAT_BOUND(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 namespace pat {
 
@@ -276,15 +294,23 @@ __device__ __forceinline__ Step make_step(const KPlan& p, uint64_t base, int i, 
   s.lr = lr;
   s.c = c;
   s.buf = static_cast<int>(s.g % static_cast<uint64_t>(p.depth));
+  PAT_BOUND(s.len == 0 || (s.off >= 0 && s.off + s.len <= p.chunk_bytes));
+  PAT_BOUND(s.len <= p.slice_bytes);
   return s;
 }
 
+
 __device__ __forceinline__ char* slot_ptr(const KPlan& p, int rank, int c, int buf, int j) {
+  PAT_BOUND(rank >= 0 && rank < p.n && c >= 0 && c < p.channels && buf >= 0 && buf < p.depth && j >= 0 &&
+            j < p.nslots);
+  PAT_BOUND(c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j + 1) * p.slot_stride <= p.region_bytes);
   return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j) * p.slot_stride;
 }
 
 // PULL staging: accumulator `a` of buffer `buf` (pull_nacc accumulators per buffer)
 __device__ __forceinline__ char* acc_ptr(const KPlan& p, int rank, int c, int buf, int a) {
+  PAT_BOUND(rank >= 0 && rank < p.n && a >= 0 && a < p.pull_nacc && buf >= 0 && buf < p.depth);
+  PAT_BOUND(c * p.chan_stride + (static_cast<int64_t>(buf) * p.pull_nacc + a + 1) * p.slot_stride <= p.region_bytes);
   return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.pull_nacc + a) * p.slot_stride;
 }
 
@@ -580,6 +606,7 @@ __device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
   const uint32_t flag = static_cast<uint32_t>(s.g + 1);
   const int64_t nlines = (s.len + 7) >> 3;
   const int B = blockDim.x;
+  PAT_BOUND(16 * nlines <= p.slot_stride);
 
   if constexpr (KIND == kAG) {
     if (out + s.R * Cb != snd)
@@ -816,6 +843,7 @@ __device__ void ll32_phase(const KPlan& p, const Step& s, int t, Waiter& w, int 
   const uint32_t flag = static_cast<uint32_t>(s.g + 1);
   const int64_t nlines = (s.len + G - 1) / G * 32;
   const int B = blockDim.x;
+  PAT_BOUND(32 * nlines <= p.slot_stride);
   const int lane = threadIdx.x & 31;
 
   // lines inner: a round's stores are all in flight before the next round polls its first arrival
