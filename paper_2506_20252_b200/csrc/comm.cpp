@@ -572,11 +572,15 @@ int64_t pull_slot_bytes(const patComm* comm, int nacc) {
 }
 
 Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int max_channels, int64_t es,
-              int nacc) {
+              int nacc, bool direct_ag = false) {
   Slicing s{};
   s.proto = proto;
-  const int channels = std::max(1, std::min(comm->region_channels[proto], max_channels));
+  // a direct all-gather pushes into the peers' recvbufs: no inbox slots, so neither the slot size
+  // nor the SIMPLE region's channel count (both shrink under a staging cap) bound its slicing
+  const bool unstaged = direct_ag && proto == kProtoSimple;
+  const int channels = std::max(1, std::min(unstaged ? comm->channels : comm->region_channels[proto], max_channels));
   int64_t cap = static_cast<int64_t>(comm->slot_bytes);
+  if (unstaged) cap = std::max<int64_t>(cap, comm->pull_slice);
   int64_t minslice = 16 << 10;
   if (proto == kProtoLL) {
     cap = static_cast<int64_t>(comm->ll_slot_bytes / 2);
@@ -605,7 +609,7 @@ Slicing shape(const patComm* comm, int proto, int kind, int64_t chunk_bytes, int
 }
 
 Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int max_channels, bool pull_ok,
-                       int rounds, int64_t es, int nacc) {
+                       int rounds, int64_t es, int nacc, bool direct_ag = false) {
   const int channels = std::max(1, std::min(comm->channels, max_channels));
   int proto = comm->cfg.protocol;
   if (proto == patProtoAuto) {
@@ -620,7 +624,7 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
       for (const int cand : std::array<int, 3>{kProtoLL, kProtoLL32, bulk}) {
         if (cand == kProtoLL32 && static_cast<int64_t>(comm->n - 1) * chunk_bytes > kLL32MaxPayload) continue;
         const double t = predict_us(cand, comm->n, rounds, chunk_bytes,
-                                    shape(comm, cand, kind, chunk_bytes, channels, es, nacc).iters);
+                                    shape(comm, cand, kind, chunk_bytes, channels, es, nacc, direct_ag).iters);
         if (cand == kProtoLL || t < best) {
           best = t;
           proto = cand;
@@ -629,7 +633,7 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
     }
   }
   if (proto == kProtoPull && !pull_ok) proto = kProtoSimple;
-  return shape(comm, proto, kind, chunk_bytes, channels, es, nacc);
+  return shape(comm, proto, kind, chunk_bytes, channels, es, nacc, direct_ag);
 }
 
 // Channels per rank such that every device's launch stays co-resident (cooperative launch).
@@ -870,8 +874,21 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
                  (comm->cfg.protocol == patProtoPull || (kind == kRS && chunk_bytes > kPullMinRS));
   for (size_t l = 0; l < comm->lranks.size() && pull_ok && !single_device && !comm->multiprocess; ++l)
     pull_ok = legacy_ipc_capable(sendbuffs[l]) && (kind == kRS || legacy_ipc_capable(recvbuffs[l]));
+  // zero-copy all-gather (SIMPLE pushes straight into the peers' recvbufs) where they are
+  // reachable: one device; cudaMalloc'd buffers under peer access (one process); symmetric windows
+  // (one process per rank). Only bulk calls can take SIMPLE, so small calls skip the queries.
+  bool direct_ok = kind == kAG && comm->cfg.direct >= 0 && comm->cfg.protocol != patProtoLL &&
+                   comm->cfg.protocol != patProtoLL32 && comm->cfg.protocol != patProtoPull &&
+                   (comm->cfg.protocol == patProtoSimple || static_cast<int64_t>(n - 1) * chunk_bytes > (4 << 20));
+  if (direct_ok) {
+    if (comm->multiprocess) {
+      direct_ok = wrecv != nullptr;
+    } else if (!single_device && comm->cfg.direct == 0) {  // auto: every recvbuf reachable through peer access
+      for (size_t l = 0; l < comm->lranks.size() && direct_ok; ++l) direct_ok = legacy_ipc_capable(recvbuffs[l]);
+    }
+  }
   const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es),
-                                    cp->proto.pull_nacc);
+                                    cp->proto.pull_nacc, direct_ok);
   int vec = 16;
   bool aligned4 = (chunk_bytes % 4) == 0, aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
   for (size_t l = 0; l < comm->lranks.size(); ++l) {
@@ -887,18 +904,7 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   const bool fused = fused_path(comm, cp);
   if (!fused)
     if (patResult_t e = ensure_pools(comm)) return e;
-  bool direct = false;
-  if (kind == kAG && sl.proto == kProtoSimple && comm->cfg.direct >= 0) {
-    if (comm->multiprocess) {
-      direct = wrecv != nullptr;  // the peers' recvbufs: same offset of their windows
-    } else {
-      direct = single_device || comm->cfg.direct > 0;
-      if (!direct) {  // auto: cudaMalloc'd recvbufs are reachable through the enabled peer access
-        direct = true;
-        for (size_t l = 0; l < comm->lranks.size() && direct; ++l) direct = legacy_ipc_capable(recvbuffs[l]);
-      }
-    }
-  }
+  const bool direct = direct_ok && sl.proto == kProtoSimple;
   // window tag the kernels compare at entry (transport.cuh: sym_check)
   uint64_t sym_tag = 0;
   if (comm->multiprocess && (direct || sl.proto == kProtoPull)) {
@@ -1346,8 +1352,9 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
   // as run_collective decides, assuming cudaMalloc'd (peer-reachable) buffers
   const bool pull_ok = !comm->multiprocess && comm->cfg.protocol != patProtoSimple &&
                        (comm->cfg.protocol == patProtoPull || (static_cast<int>(kind) == kRS && cb > kPullMinRS));
+  const bool direct_ok = static_cast<int>(kind) == kAG && !comm->multiprocess && comm->cfg.direct >= 0;
   const Slicing sl = choose_slicing(comm, kind, cb, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es),
-                                    cp->proto.pull_nacc);
+                                    cp->proto.pull_nacc, direct_ok);
   std::memset(info, 0, sizeof(*info));
   info->trees = trees;
   info->rounds = cp->proto.nrounds;
@@ -1366,8 +1373,7 @@ patResult_t patCommPlan(patComm_t comm, patCollKind_t kind, size_t count, patDat
     return patSuccess;
   }
   // direct all-gather as run_collective decides it for cudaMalloc'd buffers in one process
-  const bool direct = static_cast<int>(kind) == kAG && sl.proto == kProtoSimple && !comm->multiprocess &&
-                      comm->cfg.direct >= 0;
+  const bool direct = direct_ok && sl.proto == kProtoSimple;
   const bool polling = sl.proto == kProtoLL || sl.proto == kProtoLL32;
   info->protocol = sl.proto;
   info->channels = sl.channels;

@@ -1052,6 +1052,15 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
   const uint64_t base = s_base;
   Waiter w{p.timeout_ns, p.err, false, p.gpu_scope != 0};
 
+  // done(step) for the previous call's last step on this channel: a polling-protocol call defers
+  // it from its exit (below), and EVERY protocol publishes it here — a bulk call that follows a
+  // polling one needs it, or its sender's credit for step base + depth - 1 (which the skew allows
+  // to wait on step base - 1) would wait on the peer's receiver, itself waiting on this sender.
+  // Every step before `base` finished: the previous kernel completed before this one started.
+  if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
+    st_relaxed(chan_flags(p, threadIdx.x, c) + 8 + R, base, w.gpu);
+  __syncthreads();  // orders it before any later done store of another thread (release cumulativity)
+
   if (p.direct && KIND == kAG) {
     // entry handshake: a peer may be written directly only once it entered this call
     __shared__ int s_abort;
@@ -1075,10 +1084,6 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
   if (p.proto == kProtoPull) {
     pull_role<DT, OP, KIND>(p, base, R, lr, c, w);
   } else if (p.proto == kProtoLL || p.proto == kProtoLL32) {
-    // done(step) for the previous call's last step, deferred from its exit (below): every step
-    // before `base` finished, since that kernel completed before this one started
-    if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
-      st_relaxed(chan_flags(p, threadIdx.x, c) + 8 + R, base, w.gpu);
     // 8-byte reductions use 8-byte LL32 units (whole elements); everything else 4-byte units
     constexpr int U = KIND == kRS && sizeof(typename DType<DT>::S) == 8 ? 8 : 4;
     // Steps in order. (A wavefront — phase t of step k - t in iteration k, as send_role — was

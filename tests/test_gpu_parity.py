@@ -655,3 +655,29 @@ def test_one_process_graph_capture_and_eager_launch_threads():
         torch.cuda.synchronize(r)
         assert same(recvs[r].cpu().numpy(), want[r]), r
     comm.raise_async_error()
+
+
+@pytest.mark.parametrize("spread", [False, True])
+def test_bulk_after_polling_call_single_tree(spread):
+    """A staged SIMPLE call right after a polling (LL32) call, with the skew at its deepest
+    (single-tree PAT, n-1 rounds, depth = rounds): the bulk sender's credit for step base+depth-1
+    needs the polling call's last done(step), which that call defers to the next kernel's entry —
+    every protocol must publish it there, or sender and receiver wait on each other (regression:
+    timed out before transport.cuh published it for bulk kernels)."""
+    if spread and NGPU < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = 4
+    devices = [r % max(NGPU, 1) for r in range(n)] if spread else [0] * n
+    comm = comm_for(n, devices, fused=-1, direct=-1, depth=3, ll_threshold=1 << 16, channels=4)
+    sched_ag = S.pat_allgather(n, 1)
+    sched_rs = S.pat_reduce_scatter(n, 1)
+    for it in range(12):
+        elems = [1000, 200000][it % 2]  # LL32, then staged SIMPLE
+        p = (np.arange(n * elems, dtype=np.int64) % 97 + it).astype(np.int32)
+        got = gpu_allgather(comm, devices, p, elems, O.INT32, schedule=sched_ag)
+        want = oracle_ag(n, 1, O.INT32, p, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (it, mismatch(got, want, elems))
+        q = (np.arange(n * n * elems, dtype=np.int64) % 89 + it).astype(np.int32)
+        got = gpu_reduce_scatter(comm, devices, q, elems, O.INT32, O.SUM, schedule=sched_rs)
+        want = oracle_rs(n, 1, O.INT32, O.SUM, q, elems)
+        assert all(same(got[r], want[r]) for r in range(n)), (it, mismatch(got, want, elems))

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--total-bytes", type=int, default=256 * 1000 * 1000)
     ap.add_argument("--caps", default="512,128,32", help="staging caps per rank, MiB")
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--windows", action="store_true", help="register the four tensors as symmetric windows")
+    ap.add_argument("--nccl", action="store_true", help="also time NCCL (NCCL_ALGO as set) on the same tensors")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -39,6 +41,9 @@ def main():
     gshard = torch.empty(shard, dtype=torch.bfloat16, device=dev)
     for cap_mib in [int(x) for x in args.caps.split(",")]:
         comm = PatComm.from_process_group(device=local, staging_bytes=cap_mib << 20)
+        if args.windows:  # zero copy: direct all-gather into `gathered`, PULL reduce-scatter from `grads`
+            for t in (params, gathered, grads, gshard):
+                comm.register(t)
         plan_ag, plan_rs = comm.plan(0, shard, BFLOAT16), comm.plan(1, shard, BFLOAT16)
 
         def step():
@@ -66,6 +71,23 @@ def main():
             ok.zero_()
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         bytes_ = 2 * (n - 1) * shard * 2
+        nccl_ms = None
+        if args.nccl:
+            def nstep():
+                dist.all_gather_into_tensor(gathered, params)
+                dist.reduce_scatter_tensor(gshard, grads)
+            for _ in range(3):
+                nstep()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a.record()
+            for _ in range(args.iters):
+                nstep()
+            b.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / args.iters], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            nccl_ms = float(t)
         if rank == 0:
             print(json.dumps({"config": "zero3", "n": n, "dtype": "bf16", "total_bytes": args.total_bytes,
                               "shard_bytes": shard * 2, "staging_cap_mib": cap_mib,
@@ -73,7 +95,9 @@ def main():
                               "slice_bytes": plan_ag["slice_bytes"], "protocol": [plan_ag["protocol"], plan_rs["protocol"]],
                               "peak_intermediate_slots": plan_ag["peak_intermediate_slots"],
                               "ms_per_step": float(ms), "busbw_gbs": bytes_ / (float(ms) * 1e-3) / 1e9,
-                              "allgather_matches_nccl": bool(ok.item())}), flush=True)
+                              "allgather_matches_nccl": bool(ok.item()), "windows": args.windows,
+                              "staging_bytes_used": [plan_ag.get("staging_bytes_used"), plan_rs.get("staging_bytes_used")],
+                              "nccl_ms_per_step": nccl_ms, "nccl_algo": os.environ.get("NCCL_ALGO")}), flush=True)
         comm.destroy()
     dist.barrier()
     dist.destroy_process_group()
