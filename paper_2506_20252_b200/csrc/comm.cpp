@@ -295,12 +295,21 @@ Layout plan_layout(const patConfig_t& c, int n, int depth_poll, bool explicit_sl
   size_t bulk_budget = kDefaultPoolBytes, poll_budget = poll_default;
   if (c.staging_bytes != 0) {
     const size_t B = c.staging_bytes > kFlagBytes + 3 * 4096 ? c.staging_bytes - kFlagBytes - 3 * 4096 : 0;
-    poll_budget = std::min(poll_default, B / 4);
+    // Under a cap the polling regions get up to 90% of the pool (never more than their uncapped
+    // size), the bulk region the rest: with a small pool LL32 — no fence per step — sustains far
+    // more than SIMPLE, whose per-iteration fence stalls the few channels a small pool leaves it
+    // (n = 4, ZeRO-3 shape, 12 / 32 / 64 MiB caps: LL32 325 / 530 / 523 GB/s busbw against SIMPLE
+    // 177 / 408 / 489, profiles/r02_capped_ll32_vs_simple.jsonl). PAT_POLL_SHARE overrides (percent).
+    long long pct = 90;
+    if (env_int("PAT_POLL_SHARE", &pct)) pct = std::min(95LL, std::max(5LL, pct));
+    poll_budget = std::min(poll_default, B / 100 * static_cast<size_t>(pct));
     bulk_budget = B - poll_budget;
   }
-  // LL gets a quarter of the polling budget, LL32 the rest (LL32 carries up to 48 MiB per call)
-  fit_region(poll_budget / 4, ch_ll, depth_poll * slots, ll_pref, 1024, 1024, &L.ch[kProtoLL], &L.slot[kProtoLL]);
-  fit_region(poll_budget - poll_budget / 4, c.max_channels, depth_poll * slots, ll32_pref, 1024, 1024,
+  // LL gets a fifth of the polling budget (it serves chunks up to 256 KiB), LL32 the rest (LL32
+  // carries up to 48 MiB per call uncapped, any size under a cap)
+  const size_t ll_budget = c.staging_bytes != 0 ? poll_budget / 5 : poll_budget / 4;
+  fit_region(ll_budget, ch_ll, depth_poll * slots, ll_pref, 1024, 1024, &L.ch[kProtoLL], &L.slot[kProtoLL]);
+  fit_region(poll_budget - ll_budget, c.max_channels, depth_poll * slots, ll32_pref, 1024, 1024,
              &L.ch[kProtoLL32], &L.slot[kProtoLL32]);
   if (explicit_slice && c.staging_bytes == 0) {
     L.ch[kProtoSimple] = c.max_channels;
@@ -549,6 +558,8 @@ constexpr CostRow kCostLL32{3.07, 2.42, 608.0, 32.0 / 28.0};  // one fixed cost 
 // (profiles/r01f_ll32_noskew_n*.jsonl, r01f_forced_n*_p2.jsonl, r01f_loopmid_n*.jsonl); the
 // linear model alone would keep it far beyond, where SIMPLE's pipelined pushes reach 670 GB/s.
 constexpr int64_t kLL32MaxPayload = 48ll << 20;
+constexpr double kCappedIterUs = 10.0;  // per extra bulk iteration under a staging cap (fence + flag)
+constexpr size_t kCappedSmallSlot = 64 << 10;  // bulk slots below this make the fence dominate
 constexpr CostRow kCostBulk{5.99, 6.11, 560.0, 1.0};
 
 double predict_us(int proto, int n, int rounds, int64_t chunk_bytes, int iters) {
@@ -622,9 +633,21 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
     } else {  // the cost model picks the fastest of LL, LL32 and the bulk protocol
       double best = 0;
       for (const int cand : std::array<int, 3>{kProtoLL, kProtoLL32, bulk}) {
-        if (cand == kProtoLL32 && static_cast<int64_t>(comm->n - 1) * chunk_bytes > kLL32MaxPayload) continue;
-        const double t = predict_us(cand, comm->n, rounds, chunk_bytes,
-                                    shape(comm, cand, kind, chunk_bytes, channels, es, nacc, direct_ag).iters);
+        // uncapped, SIMPLE's pipelined pushes beat LL32's polled lines beyond 48 MiB of payload;
+        // under a cap that shrank the bulk slots every size is a candidate for LL32
+        const bool capped = comm->slot_bytes < kMaxSlice;
+        if (cand == kProtoLL32 && !capped && static_cast<int64_t>(comm->n - 1) * chunk_bytes > kLL32MaxPayload)
+          continue;
+        const Slicing sh = shape(comm, cand, kind, chunk_bytes, channels, es, nacc, direct_ag);
+        double t = predict_us(cand, comm->n, rounds, chunk_bytes, sh.iters);
+        if (capped && comm->slot_bytes < kCappedSmallSlot && (cand == kProtoSimple || cand == kProtoPull) &&
+            !(direct_ag && cand == kProtoSimple)) {
+          // a bulk region shrunk to small slots: fewer channels push (each SM pushes ~5 GB/s) and
+          // every iteration pays a fence for little data (profiles/r02_zero3_*: ~10 us per iteration)
+          t += (static_cast<double>(kDefaultChannels) / std::max(sh.channels, 1) - 1.0) *
+                   (comm->n - 1) * static_cast<double>(chunk_bytes) / (kCostBulk.gbs * 1e3) +
+               kCappedIterUs * std::max(sh.iters - 1, 0);
+        }
         if (cand == kProtoLL || t < best) {
           best = t;
           proto = cand;
@@ -710,7 +733,11 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
     comm->skew = env_int("PAT_SKEW", &v) ? static_cast<int>(std::max(0LL, v)) : 1;
     comm->leaves_first = env_int("PAT_LEAVES_FIRST", &v) ? static_cast<int>(v != 0) : -1;
     // the polling protocols need depth >= 2 (deferred credit, transport.cuh); they do not skew
-    comm->depth_poll = env_int("PAT_POLL_DEPTH", &v) ? static_cast<int>(v) : c.depth;
+    // a small cap (< 24 MiB) buys larger LL32 slots with two buffers per channel instead of depth:
+    // 12 MiB, n = 4: 455 vs 326 GB/s busbw (profiles/r02_capped_poll_depth.jsonl)
+    comm->depth_poll = env_int("PAT_POLL_DEPTH", &v)                         ? static_cast<int>(v)
+                       : (c.staging_bytes != 0 && c.staging_bytes < (24u << 20)) ? 2
+                                                                                  : c.depth;
     comm->depth_poll = std::min(std::max(comm->depth_poll, 2), c.depth);
     if (env_int("PAT_EPOCH_SHIFT", &v) && v >= 3 && v <= 31 && (1ll << v) > 2 * comm->depth_poll)
       comm->epoch_mask = (1ull << v) - 1;

@@ -38,29 +38,50 @@ def summarize(tr):
     return "\n".join(out)
 
 
+def channel_timeline(tr, cta):
+    """Per event of one CTA (both roles), time in us from the CTA's first event: the per-iteration
+    picture of credit waits, pushes, fences and arrivals."""
+    rows = []
+    for role in range(2):
+        for e in range(tr.shape[2]):
+            ns, code = int(tr[cta, role, e, 0]), int(tr[cta, role, e, 1])
+            if ns:
+                rows.append((ns, "push" if role == 0 else "recv", EV.get(code >> 56, code >> 56),
+                             (code >> 40) & 0xFFFF, (code >> 32) & 0xFF))
+    if not rows:
+        return ""
+    t0 = min(r[0] for r in rows)
+    return "\n".join(f"{(ns - t0) / 1e3:9.2f} {role} {ev:9s} step {st:5d} r{rd}" for ns, role, ev, st, rd in sorted(rows))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bytes", type=int, default=16 << 20)
     ap.add_argument("--coll", default="ag")
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--staging-mib", type=int, default=0, help="patConfig staging_bytes cap")
+    ap.add_argument("--protocol", type=int, default=0)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     args = ap.parse_args()
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_2506_20252_b200 import FLOAT32, SUM, PatComm
+    from paper_2506_20252_b200 import BFLOAT16, FLOAT32, SUM, PatComm
 
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
-    comm = PatComm.from_process_group(device=local)
-    n, elems = world, args.bytes // 4
+    comm = PatComm.from_process_group(device=local, staging_bytes=args.staging_mib << 20,
+                                      protocol=args.protocol or None)
+    tdt, FLOAT32 = (torch.float32, FLOAT32) if args.dtype == "f32" else (torch.bfloat16, BFLOAT16)
+    n, elems = world, args.bytes // (4 if args.dtype == "f32" else 2)
     if args.coll == "ag":
-        s, r = torch.ones(elems, device=dev), torch.empty(n * elems, device=dev)
+        s, r = torch.ones(elems, device=dev, dtype=tdt), torch.empty(n * elems, device=dev, dtype=tdt)
         fn = lambda: comm.all_gather([s], [r], elems, FLOAT32)
     else:
-        s, r = torch.ones(n * elems, device=dev), torch.empty(elems, device=dev)
+        s, r = torch.ones(n * elems, device=dev, dtype=tdt), torch.empty(elems, device=dev, dtype=tdt)
         fn = lambda: comm.reduce_scatter([s], [r], elems, FLOAT32, SUM)
     for _ in range(args.warmup):
         fn()
@@ -75,6 +96,7 @@ def main():
     if rank == 0:
         print(comm.plan(0 if args.coll == "ag" else 1, elems, FLOAT32))
         print(summarize(tr))
+        print(channel_timeline(tr, 0))
     dist.barrier()
     comm.destroy()
     dist.destroy_process_group()
