@@ -608,6 +608,21 @@ def run_pat(args, rank, world, local):
                                       "72 MiB takes 12.2 us = 0.94 of hbm_gbs (profiles/r02_local_tune.jsonl, "
                                       "ceil_write_only), so ~0.94 bounds the all-gather's frac"}
         achieved = algo_bytes / (dom_us * 1e-6) / 1e9
+        # live write-only ceiling for the same byte count (the all-gather is n^2 C writes + n C
+        # reads): K fills of a 72 MiB buffer, rotated over 4 (more than 2x L2), events around them
+        wbufs = [torch.empty(algo_bytes // 4, device=dev0) for _ in range(4)]
+        for b_ in wbufs:
+            b_.fill_(0.0)
+        D.sync()
+        def fills():
+            with torch.cuda.stream(D.streams[devices[0]]):
+                for k in range(K):
+                    wbufs[k % 4].fill_(float(k))
+        fill_ms = D.time_ms(fills)
+        wgbs = algo_bytes / (fill_ms / K * 1e-3) / 1e9
+        roof["write_ceiling"] = {"gbs": wgbs, "frac_of_peak": wgbs / peak, "us": 1e3 * fill_ms / K,
+                                 "kernel": "torch fill_ of the same bytes (write-only), K launches, 4 rotating buffers"}
+        del wbufs
     else:
         # per GPU: every rank on it receives (n-1)*C over NVLink per launch (ranks sharing a GPU
         # share its links, so the GPU's ingress is ranks_on_gpu * (n-1) * C minus what stays local)
@@ -621,6 +636,8 @@ def run_pat(args, rank, world, local):
         roof["frac_of_sm_push_704"] = achieved / NVLINK_SM_PUSH_GBS
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
                  "launch_us": dom_us})
+    if "write_ceiling" in roof and dom == "all_gather":
+        roof["frac_of_write_ceiling"] = achieved / roof["write_ceiling"]["gbs"]
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
