@@ -58,6 +58,7 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--nccl-graph", action="store_true", help="time NCCL Ring from CUDA graphs (hangs on some boxes)")
+    ap.add_argument("--no-group", action="store_true", help="issue a step's all-gather and reduce-scatter ungrouped")
     ap.add_argument("--no-extras", action="store_true", help="skip transport_local / ref_dtypes records")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args(argv)
@@ -280,6 +281,7 @@ def run_pat(args, rank, world, local):
     dist = None
     n, devices, n_gpus, mode = placement(args, world, torch.cuda.device_count())
     from paper_2506_20252_b200 import FLOAT32, FLOAT64, INT64, SUM, PatComm
+    from paper_2506_20252_b200._lib import lib
 
     C = args.chunk_bytes
     elems = C // 4
@@ -341,10 +343,21 @@ def run_pat(args, rank, world, local):
         })
 
     def call(c, kinds, bs, dtype=FLOAT32, count=elems):
-        if "ag" in kinds:
-            c.all_gather(bs["ag_send"], bs["ag_recv"], count, dtype, streams=streams)
-        if "rs" in kinds:
-            c.reduce_scatter(bs["rs_send"], bs["rs_recv"], count, dtype, SUM, streams=streams)
+        # a step ("ag", "rs") is one group (patGroupStart/End): the all-gather and the reduce-scatter
+        # run as one launch; "ungrouped" issues them one after the other
+        grouped = "ag" in kinds and "rs" in kinds and "ungrouped" not in kinds and not args.no_group
+        if grouped:
+            lib().patGroupStart()
+        try:
+            if "ag" in kinds:
+                c.all_gather(bs["ag_send"], bs["ag_recv"], count, dtype, streams=streams)
+            if "rs" in kinds:
+                c.reduce_scatter(bs["rs_send"], bs["rs_recv"], count, dtype, SUM, streams=streams)
+        finally:
+            if grouped:
+                rc = lib().patGroupEnd()
+                if rc:
+                    raise RuntimeError(f"patGroupEnd: {rc}")
 
     dbg("warmup")
     for _ in range(args.warmup):
@@ -382,7 +395,7 @@ def run_pat(args, rank, world, local):
         return run
 
     dbg("capture")
-    graphs = {kinds: graphs_for(comm, kinds) for kinds in (("ag", "rs"), ("ag",), ("rs",))}
+    graphs = {kinds: graphs_for(comm, kinds) for kinds in (("ag", "rs"), ("ag", "rs", "ungrouped"), ("ag",), ("rs",))}
     for pair in graphs.values():  # warm replay
         replay_k(pair)()
     D.barrier()
@@ -395,8 +408,9 @@ def run_pat(args, rank, world, local):
             dbg(f"step trials (us/step): {[round(1e3 * x / K, 2) for x in [step_ms] + extra]}")
         ag_ms = D.time_ms(replay_k(graphs[("ag",)]))
         rs_ms = D.time_ms(replay_k(graphs[("rs",)]))
+        step_ung_ms = D.time_ms(replay_k(graphs[("ag", "rs", "ungrouped")]))
     comm.raise_async_error()
-    step_ms, ag_ms, rs_ms = max_over_ranks(torch, dist, dev0, [step_ms, ag_ms, rs_ms])
+    step_ms, ag_ms, rs_ms, step_ung_ms = max_over_ranks(torch, dist, dev0, [step_ms, ag_ms, rs_ms, step_ung_ms])
     del graphs
     ms_per_step = step_ms / K
     value = busbw_gbs(n, C, ms_per_step / 1e3)
@@ -545,7 +559,11 @@ def run_pat(args, rank, world, local):
                 "busbw_gbs": busbw_gbs(n, C, nt[0] / K / 1e3),
                 "ag_us": 1e3 * nt[1] / K, "rs_us": 1e3 * nt[2] / K,
                 "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()), "timing": timing,
-                "pat_speedup_step": nt[0] / step_ms}
+                "pat_speedup_step": nt[0] / step_ms,
+                "pat_speedup_step_ungrouped": nt[0] / step_ung_ms,
+                "note": "NCCL's all-gather and reduce-scatter run one after the other (torch.distributed cannot "
+                        "coalesce two different collectives); compare with pat_speedup_step_ungrouped for the "
+                        "same call sequence, pat_speedup_step for PAT's grouped launch"}
 
     # ---- N = 1 extras: the same n = 8 workload through the PAT transport kernel (per-round
     # messages through the inbox pools with flags), and the repo at the reference arm's dtypes
@@ -691,7 +709,7 @@ def run_pat(args, rank, world, local):
                                  f"payloads built once, ExecMode::Parallel x{thr} threads, {args.cpu_seconds:.0f} s budget"}
             except Exception as e:  # the reference library must be built in-tree
                 cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
-        launches_per_gpu = 2 * K
+        launches_per_gpu = (1 if not args.no_group else 2) * K  # a grouped step is one launch per GPU
         out = {
             "metric": "PAT all-gather + reduce-scatter(sum) aggregate bus bandwidth, 1 MiB fp32 per rank",
             "value": value, "unit": "GB/s", "n_gpus": n_gpus, "steps": K, "warmup": args.warmup,
@@ -707,6 +725,9 @@ def run_pat(args, rank, world, local):
                        "plan_allgather": plan_ag, "plan_reduce_scatter": plan_rs},
             "latency_us": {"all_gather": 1e3 * ag_ms / K, "reduce_scatter": 1e3 * rs_ms / K,
                            "timing": "graph of K back-to-back calls per collective"},
+            "step_grouped": not args.no_group,
+            "ms_per_step_ungrouped": step_ung_ms / K,
+            "value_ungrouped": busbw_gbs(n, C, step_ung_ms / K / 1e3),
             "latency_us_eager": eager_us,
             "latency_us_eager_isolated": eager_iso_us,
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,

@@ -246,6 +246,15 @@ patResult_t patReduceScatter(patComm_t comm, const void* const* sendbuffs, void*
                              size_t recvcount, patDataType_t datatype, patRedOp_t op,
                              const patStream_t* streams);
 
+/* Groups (NCCL's ncclGroupStart / ncclGroupEnd, per host thread): the collectives issued between
+ * the outermost patGroupStart and patGroupEnd are launched at patGroupEnd. An all-gather followed
+ * by a reduce-scatter (sum) of the same communicator on the same streams becomes ONE launch per
+ * device — each call on half of the channels — so the two calls run at the same time; other calls
+ * are launched one by one, in order. Calls in a group must not depend on each other; their
+ * buffers must stay valid until patGroupEnd. Errors of recorded calls are returned by patGroupEnd. */
+patResult_t patGroupStart(void);
+patResult_t patGroupEnd(void);
+
 /* Same collectives over an explicit, caller-supplied rank-relative schedule (any validated
  * non-exchange schedule of the communicator's rank count: PAT with any T, ring, Bruck), the
  * generic executor of the reference (run_allgather/run_reduce_scatter take a schedule,

@@ -13,9 +13,9 @@ The product is ``libpatb200.so`` (sm_100a kernels + C++ host runtime behind the 
 from . import _lib
 from ._lib import BFLOAT16, FLOAT16, FLOAT32, FLOAT64, INT8, INT32, INT64, MAX, MIN, PROD, SUM, UINT8, UINT32, UINT64
 from ._lib import PROTO_AUTO, PROTO_LL, PROTO_LL32, PROTO_PULL, PROTO_SIMPLE, PatError
-from .comm import PatComm
+from .comm import PatComm, group
 
-__all__ = ["PatComm", "PatError", "schedule", "simulate", "comm", "SUM", "PROD", "MAX", "MIN",
+__all__ = ["PatComm", "PatError", "group", "schedule", "simulate", "comm", "SUM", "PROD", "MAX", "MIN",
            "INT8", "UINT8", "INT32", "UINT32", "INT64", "UINT64", "FLOAT16", "FLOAT32", "FLOAT64", "BFLOAT16",
            "PROTO_AUTO", "PROTO_LL", "PROTO_LL32", "PROTO_SIMPLE", "PROTO_PULL", "library_path"]
 

@@ -128,7 +128,7 @@ SYMBOLS = [
     "patReduceScatter", "patAllGatherSchedule", "patReduceScatterSchedule", "patScheduleBuild",
     "patScheduleMirror", "patScheduleValidate", "patScheduleStats", "patScheduleTraceCsv",
     "patMaxTrees", "patTreesFromBuffer", "patPatBufferSlots", "patRoundCountFormula", "patCommTraceRead",
-    "patCommMemInfo", "patCommRegisterPrepare", "patCommRegisterFinish", "patCommDeregister", "patCommBarrier", "patCommStatsRead",
+    "patCommMemInfo", "patCommRegisterPrepare", "patCommRegisterFinish", "patCommDeregister", "patCommBarrier", "patCommStatsRead", "patGroupStart", "patGroupEnd",
 ]
 
 _lib = None
@@ -181,6 +181,8 @@ def lib() -> ctypes.CDLL:
         L.patCommDeregister.argtypes = [VP, VP]
         L.patCommBarrier.argtypes = [VP, PP]
         L.patCommStatsRead.argtypes = [VP, I32P, IP, IP]
+        L.patGroupStart.argtypes = []
+        L.patGroupEnd.argtypes = []
         _lib = L
     return _lib
 

@@ -78,6 +78,22 @@ def make_exchange(group=None) -> Callable[[bytes], list]:
     return exchange
 
 
+class group:
+    """``with group(): ...`` — patGroupStart / patGroupEnd: the collectives issued inside are launched
+    at exit; an all-gather and a reduce-scatter (sum) of one communicator on the same streams run
+    as one launch. The calls must be independent; errors surface at exit."""
+
+    def __enter__(self):
+        check(lib().patGroupStart(), "patGroupStart")
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        rc = lib().patGroupEnd()
+        if exc_type is None:
+            check(rc, "patGroupEnd")
+        return False
+
+
 class PatComm:
     def __init__(self, handle: ctypes.c_void_p):
         self._h = handle
@@ -238,6 +254,10 @@ class PatComm:
                   "patReduceScatter")
             return
         self.reduce_scatter([input], [output], output.numel(), None, op, None if stream is None else [stream])
+
+    @staticmethod
+    def group() -> "group":
+        return group()
 
     def barrier(self, streams=None) -> None:
         """Device-side barrier over every rank on `streams` (default: the current streams)."""

@@ -35,6 +35,10 @@ namespace pat {
 using KernelFn = void (*)(const KPlan);
 cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream);
 cudaError_t launch_barrier(const BPlan& b, cudaStream_t stream);
+cudaError_t launch_group(const KPlan2& plans, int dtype, int threads, cudaStream_t stream);
+cudaError_t launch_local_group(int n, int dtype, int64_t a_bytes, const char* const* a_send, char* const* a_recv,
+                               int64_t b_bytes, const char* const* b_send, char* const* b_recv, int sm_count,
+                               cudaStream_t stream);
 cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out);
 cudaError_t init_pool_state(char* pool, int64_t ll_off, int64_t ll_bytes, int64_t ll32_off, int64_t ll32_bytes,
                             uint64_t start, cudaStream_t stream);
@@ -860,9 +864,23 @@ int64_t proto_slot_stride(const patComm* comm, int proto, int nacc) {
                                                     : comm->slot_bytes);
 }
 
+// A collective ready to launch: per device group the KPlan (or, fused, the local executor's args).
+struct Prepared {
+  bool fused = false;
+  int kind = 0, dtype = 0, op = 0;
+  int64_t chunk_bytes = 0;
+  size_t es = 0;
+  bool aligned16 = false;
+  std::vector<KPlan> plans;  // per device group
+};
+
+patResult_t submit_prepared(patComm* comm, const Prepared& a, const Prepared* b, const patStream_t* streams);
+
+// split: 0 = the call alone; 1 / 2 = first / second half of the channels of its protocol's region
+// (a grouped pair sharing one launch, patGroupEnd). prep != nullptr: build the plans, do not launch.
 patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs, void* const* recvbuffs,
                            size_t count, int dtype, int op, const patStream_t* streams,
-                           const Schedule* explicit_sched = nullptr) {
+                           const Schedule* explicit_sched = nullptr, int split = 0, Prepared* prep = nullptr) {
   if (!comm || !comm->finished) return patInvalidUsage;
   const size_t es = dtype_size(dtype);
   if (!es) return patInvalidArgument;
@@ -914,8 +932,22 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       for (size_t l = 0; l < comm->lranks.size() && direct_ok; ++l) direct_ok = legacy_ipc_capable(recvbuffs[l]);
     }
   }
-  const Slicing sl = choose_slicing(comm, kind, chunk_bytes, cap, pull_ok, cp->proto.nrounds, static_cast<int64_t>(es),
-                                    cp->proto.pull_nacc, direct_ok);
+  if (split) {  // a grouped pair: both halves of one launch must be co-resident together
+    int gcap = 0;
+    if (patResult_t e = channel_cap(comm, 2, dtype, op, &gcap)) return e;
+    cap = std::min(cap, gcap / 2);
+  }
+  Slicing sl = choose_slicing(comm, kind, chunk_bytes, split ? std::max(cap, 1) : cap, pull_ok, cp->proto.nrounds,
+                              static_cast<int64_t>(es), cp->proto.pull_nacc, direct_ok);
+  int chan_base = 0;
+  if (split) {  // half of the protocol's channel region each, so the two ranges never overlap
+    const int region = (direct_ok && sl.proto == kProtoSimple) ? comm->channels : comm->region_channels[sl.proto];
+    const int half = std::max(region / 2, 1);
+    if (region < 2) return patInvalidUsage;
+    sl = shape(comm, sl.proto, kind, chunk_bytes, std::min(std::max(cap, 1), half), static_cast<int64_t>(es),
+               cp->proto.pull_nacc, direct_ok);
+    chan_base = split == 2 ? half : 0;
+  }
   int vec = 16;
   bool aligned4 = (chunk_bytes % 4) == 0, aligned8 = (chunk_bytes % 8) == 0, aligned16 = (chunk_bytes % 16) == 0;
   for (size_t l = 0; l < comm->lranks.size(); ++l) {
@@ -953,6 +985,7 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.vec = vec;
     p.esize = static_cast<int>(es);
     p.channels = sl.channels;
+    p.chan_base = chan_base;
     p.iters = sl.iters;
     p.chunk_bytes = chunk_bytes;
     p.slice_bytes = sl.slice;
@@ -1012,16 +1045,16 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     p.poll_slot[1] = static_cast<int64_t>(comm->ll32_slot_bytes);
     p.err = comm->err_dev;
     p.occ = nullptr;
-    if (g.occ && sl.proto == kProtoSimple) {
+    if (g.occ && sl.proto == kProtoSimple && !split) {
       p.occ = g.occ;
       g.occ_rounds = p.nrounds;
       CUDA_TRY(cudaSetDevice(g.device));
       CUDA_TRY(cudaMemsetAsync(g.occ, 0, sizeof(int) * 2 * kMaxRounds * g.lidx.size(),
                                streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr));
     }
-    p.trace = g.trace;
+    p.trace = split ? nullptr : g.trace;  // the trace indexes CTAs by blockIdx: single calls only
     p.trace_cap = g.trace_cap;
-    if (g.trace) {
+    if (p.trace) {
       g.trace_ctas = p.nlocal * p.channels;
       CUDA_TRY(cudaMemsetAsync(g.trace, 0, sizeof(uint64_t) * 4 * g.trace_cap * g.trace_ctas,
                                streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr));
@@ -1038,10 +1071,28 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       p.iter_state[i] = g.iter_state + i * kMaxChannels;
     }
   }
+  Prepared local;
+  Prepared& P = prep ? *prep : local;
+  P.fused = fused;
+  P.kind = kind;
+  P.dtype = dtype;
+  P.op = op;
+  P.chunk_bytes = chunk_bytes;
+  P.es = es;
+  P.aligned16 = aligned16;
+  P.plans = std::move(plans);
+  if (prep) return patSuccess;
+  return submit_prepared(comm, P, nullptr, streams);
+}
+
+// Launch a prepared call — or a grouped pair (a = all-gather, b = reduce-scatter sum) as ONE
+// launch per device — on the streams of the local ranks.
+patResult_t submit_prepared(patComm* comm, const Prepared& a, const Prepared* b, const patStream_t* streams) {
+  const int n = comm->n;
   // submission to one device: join the stream of every local rank of the device, one launch
   auto submit = [&](size_t gi) -> patResult_t {
     const DevGroup& g = comm->groups[gi];
-    const KPlan& p = plans[gi];
+    const KPlan& p = a.plans[gi];
     CUDA_TRY(cudaSetDevice(g.device));
     const int threads = comm->cfg.threads;
     cudaStream_t s0 = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr;
@@ -1051,17 +1102,44 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       CUDA_TRY(cudaEventRecord(comm->events[g.lidx[i]], si));
       CUDA_TRY(cudaStreamWaitEvent(s0, comm->events[g.lidx[i]], 0));
     }
-    if (fused) {  // every rank in this HBM: fused executor (local.cu), no transport
+    if (a.fused) {  // every rank in this HBM: fused executor (local.cu), no transport
       const char* sb[kMaxRanks];
       char* rb[kMaxRanks];
       for (size_t i = 0; i < g.lidx.size(); ++i) {
         sb[p.rank[i]] = p.send[i];
         rb[p.rank[i]] = p.recv[i];
       }
-      CUDA_TRY(launch_local(kind, n, dtype, op, aligned16 ? 16 : 0, static_cast<int>(es), chunk_bytes, sb, rb,
-                            g.sm_count, s0));
+      bool done = false;
+      if (b) {
+        const KPlan& q = b->plans[gi];
+        const char* sb2[kMaxRanks];
+        char* rb2[kMaxRanks];
+        for (size_t i = 0; i < g.lidx.size(); ++i) {
+          sb2[q.rank[i]] = q.send[i];
+          rb2[q.rank[i]] = q.recv[i];
+        }
+        const cudaError_t e = launch_local_group(n, b->dtype, a.chunk_bytes, sb, rb, b->chunk_bytes, sb2, rb2,
+                                                 g.sm_count, s0);
+        if (e == cudaErrorNotSupported) {  // alignment: one after the other
+          CUDA_TRY(launch_local(a.kind, n, a.dtype, a.op, a.aligned16 ? 16 : 0, static_cast<int>(a.es), a.chunk_bytes,
+                                sb, rb, g.sm_count, s0));
+          CUDA_TRY(launch_local(b->kind, n, b->dtype, b->op, b->aligned16 ? 16 : 0, static_cast<int>(b->es),
+                                b->chunk_bytes, sb2, rb2, g.sm_count, s0));
+        } else {
+          CUDA_TRY(e);
+        }
+        done = true;
+      }
+      if (!done)
+        CUDA_TRY(launch_local(a.kind, n, a.dtype, a.op, a.aligned16 ? 16 : 0, static_cast<int>(a.es), a.chunk_bytes,
+                              sb, rb, g.sm_count, s0));
+    } else if (b) {
+      KPlan2 both;
+      both.a = p;
+      both.b = b->plans[gi];
+      CUDA_TRY(launch_group(both, b->dtype, threads, s0));
     } else {
-      CUDA_TRY(launch(p, dtype, op, threads, s0));
+      CUDA_TRY(launch(p, a.dtype, a.op, threads, s0));
     }
     bool joined = false;
     for (size_t i = 1; i < g.lidx.size(); ++i) {
@@ -1102,6 +1180,93 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
     if (first == patSuccess) first = e;
   }
   return first;
+}
+
+// ---------------------------------------------------------------------------- groups
+// patGroupStart / patGroupEnd (NCCL's group semantics, per host thread): collectives issued in
+// between are recorded and launched at the outermost patGroupEnd. An all-gather and a
+// reduce-scatter (sum) of one communicator on the same streams become ONE launch — each on half
+// of the channels, fused executor or transport — so their latencies overlap; anything else is
+// launched call by call, in order. The calls of a group must be independent (as in NCCL).
+struct PendingCall {
+  patComm* comm = nullptr;
+  int kind = 0, dtype = 0, op = 0;
+  size_t count = 0;
+  std::vector<const void*> send;
+  std::vector<void*> recv;
+  std::vector<patStream_t> streams;
+  bool has_streams = false;
+  bool has_sched = false;
+  Schedule sched;
+};
+struct GroupState {
+  int depth = 0;
+  std::vector<PendingCall> calls;
+};
+thread_local GroupState t_group;
+
+patResult_t record_call(patComm* comm, int kind, const void* const* sendbuffs, void* const* recvbuffs, size_t count,
+                        int dtype, int op, const patStream_t* streams, const Schedule* sched) {
+  if (!comm || !comm->finished) return patInvalidUsage;
+  if (!sendbuffs || !recvbuffs) return patInvalidArgument;
+  PendingCall c;
+  c.comm = comm;
+  c.kind = kind;
+  c.dtype = dtype;
+  c.op = op;
+  c.count = count;
+  const size_t L = comm->lranks.size();
+  c.send.assign(sendbuffs, sendbuffs + L);
+  c.recv.assign(recvbuffs, recvbuffs + L);
+  if (streams) {
+    c.streams.assign(streams, streams + L);
+    c.has_streams = true;
+  }
+  if (sched) {
+    c.sched = *sched;
+    c.has_sched = true;
+  }
+  t_group.calls.push_back(std::move(c));
+  return patSuccess;
+}
+
+patResult_t run_pending(PendingCall& c) {
+  return run_collective(c.comm, c.kind, c.send.data(), c.recv.data(), c.count, c.dtype, c.op,
+                        c.has_streams ? c.streams.data() : nullptr, c.has_sched ? &c.sched : nullptr);
+}
+
+bool groupable(const PendingCall& x, const PendingCall& y) {
+  if (x.comm != y.comm || x.kind == y.kind || x.has_sched || y.has_sched || !x.count || !y.count) return false;
+  if (x.has_streams != y.has_streams || x.streams != y.streams) return false;
+  const PendingCall& rs = x.kind == kRS ? x : y;
+  if (rs.op != patSum || !dtype_size(rs.dtype) || !dtype_size(x.kind == kAG ? x.dtype : y.dtype)) return false;
+  static const bool off = [] {
+    long long v = 0;
+    return env_int("PAT_GROUP_FUSE", &v) && v == 0;
+  }();
+  return !off;
+}
+
+patResult_t run_group_pair(PendingCall& x, PendingCall& y) {
+  PendingCall& ag = x.kind == kAG ? x : y;
+  PendingCall& rs = x.kind == kAG ? y : x;
+  patComm* comm = ag.comm;
+  Prepared pa, pb;
+  const patStream_t* st = ag.has_streams ? ag.streams.data() : nullptr;
+  if (patResult_t e = run_collective(comm, kAG, ag.send.data(), ag.recv.data(), ag.count, ag.dtype, ag.op, st,
+                                     nullptr, 1, &pa))
+    return e;
+  if (patResult_t e = run_collective(comm, kRS, rs.send.data(), rs.recv.data(), rs.count, rs.dtype, rs.op, st,
+                                     nullptr, 2, &pb))
+    return e;
+  if (pa.fused != pb.fused || (!pa.fused && (pa.plans.empty() || pb.plans.empty()))) {
+    // not the same executor: one after the other
+    if (patResult_t e = run_pending(x)) return e;
+    return run_pending(y);
+  }
+  std::lock_guard<std::mutex> lock(comm->mu);
+  DeviceGuard guard;
+  return submit_prepared(comm, pa, &pb, st);
 }
 
 }  // namespace
@@ -1559,11 +1724,13 @@ patResult_t patCommBarrier(patComm_t comm, const patStream_t* streams) {
 
 patResult_t patAllGather(patComm_t comm, const void* const* sendbuffs, void* const* recvbuffs, size_t sendcount,
                          patDataType_t datatype, const patStream_t* streams) {
+  if (t_group.depth > 0) return record_call(comm, kAG, sendbuffs, recvbuffs, sendcount, datatype, patSum, streams, nullptr);
   return run_collective(comm, kAG, sendbuffs, recvbuffs, sendcount, datatype, patSum, streams);
 }
 
 patResult_t patReduceScatter(patComm_t comm, const void* const* sendbuffs, void* const* recvbuffs,
                              size_t recvcount, patDataType_t datatype, patRedOp_t op, const patStream_t* streams) {
+  if (t_group.depth > 0) return record_call(comm, kRS, sendbuffs, recvbuffs, recvcount, datatype, op, streams, nullptr);
   return run_collective(comm, kRS, sendbuffs, recvbuffs, recvcount, datatype, op, streams);
 }
 
@@ -1572,6 +1739,7 @@ patResult_t patAllGatherSchedule(patComm_t comm, const int32_t* sched, size_t le
                                  const patStream_t* streams) {
   Schedule s;
   if (Err e = decode(sched, len, &s)) return to_result(e);
+  if (t_group.depth > 0) return record_call(comm, kAG, sendbuffs, recvbuffs, sendcount, datatype, patSum, streams, &s);
   return run_collective(comm, kAG, sendbuffs, recvbuffs, sendcount, datatype, patSum, streams, &s);
 }
 
@@ -1580,7 +1748,32 @@ patResult_t patReduceScatterSchedule(patComm_t comm, const int32_t* sched, size_
                                      patRedOp_t op, const patStream_t* streams) {
   Schedule s;
   if (Err e = decode(sched, len, &s)) return to_result(e);
+  if (t_group.depth > 0) return record_call(comm, kRS, sendbuffs, recvbuffs, recvcount, datatype, op, streams, &s);
   return run_collective(comm, kRS, sendbuffs, recvbuffs, recvcount, datatype, op, streams, &s);
+}
+
+patResult_t patGroupStart(void) {
+  ++t_group.depth;
+  return patSuccess;
+}
+
+patResult_t patGroupEnd(void) {
+  if (t_group.depth <= 0) return patInvalidUsage;
+  if (--t_group.depth > 0) return patSuccess;
+  std::vector<PendingCall> calls;
+  calls.swap(t_group.calls);
+  patResult_t first = patSuccess;
+  for (size_t i = 0; i < calls.size(); ++i) {
+    patResult_t e;
+    if (i + 1 < calls.size() && groupable(calls[i], calls[i + 1])) {
+      e = run_group_pair(calls[i], calls[i + 1]);
+      ++i;
+    } else {
+      e = run_pending(calls[i]);
+    }
+    if (first == patSuccess) first = e;
+  }
+  return first;
 }
 
 // ---------------------------------------------------------------- schedules (host only)

@@ -15,12 +15,20 @@ static const KernelFn* const kRsTable[10] = {kRsRowI8,  kRsRowU8,  kRsRowI32, kR
                                              kRsRowU64, kRsRowF16, kRsRowF32, kRsRowF64, kRsRowBF16};
 static const KernelFn kAgKernel = pat_kernel<kU8, kSum, kAG>;
 
+using GroupFn = void (*)(const KPlan2);
+extern const GroupFn kGroupI8, kGroupU8, kGroupI32, kGroupU32, kGroupI64, kGroupU64, kGroupF16, kGroupF32, kGroupF64,
+    kGroupBF16;
+static const GroupFn* const kGroupTable[10] = {&kGroupI8,  &kGroupU8,  &kGroupI32, &kGroupU32, &kGroupI64,
+                                               &kGroupU64, &kGroupF16, &kGroupF32, &kGroupF64, &kGroupBF16};
+
 KernelFn kernel_for(int kind, int dtype, int op) {
   if (kind == kAG) return kAgKernel;
   return kRsTable[dtype][op];
 }
 
 cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out) {
+  if (kind == 2)  // the grouped all-gather + reduce-scatter kernel
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, *kGroupTable[dtype], threads, 0);
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel_for(kind, dtype, op), threads, 0);
 }
 
@@ -80,6 +88,26 @@ __global__ void barrier_kernel(const __grid_constant__ BPlan b) {
 cudaError_t launch_barrier(const BPlan& b, cudaStream_t stream) {
   barrier_kernel<<<1, 64, 0, stream>>>(b);
   return cudaGetLastError();
+}
+
+// Grouped all-gather (a) + reduce-scatter (b, sum, `dtype`) of one communicator in one launch.
+cudaError_t launch_group(const KPlan2& plans, int dtype, int threads, cudaStream_t stream) {
+  static const int force_coop = [] {
+    const char* e = std::getenv("PAT_COOP");
+    return e ? std::atoi(e) : -1;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plans.a.nlocal * (plans.a.channels + plans.b.channels));
+  cfg.blockDim = dim3(threads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = force_coop >= 0 ? (force_coop != 0) : (plans.a.nlocal > 1);
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, *kGroupTable[dtype], plans);
 }
 
 cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream_t stream) {

@@ -142,14 +142,13 @@ constexpr int kFlatThreads = 256;  // flat kernels: 4 CTAs of 256 threads per SM
 constexpr int kFlatCtasPerSm = 4;
 constexpr int kAgU = 2;
 
-__global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) local_ag32_kernel(const __grid_constant__ LPlan p) {
-  pdl_enter();
+__device__ __forceinline__ void local_ag32_body(const LPlan& p, int blk, int nblk) {
   const int n = p.n;
   const int64_t Cb = p.chunk_bytes;
   const int64_t nu = Cb >> 5;
   const int64_t total = n * nu;
-  const int64_t TT = static_cast<int64_t>(gridDim.x) * kFlatThreads;
-  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kFlatThreads + threadIdx.x; g < total; g += kAgU * TT) {
+  const int64_t TT = static_cast<int64_t>(nblk) * kFlatThreads;
+  for (int64_t g = static_cast<int64_t>(blk) * kFlatThreads + threadIdx.x; g < total; g += kAgU * TT) {
     V8 v[kAgU];
     int o[kAgU];
     int64_t u[kAgU];
@@ -168,6 +167,11 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) local_ag32_kerne
         if (dst != p.send[o[k]] + 32 * u[k]) st32(dst, v[k]);  // in place: rank o's own block is there
       }
   }
+}
+
+__global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) local_ag32_kernel(const __grid_constant__ LPlan p) {
+  pdl_enter();
+  local_ag32_body(p, blockIdx.x, gridDim.x);
 }
 
 // All-gather through the tensor memory accelerator: one elected thread per CTA streams tiles of
@@ -279,12 +283,12 @@ __device__ __forceinline__ void local_rs_body(const LPlan& p) {
 // n = 8, 1 MiB fp32, against 11.3-12.3 us for the per-rank two-wave grid, which varies with the
 // box; a bulk-copy-staged variant reached only 12.7 us).
 template <int DT, int OP, int N>
-__device__ __forceinline__ void local_rs_flat(const LPlan& p) {
+__device__ __forceinline__ void local_rs_flat(const LPlan& p, int blk, int nblk) {
   const int64_t Cb = p.chunk_bytes;
   const int64_t nu = Cb >> 4;
   const int64_t total = N * nu;
-  const int64_t TT = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += TT) {
+  const int64_t TT = static_cast<int64_t>(nblk) * blockDim.x;
+  for (int64_t g = static_cast<int64_t>(blk) * blockDim.x + threadIdx.x; g < total; g += TT) {
     const int r = static_cast<int>(g / nu);
     const int64_t off = r * Cb + 16 * (g - r * nu);
     uint4 x[N];
@@ -314,19 +318,104 @@ __global__ void __launch_bounds__(kLocalThreads, 2) local_rs_kernel(const __grid
 }
 
 template <int DT, int OP>
-__global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) local_rs_flat_kernel(const __grid_constant__ LPlan p) {
-  pdl_enter();
+__device__ __forceinline__ void local_rs_flat_any(const LPlan& p, int blk, int nblk) {
   switch (p.n) {
-    case 1: local_rs_flat<DT, OP, 1>(p); break;
-    case 2: local_rs_flat<DT, OP, 2>(p); break;
-    case 3: local_rs_flat<DT, OP, 3>(p); break;
-    case 4: local_rs_flat<DT, OP, 4>(p); break;
-    case 5: local_rs_flat<DT, OP, 5>(p); break;
-    case 6: local_rs_flat<DT, OP, 6>(p); break;
-    case 7: local_rs_flat<DT, OP, 7>(p); break;
-    default: local_rs_flat<DT, OP, 8>(p); break;
+    case 1: local_rs_flat<DT, OP, 1>(p, blk, nblk); break;
+    case 2: local_rs_flat<DT, OP, 2>(p, blk, nblk); break;
+    case 3: local_rs_flat<DT, OP, 3>(p, blk, nblk); break;
+    case 4: local_rs_flat<DT, OP, 4>(p, blk, nblk); break;
+    case 5: local_rs_flat<DT, OP, 5>(p, blk, nblk); break;
+    case 6: local_rs_flat<DT, OP, 6>(p, blk, nblk); break;
+    case 7: local_rs_flat<DT, OP, 7>(p, blk, nblk); break;
+    default: local_rs_flat<DT, OP, 8>(p, blk, nblk); break;
   }
 }
+
+template <int DT, int OP>
+__global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) local_rs_flat_kernel(const __grid_constant__ LPlan p) {
+  pdl_enter();
+  local_rs_flat_any<DT, OP>(p, blockIdx.x, gridDim.x);
+}
+
+// A grouped all-gather (a) + reduce-scatter (b, sum) in one launch (patGroupStart/End): the
+// first `ga` CTAs broadcast, the rest fold, at the same time — the write-bound broadcast and the
+// read-bound fold share HBM instead of taking turns, and one launch ramps up and drains.
+struct LPlan2 {
+  LPlan a, b;
+  int ga;
+};
+// Interleaved form (default): every thread does both kinds of work each round — kAgU broadcast
+// units, then qB fold units — so the two calls drain together instead of one half of the grid
+// idling while the other finishes.
+template <int DT, int N>
+__device__ __forceinline__ void local_group_interleaved(const LPlan2& p) {
+  const int64_t nuA = p.a.chunk_bytes >> 5, totA = N * nuA;
+  const int64_t nuB = p.b.chunk_bytes >> 4, totB = N * nuB;
+  const int64_t TT = static_cast<int64_t>(gridDim.x) * kFlatThreads;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * kFlatThreads + threadIdx.x;
+  const int64_t rounds = std::max<int64_t>(1, (totA + kAgU * TT - 1) / (kAgU * TT));
+  const int64_t qB = (totB + rounds * TT - 1) / (rounds * TT);
+  const int64_t CbA = p.a.chunk_bytes, CbB = p.b.chunk_bytes;
+  for (int64_t rd = 0; rd < rounds; ++rd) {
+    V8 v[kAgU];
+    int o[kAgU];
+    int64_t u[kAgU];
+#pragma unroll
+    for (int k = 0; k < kAgU; ++k) {  // broadcast loads first: in flight while the folds run
+      const int64_t gg = tid + (rd * kAgU + k) * TT;
+      o[k] = gg < totA ? static_cast<int>(gg / nuA) : -1;
+      u[k] = gg - static_cast<int64_t>(o[k]) * nuA;
+      if (o[k] >= 0) v[k] = ld_nc32(p.a.send[o[k]] + 32 * u[k]);
+    }
+    for (int64_t j = 0; j < qB; ++j) {
+      const int64_t g = tid + (rd * qB + j) * TT;
+      if (g >= totB) break;
+      const int r = static_cast<int>(g / nuB);
+      const int64_t off = r * CbB + 16 * (g - r * nuB);
+      uint4 x[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        int src = r + i;
+        src = src >= N ? src - N : src;
+        x[i] = ld_nc16(p.b.send[src] + off);
+      }
+      st_cs16(p.b.recv[r] + (off - r * CbB), tree<DT, kSum, N>(x));
+    }
+    for (int dst_r = 0; dst_r < N; ++dst_r)
+#pragma unroll
+      for (int k = 0; k < kAgU; ++k) {
+        if (o[k] < 0) continue;
+        char* dst = p.a.recv[dst_r] + o[k] * CbA + 32 * u[k];
+        if (dst != p.a.send[o[k]] + 32 * u[k]) st32(dst, v[k]);
+      }
+  }
+}
+
+constexpr int kGroupCtasPerSm = 3;  // the interleaved body needs ~80 registers (4 CTAs/SM: 64, spills)
+template <int DT>
+__global__ void __launch_bounds__(kFlatThreads, kGroupCtasPerSm) local_group_kernel(const __grid_constant__ LPlan2 p) {
+  pdl_enter();
+  if (p.ga < 0) {  // interleaved
+    switch (p.a.n) {
+      case 1: local_group_interleaved<DT, 1>(p); break;
+      case 2: local_group_interleaved<DT, 2>(p); break;
+      case 3: local_group_interleaved<DT, 3>(p); break;
+      case 4: local_group_interleaved<DT, 4>(p); break;
+      case 5: local_group_interleaved<DT, 5>(p); break;
+      case 6: local_group_interleaved<DT, 6>(p); break;
+      case 7: local_group_interleaved<DT, 7>(p); break;
+      default: local_group_interleaved<DT, 8>(p); break;
+    }
+    return;
+  }
+  if (static_cast<int>(blockIdx.x) < p.ga) local_ag32_body(p.a, blockIdx.x, p.ga);
+  else local_rs_flat_any<DT, kSum>(p.b, blockIdx.x - p.ga, gridDim.x - p.ga);
+}
+using LocalGroupFn = void (*)(const LPlan2);
+static const LocalGroupFn kLocalGroup[10] = {
+    local_group_kernel<kI8>, local_group_kernel<kU8>, local_group_kernel<kI32>, local_group_kernel<kU32>,
+    local_group_kernel<kI64>, local_group_kernel<kU64>, local_group_kernel<kF16>, local_group_kernel<kF32>,
+    local_group_kernel<kF64>, local_group_kernel<kBF16>};
 
 using LocalFn = void (*)(const LPlan);
 #define PAT_LRS_ROW(DT) \
@@ -430,6 +519,51 @@ cudaError_t launch_local(int kind, int n, int dtype, int op, int vec, int esize,
   cfg.blockDim = dim3(kLocalThreads);
   if (kind == 0) return cudaLaunchKernelEx(&cfg, local_ag_kernel, p);
   return cudaLaunchKernelEx(&cfg, kLocalRs[dtype][op], p);
+}
+
+// Grouped all-gather (chunk a_bytes) + reduce-scatter (sum, chunk b_bytes) of one single-device
+// communicator in one launch. Returns cudaErrorNotSupported when the flat kernels cannot take
+// both (alignment): the caller launches them one after the other instead.
+cudaError_t launch_local_group(int n, int dtype, int64_t a_bytes, const char* const* a_send, char* const* a_recv,
+                               int64_t b_bytes, const char* const* b_send, char* const* b_recv, int sm_count,
+                               cudaStream_t stream) {
+  LPlan2 p{};
+  p.a.n = p.b.n = n;
+  p.a.kind = 0;
+  p.b.kind = 1;
+  p.a.vec = p.b.vec = 16;
+  p.a.chunk_bytes = a_bytes;
+  p.b.chunk_bytes = b_bytes;
+  bool ok = (a_bytes % 32) == 0 && (b_bytes % 16) == 0;
+  for (int r = 0; r < n; ++r) {
+    p.a.send[r] = a_send[r];
+    p.a.recv[r] = a_recv[r];
+    p.b.send[r] = b_send[r];
+    p.b.recv[r] = b_recv[r];
+    ok = ok && ((reinterpret_cast<uintptr_t>(a_send[r]) | reinterpret_cast<uintptr_t>(a_recv[r])) % 32) == 0 &&
+         ((reinterpret_cast<uintptr_t>(b_send[r]) | reinterpret_cast<uintptr_t>(b_recv[r])) % 16) == 0;
+  }
+  if (!ok) return cudaErrorNotSupported;
+  // CTAs split in proportion to each call's HBM bytes ((n^2 + n) C for both)
+  const int grid = kGroupCtasPerSm * sm_count;
+  const double wa = static_cast<double>(a_bytes), wb = static_cast<double>(b_bytes);
+  p.ga = std::max(1, std::min(grid - 1, static_cast<int>(grid * wa / (wa + wb) + 0.5)));
+  // PAT_GROUP_LOCAL: 0 = interleaved (default), 1 = the grid split in two halves
+  static const int mode = [] {
+    const char* e = std::getenv("PAT_GROUP_LOCAL");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (mode == 0) p.ga = -1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFlatThreads);
+  return cudaLaunchKernelEx(&cfg, kLocalGroup[dtype], p);
 }
 
 }  // namespace pat

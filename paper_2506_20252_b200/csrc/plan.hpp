@@ -53,6 +53,8 @@ struct KPlan {
   int n, nrounds, nslots, nlocal;
   int kind, proto, vec, esize;
   int channels, iters;
+  int chan_base;    // first channel (flags, counters, inbox) of this call: grouped calls share a launch
+                    // on disjoint channel ranges [chan_base, chan_base + channels)
   int depth;        // inbox buffers per channel (pipeline depth); buffer of step g = g % depth
   int send_warps;   // SIMPLE: warps [0, send_warps) push, the rest deliver / fold
   int gpu_scope;    // all ranks on this device: flags and fences at .gpu scope instead of .sys
@@ -108,6 +110,12 @@ struct KPlan {
   // (the reference's StatsBuilder occupancy, simulate.cpp:109-129, brute_force.hpp:25-54)
   int* occ;
   int64_t region_bytes;  // bytes of the inbox region this launch uses (bounds checks, PAT_BOUNDS_CHECK builds)
+};
+
+// Two independent collectives of one communicator in one launch (patGroupStart/End): CTAs
+// [0, a.nlocal * a.channels) run `a` (all-gather), the rest `b` (reduce-scatter).
+struct KPlan2 {
+  KPlan a, b;
 };
 
 // Device barrier (patCommBarrier): every rank's barrier words, as seen from the launching device.

@@ -8,4 +8,7 @@ using KernelFn = void (*)(const KPlan);
                                   pat_kernel<DT, kMin, kRS>};
 PAT_RS_ROW(kF16, kRsRowF16)
 PAT_RS_ROW(kBF16, kRsRowBF16)
+using GroupFn = void (*)(const KPlan2);
+extern const GroupFn kGroupF16 = pat_group_kernel<kF16>;
+extern const GroupFn kGroupBF16 = pat_group_kernel<kBF16>;
 }  // namespace pat

@@ -7,4 +7,6 @@ using KernelFn = void (*)(const KPlan);
   extern const KernelFn NAME[4] = {pat_kernel<DT, kSum, kRS>, pat_kernel<DT, kProd, kRS>, pat_kernel<DT, kMax, kRS>, \
                                   pat_kernel<DT, kMin, kRS>};
 PAT_RS_ROW(kF32, kRsRowF32)
+using GroupFn = void (*)(const KPlan2);
+extern const GroupFn kGroupF32 = pat_group_kernel<kF32>;
 }  // namespace pat

@@ -8,4 +8,7 @@ using KernelFn = void (*)(const KPlan);
                                   pat_kernel<DT, kMin, kRS>};
 PAT_RS_ROW(kI32, kRsRowI32)
 PAT_RS_ROW(kU32, kRsRowU32)
+using GroupFn = void (*)(const KPlan2);
+extern const GroupFn kGroupI32 = pat_group_kernel<kI32>;
+extern const GroupFn kGroupU32 = pat_group_kernel<kU32>;
 }  // namespace pat

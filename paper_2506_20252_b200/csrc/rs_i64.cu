@@ -8,4 +8,7 @@ using KernelFn = void (*)(const KPlan);
                                   pat_kernel<DT, kMin, kRS>};
 PAT_RS_ROW(kI64, kRsRowI64)
 PAT_RS_ROW(kU64, kRsRowU64)
+using GroupFn = void (*)(const KPlan2);
+extern const GroupFn kGroupI64 = pat_group_kernel<kI64>;
+extern const GroupFn kGroupU64 = pat_group_kernel<kU64>;
 }  // namespace pat

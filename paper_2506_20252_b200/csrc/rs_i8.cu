@@ -8,4 +8,7 @@ using KernelFn = void (*)(const KPlan);
                                   pat_kernel<DT, kMin, kRS>};
 PAT_RS_ROW(kI8, kRsRowI8)
 PAT_RS_ROW(kU8, kRsRowU8)
+using GroupFn = void (*)(const KPlan2);
+extern const GroupFn kGroupI8 = pat_group_kernel<kI8>;
+extern const GroupFn kGroupU8 = pat_group_kernel<kU8>;
 }  // namespace pat

@@ -288,7 +288,7 @@ struct Step {
 __device__ __forceinline__ Step make_step(const KPlan& p, uint64_t base, int i, int R, int lr, int c) {
   Step s;
   s.g = base + i;
-  s.off = (static_cast<int64_t>(i) * p.channels + c) * p.slice_bytes;
+  s.off = (static_cast<int64_t>(i) * p.channels + (c - p.chan_base)) * p.slice_bytes;
   s.len = max(int64_t{0}, min(p.slice_bytes, p.chunk_bytes - s.off));
   s.R = R;
   s.lr = lr;
@@ -301,8 +301,8 @@ __device__ __forceinline__ Step make_step(const KPlan& p, uint64_t base, int i, 
 
 
 __device__ __forceinline__ char* slot_ptr(const KPlan& p, int rank, int c, int buf, int j) {
-  PAT_BOUND(rank >= 0 && rank < p.n && c >= 0 && c < p.channels && buf >= 0 && buf < p.depth && j >= 0 &&
-            j < p.nslots);
+  PAT_BOUND(rank >= 0 && rank < p.n && c >= p.chan_base && c < p.chan_base + p.channels && buf >= 0 &&
+            buf < p.depth && j >= 0 && j < p.nslots);
   PAT_BOUND(c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j + 1) * p.slot_stride <= p.region_bytes);
   return p.inbox[rank] + c * p.chan_stride + (static_cast<int64_t>(buf) * p.nslots + j) * p.slot_stride;
 }
@@ -498,7 +498,7 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
         for (int t2 = 0; t2 < NR; ++t2) send_round<DT, OP, KIND>(p, s, t2, wm, w, tid, nthr, false, kLeafPos);
     }
     send_round<DT, OP, KIND>(p, s, t, wm, w, tid, nthr, signal, p.leaves_first ? kFwdPos : kAllPos);
-    if (p.occ && i == 0 && c == 0 && tid == 0) occ_sent(p, lr, t);
+    if (p.occ && i == 0 && c == p.chan_base && tid == 0) occ_sent(p, lr, t);
     tr.rec(kEvPushed, s.g, t);
     if (signal && t == NR - 1 && tid == 0) *sent_steps = s.g + 1;  // after the round's barrier
   };
@@ -551,7 +551,7 @@ __device__ void recv_step(const KPlan& p, const Step& s, Waiter& w, int tid, int
   for (int t = 0; t < p.nrounds; ++t) {
     if (tid == 0) {
       wait_flag(myflags + t, s.g + 1, w);
-      if (p.occ && first_step && s.c == 0) occ_arrived(p, s.lr, t);
+      if (p.occ && first_step && s.c == p.chan_base) occ_arrived(p, s.lr, t);
     }
     tr.rec(kEvArrived, s.g, t);
     named_bar(2, nthr);
@@ -1032,10 +1032,12 @@ __device__ void pull_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
   if (tid < n && tid != R) wait_flag(myflags + 8 + tid, base + p.iters, w);
 }
 
+// One CTA of a call: virtual block vb in [0, nlocal * channels) runs channel chan_base + vb %
+// channels of local rank vb / channels.
 template <int DT, int OP, int KIND>
-__global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant__ KPlan p) {
-  const int lr = blockIdx.x / p.channels;
-  const int c = blockIdx.x - lr * p.channels;
+__device__ __forceinline__ void pat_body(const KPlan& p, int vb) {
+  const int lr = vb / p.channels;
+  const int c = p.chan_base + (vb - lr * p.channels);
   const int R = p.rank[lr];
   __shared__ uint64_t s_base;
   __shared__ volatile uint64_t s_sent;
@@ -1137,6 +1139,20 @@ __global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant_
   }
   __syncthreads();
   if (threadIdx.x == 0) p.iter_state[lr][c] = base + p.iters;
+}
+
+template <int DT, int OP, int KIND>
+__global__ void __launch_bounds__(kMaxThreads) pat_kernel(const __grid_constant__ KPlan p) {
+  pat_body<DT, OP, KIND>(p, blockIdx.x);
+}
+
+// A grouped all-gather + reduce-scatter (patGroupStart/End) in one launch: the two calls run
+// side by side on disjoint channels, so their latencies overlap instead of adding up.
+template <int DT>
+__global__ void __launch_bounds__(kMaxThreads) pat_group_kernel(const __grid_constant__ KPlan2 p) {
+  const int na = p.a.nlocal * p.a.channels;
+  if (static_cast<int>(blockIdx.x) < na) pat_body<kU8, kSum, kAG>(p.a, blockIdx.x);
+  else pat_body<DT, kSum, kRS>(p.b, blockIdx.x - na);
 }
 
 }  // namespace pat

@@ -14,6 +14,41 @@ import oracle as O  # noqa: E402
 from paper_2506_20252_b200 import PatComm  # noqa: E402
 
 
+def group_section(rank, n, dev):
+    """patGroupStart/End across processes: one launch runs the all-gather and the reduce-scatter on
+    disjoint channel halves; bit-exact, both orders, LL32 and SIMPLE sizes."""
+    from paper_2506_20252_b200 import group
+    fails = 0
+    comm = PatComm.from_process_group(device=dev.index)
+    for elems in (3000, 1 << 18, 1 << 22):
+        for rs_first in (False, True):
+            p = O.random_payload(O.FLOAT32, n, elems, elems + rs_first)
+            q = O.random_payload(O.FLOAT32, n * n, elems, elems + 7)
+            s = torch.from_numpy(p[rank * elems:(rank + 1) * elems].copy()).to(dev)
+            r = torch.zeros(n * elems, dtype=torch.float32, device=dev)
+            s2 = torch.from_numpy(q[rank * n * elems:(rank + 1) * n * elems].copy()).to(dev)
+            r2 = torch.zeros(elems, dtype=torch.float32, device=dev)
+            with group():
+                if rs_first:
+                    comm.reduce_scatter([s2], [r2], elems, O.FLOAT32, O.SUM)
+                    comm.all_gather([s], [r], elems, O.FLOAT32)
+                else:
+                    comm.all_gather([s], [r], elems, O.FLOAT32)
+                    comm.reduce_scatter([s2], [r2], elems, O.FLOAT32, O.SUM)
+            torch.cuda.synchronize(dev)
+            want, _ = O.run_allgather(O.pat_allgather(n, O.max_trees(n)), O.FLOAT32, p, elems)
+            if r.cpu().numpy().tobytes() != want[rank].tobytes():
+                fails += 1
+                print(f"rank {rank} grouped AG mismatch elems={elems} rs_first={rs_first}", flush=True)
+            want, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, O.max_trees(n)), O.FLOAT32, O.SUM, q, elems)
+            if r2.cpu().numpy().tobytes() != want[rank].tobytes():
+                fails += 1
+                print(f"rank {rank} grouped RS mismatch elems={elems} rs_first={rs_first}", flush=True)
+    comm.raise_async_error()
+    comm.destroy()
+    return fails
+
+
 def windows_section(rank, n, dev):
     """Symmetric windows (patCommRegister*): zero-copy direct all-gather, PULL reduce-scatter and
     PULL all-gather across processes, bit-exact; then a rank-dependent offset must be refused."""
@@ -140,6 +175,7 @@ def main():
             print(f"rank {rank} reduce_scatter_tensor differs from the oracle elems={elems}", flush=True)
     comm.raise_async_error()
     comm.destroy()
+    fails += group_section(rank, n, dev)
     fails += windows_section(rank, n, dev)
     t = torch.tensor([fails], device=dev)
     dist.all_reduce(t)

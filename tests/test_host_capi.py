@@ -145,3 +145,13 @@ def test_comm_init_without_gpu_fails_cleanly():
     with pytest.raises(_lib.PatError):
         from paper_2506_20252_b200 import PatComm
         PatComm.init_all(2, [0, 0])
+
+
+def test_group_calls_without_gpu():
+    """patGroupEnd without patGroupStart is InvalidUsage; nested groups balance (no GPU needed)."""
+    from paper_2506_20252_b200 import _lib as L
+    lib = L.lib()
+    assert lib.patGroupEnd() == 5
+    assert lib.patGroupStart() == 0 and lib.patGroupStart() == 0
+    assert lib.patGroupEnd() == 0 and lib.patGroupEnd() == 0
+    assert lib.patGroupEnd() == 5
