@@ -666,7 +666,8 @@ def run_pat(args, rank, world, local):
                 roof["traffic_source"] = tr[key].get("source")
                 if "nvlink_tx_bytes_per_launch" in tr[key]:  # NVLink egress of the same ncu launch
                     roof["nvlink_tx_bytes"] = tr[key]["nvlink_tx_bytes_per_launch"]
-                    roof["nvlink_tx_user_bytes"] = tr[key]["nvlink_tx_user_bytes_per_launch"]
+                    if "nvlink_tx_user_bytes_per_launch" in tr[key]:
+                        roof["nvlink_tx_user_bytes"] = tr[key]["nvlink_tx_user_bytes_per_launch"]
         except Exception:
             pass
 
