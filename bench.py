@@ -617,30 +617,51 @@ def run_pat(args, rank, world, local):
     dom = "reduce_scatter" if rs_ms >= ag_ms else "all_gather"
     dom_us = 1e3 * max(ag_ms, rs_ms) / K
     if mode == "local":
-        algo_bytes = (n * n + n) * C  # local mode: read n*C + write n^2*C (AG) / read n^2*C + write n*C (RS)
+        # local mode: read n*C + write n^2*C (AG) / read n^2*C + write n*C (RS) per collective; a
+        # grouped step is ONE launch (local_group_kernel) doing both, and it is the step's kernel
+        coll_bytes = (n * n + n) * C
         peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-        roof = {"bound": "hbm", "kernel": ("local_rs_flat_kernel" if dom == "reduce_scatter" else "local_ag32_kernel"),
-                "unit": "GB/s", "algorithmic_bytes_per_launch": algo_bytes,
-                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
-                "write_ceiling_note": "the all-gather is (n^2 C writes + n C reads): a write-only kernel of the same "
-                                      "72 MiB takes 12.2 us = 0.94 of hbm_gbs (profiles/r02_local_tune.jsonl, "
-                                      "ceil_write_only), so ~0.94 bounds the all-gather's frac"}
+        per_coll = {c_: {"kernel": k_, "us": 1e3 * t_ / K, "frac": coll_bytes / (t_ / K * 1e-3) / 1e9 / peak}
+                    for c_, k_, t_ in (("all_gather", "local_ag32_kernel", ag_ms),
+                                       ("reduce_scatter", "local_rs_flat_kernel", rs_ms))}
+        if not args.no_group:
+            algo_bytes, dom_us = 2 * coll_bytes, 1e3 * step_ms / K
+            kern = "local_group_kernel (the grouped step: all-gather + reduce-scatter in one launch)"
+        else:
+            algo_bytes = coll_bytes
+            kern = "local_rs_flat_kernel" if dom == "reduce_scatter" else "local_ag32_kernel"
+        roof = {"bound": "hbm", "kernel": kern, "unit": "GB/s", "algorithmic_bytes_per_launch": algo_bytes,
+                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs", "per_collective": per_coll}
         achieved = algo_bytes / (dom_us * 1e-6) / 1e9
-        # live write-only ceiling for the same byte count (the all-gather is n^2 C writes + n C
-        # reads): K fills of a 72 MiB buffer, rotated over 4 (more than 2x L2), events around them
-        wbufs = [torch.empty(algo_bytes // 4, device=dev0) for _ in range(4)]
-        for b_ in wbufs:
+        # live ceilings for the same byte counts, K launches over 4 rotating buffers (> 2x L2):
+        # a copy (the grouped step's 50/50 read/write mix) and a fill (the all-gather is write-bound)
+        nel = coll_bytes // 4
+        cbufs = [torch.empty(nel, device=dev0) for _ in range(8)]
+        for b_ in cbufs:
             b_.fill_(0.0)
         D.sync()
+
+        def copies():
+            with torch.cuda.stream(D.streams[devices[0]]):
+                for k in range(K):
+                    cbufs[2 * (k % 4) + 1].copy_(cbufs[2 * (k % 4)])
+
         def fills():
             with torch.cuda.stream(D.streams[devices[0]]):
                 for k in range(K):
-                    wbufs[k % 4].fill_(float(k))
+                    cbufs[k % 4].fill_(float(k))
+        copies()  # warm: lazy module loading of the copy kernel
+        fills()
+        D.sync()
+        copy_ms = D.time_ms(copies)
         fill_ms = D.time_ms(fills)
-        wgbs = algo_bytes / (fill_ms / K * 1e-3) / 1e9
+        cgbs = 2 * coll_bytes / (copy_ms / K * 1e-3) / 1e9
+        wgbs = coll_bytes / (fill_ms / K * 1e-3) / 1e9
+        roof["copy_ceiling"] = {"gbs": cgbs, "frac_of_peak": cgbs / peak, "us": 1e3 * copy_ms / K,
+                                "kernel": "torch copy_ of 72 MiB (144 MiB of traffic), K launches"}
         roof["write_ceiling"] = {"gbs": wgbs, "frac_of_peak": wgbs / peak, "us": 1e3 * fill_ms / K,
-                                 "kernel": "torch fill_ of the same bytes (write-only), K launches, 4 rotating buffers"}
-        del wbufs
+                                 "kernel": "torch fill_ of 72 MiB (write-only), K launches"}
+        del cbufs
     else:
         # per GPU: every rank on it receives (n-1)*C over NVLink per launch (ranks sharing a GPU
         # share its links, so the GPU's ingress is ranks_on_gpu * (n-1) * C minus what stays local)
@@ -654,13 +675,17 @@ def run_pat(args, rank, world, local):
         roof["frac_of_sm_push_704"] = achieved / NVLINK_SM_PUSH_GBS
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
                  "launch_us": dom_us})
-    if "write_ceiling" in roof and dom == "all_gather":
-        roof["frac_of_write_ceiling"] = achieved / roof["write_ceiling"]["gbs"]
+    if "copy_ceiling" in roof and not args.no_group:
+        roof["frac_of_copy_ceiling"] = achieved / roof["copy_ceiling"]["gbs"]
+    if "write_ceiling" in roof:
+        roof["per_collective"]["all_gather"]["frac_of_write_ceiling"] = (
+            coll_bytes / (ag_ms / K * 1e-3) / 1e9 / roof["write_ceiling"]["gbs"])
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath))
-            key = f"{'local' if mode == 'local' else 'nvlink'}_n{n}_{dom}"
+            key = (f"local_n{n}_group" if mode == "local" and not args.no_group else
+                   f"{'local' if mode == 'local' else 'nvlink'}_n{n}_{dom}")
             if key in tr:
                 roof["traffic"] = tr[key]["dram_bytes_per_launch"]
                 roof["traffic_source"] = tr[key].get("source")

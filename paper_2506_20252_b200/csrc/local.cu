@@ -391,7 +391,7 @@ __device__ __forceinline__ void local_group_interleaved(const LPlan2& p) {
   }
 }
 
-constexpr int kGroupCtasPerSm = 3;  // the interleaved body needs ~80 registers (4 CTAs/SM: 64, spills)
+constexpr int kGroupCtasPerSm = 2;  // interleaved body: ~80 registers; 2 CTAs/SM measured 1% faster than 3 (tools/local_tune.cu group)
 template <int DT>
 __global__ void __launch_bounds__(kFlatThreads, kGroupCtasPerSm) local_group_kernel(const __grid_constant__ LPlan2 p) {
   pdl_enter();

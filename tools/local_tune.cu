@@ -474,6 +474,116 @@ __global__ void __launch_bounds__(512, 2) ronly(const __grid_constant__ P p, int
   if (acc == 0x12345678u) *sink = 1;
 }
 
+// ---------------------------------------------------------------- grouped AG + RS (one launch)
+// P2: both calls' buffers (AG in a, RS in b), equal chunk bytes.
+struct P2 {
+  P a, b;
+};
+__device__ __forceinline__ void fold8_v8(V8& a, const V8& b) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a.w[i] = __float_as_uint(__uint_as_float(a.w[i]) + __uint_as_float(b.w[i]));
+}
+// RSW = 16 or 32 bytes per fold unit; CS = streaming stores for the broadcast
+template <int RSW, int CS, int MINB>
+__global__ void __launch_bounds__(256, MINB) grpI(const __grid_constant__ P2 p) {
+  pdl_enter();
+  const int64_t nuA = p.a.Cb >> 5, totA = N * nuA;
+  const int64_t nuB = p.b.Cb / RSW, totB = N * nuB;
+  const int64_t TT = static_cast<int64_t>(gridDim.x) * 256;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  const int64_t rounds = max(int64_t{1}, (totA + 2 * TT - 1) / (2 * TT));
+  const int64_t qB = (totB + rounds * TT - 1) / (rounds * TT);
+  for (int64_t rd = 0; rd < rounds; ++rd) {
+    V8 v[2];
+    int o[2];
+    int64_t u[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int64_t gg = tid + (rd * 2 + k) * TT;
+      o[k] = gg < totA ? static_cast<int>(gg / nuA) : -1;
+      u[k] = gg - static_cast<int64_t>(o[k]) * nuA;
+      if (o[k] >= 0) v[k] = ld_nc32(p.a.send[o[k]] + 32 * u[k]);
+    }
+    for (int64_t j = 0; j < qB; ++j) {
+      const int64_t g = tid + (rd * qB + j) * TT;
+      if (g >= totB) break;
+      const int r = static_cast<int>(g / nuB);
+      const int64_t off = r * p.b.Cb + RSW * (g - r * nuB);
+      if constexpr (RSW == 16) {
+        uint4 x[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = ld_nc16(p.b.send[(r + i) % N] + off);
+        st_cs16(p.b.recv[r] + (off - r * p.b.Cb), tree8(x));
+      } else {
+        V8 x[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = ld_nc32(p.b.send[(r + i) % N] + off);
+        auto f = [](V8 a, const V8& b) { fold8_v8(a, b); return a; };
+        V8 t = f(f(f(x[0], x[1]), f(x[3], x[2])), f(f(x[5], f(x[7], x[6])), x[4]));
+        st32<1>(p.b.recv[r] + (off - r * p.b.Cb), t);
+      }
+    }
+    for (int d = 0; d < N; ++d)
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (o[k] >= 0) st32<CS>(p.a.recv[d] + o[k] * p.a.Cb + 32 * u[k], v[k]);
+  }
+}
+// split halves: blocks [0, ga) broadcast (agD body), the rest fold (rsB body)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) grpS(const __grid_constant__ P2 p, int ga) {
+  pdl_enter();
+  if (static_cast<int>(blockIdx.x) < ga) {
+    const int64_t nu = p.a.Cb >> 5, total = N * nu, TT = static_cast<int64_t>(ga) * 256;
+    for (int64_t g = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; g < total; g += 2 * TT) {
+      V8 v[2];
+      int o[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int64_t gg = g + k * TT;
+        o[k] = gg < total ? static_cast<int>(gg / nu) : -1;
+        if (o[k] >= 0) v[k] = ld_nc32(p.a.send[o[k]] + 32 * (gg - o[k] * nu));
+      }
+      for (int d = 0; d < N; ++d)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (o[k] >= 0) st32<0>(p.a.recv[d] + o[k] * p.a.Cb + 32 * (g + k * TT - o[k] * nu), v[k]);
+    }
+  } else {
+    const int b = blockIdx.x - ga, nb = gridDim.x - ga;
+    const int64_t nu = p.b.Cb >> 4, total = N * nu, TT = static_cast<int64_t>(nb) * 256;
+    for (int64_t g = static_cast<int64_t>(b) * 256 + threadIdx.x; g < total; g += TT) {
+      const int r = static_cast<int>(g / nu);
+      const int64_t off = r * p.b.Cb + 16 * (g - r * nu);
+      uint4 x[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = ld_nc16(p.b.send[(r + i) % N] + off);
+      st_cs16(p.b.recv[r] + (off - r * p.b.Cb), tree8(x));
+    }
+  }
+}
+// mixed-traffic ceiling: a plain copy of the same bytes (reads 72 MiB, writes 72 MiB)
+__global__ void __launch_bounds__(256, 4) copyK(const __grid_constant__ P2 p) {
+  pdl_enter();
+  const int64_t per = (N + 1) * p.a.Cb >> 5;  // per "rank": read send[r] region -> write recv[r]
+  const int64_t total = N * per, TT = static_cast<int64_t>(gridDim.x) * 256;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; g < total; g += 2 * TT) {
+    V8 v[2];
+    int r[2];
+    int64_t u[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int64_t gg = g + k * TT;
+      r[k] = gg < total ? static_cast<int>(gg / per) : -1;
+      u[k] = gg - static_cast<int64_t>(r[k]) * per;
+      if (r[k] >= 0) v[k] = ld_nc32(p.b.send[r[k]] + 32 * u[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (r[k] >= 0) st32<0>(p.a.recv[r[k]] + 32 * u[k], v[k]);
+  }
+}
+
 // ----------------------------------------------------------------------------- harness
 struct Set {
   char* ag_send[N];
@@ -592,7 +702,71 @@ int main(int argc, char** argv) {
                 bytes / usg / 1e3 / 6558.4, bad);
     std::fflush(stdout);
   };
+  auto run2 = [&](const char* name, dim3 grid, auto kern, auto... extra) {
+    auto once = [&](int k) {
+      Set& s = sets[k % S];
+      P2 p{};
+      p.a.Cb = p.b.Cb = Cb;
+      for (int r = 0; r < N; ++r) {
+        p.a.send[r] = s.ag_send[r];
+        p.a.recv[r] = s.ag_recv[r];
+        p.b.send[r] = s.rs_send[r];
+        p.b.recv[r] = s.rs_recv[r];
+      }
+      cudaLaunchConfig_t c = make_cfg(grid, dim3(256), 0);
+      CK(cudaLaunchKernelEx(&c, kern, p, extra...));
+    };
+    for (int r = 0; r < N; ++r) CK(cudaMemsetAsync(sets[0].rs_recv[r], 0xab, Cb, st));
+    once(0);
+    CK(cudaStreamSynchronize(st));
+    int bad = 0;
+    for (int r = 0; r < N; ++r) {
+      CK(cudaMemcpy(got.data(), sets[0].rs_recv[r], Cb, cudaMemcpyDeviceToHost));
+      if (have_rs && std::memcmp(got.data(), ref_rs.data() + r * Cb, Cb) != 0) ++bad;
+      CK(cudaMemcpy(got.data(), sets[0].ag_recv[r], N * Cb, cudaMemcpyDeviceToHost));
+      if (have_ag && std::memcmp(got.data(), ref_ag.data(), N * Cb) != 0) ++bad;
+    }
+    for (int k = 0; k < 3 * S; ++k) once(k);
+    float bestg = 1e30f;
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    for (int k = 0; k < L; ++k) once(k);
+    CK(cudaStreamEndCapture(st, &g));
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    CK(cudaGraphLaunch(ge, st));
+    for (int rep = 0; rep < 3; ++rep) {
+      CK(cudaEventRecord(e0, st));
+      CK(cudaGraphLaunch(ge, st));
+      CK(cudaEventRecord(e1, st));
+      CK(cudaStreamSynchronize(st));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      bestg = std::min(bestg, ms);
+    }
+    CK(cudaGraphExecDestroy(ge));
+    CK(cudaGraphDestroy(g));
+    const double usg = 1e3 * bestg / L;
+    std::printf("{\"kernel\": \"%s\", \"us_graph\": %.3f, \"GBps\": %.1f, \"frac_6558\": %.4f, \"bad\": %d}\n", name,
+                usg, 2 * bytes / usg / 1e3, 2 * bytes / usg / 1e3 / 6558.4, bad);
+    std::fflush(stdout);
+  };
   const std::string only = argc > 3 ? argv[3] : "";
+  if (only == "group") {
+    run("rsB_ref", true, dim3(4 * sms), dim3(256), 0, rsB<1, 256, 4, false>);
+    run("agD_ref", false, dim3(4 * sms), dim3(256), 0, agD<2, 256, 4, 0>);
+    run2("grpI_rs16_cs0_3pSM", dim3(3 * sms), grpI<16, 0, 3>);
+    run2("grpI_rs16_cs1_3pSM", dim3(3 * sms), grpI<16, 1, 3>);
+    run2("grpI_rs32_cs0_3pSM", dim3(3 * sms), grpI<32, 0, 3>);
+    run2("grpI_rs32_cs0_2pSM", dim3(2 * sms), grpI<32, 0, 2>);
+    run2("grpI_rs16_cs0_2pSM", dim3(2 * sms), grpI<16, 0, 2>);
+    run2("grpS_4pSM_half", dim3(4 * sms), grpS<4>, 2 * sms);
+    run2("grpS_4pSM_ag40", dim3(4 * sms), grpS<4>, (4 * sms * 2) / 5);
+    run2("grpS_4pSM_ag60", dim3(4 * sms), grpS<4>, (4 * sms * 3) / 5);
+    have_rs = have_ag = false;
+    run2("copy_ceiling_same_bytes", dim3(4 * sms), copyK);
+    return 0;
+  }
   auto want = [&](const char* nm) { return only.empty() || std::string(nm).rfind(only, 0) == 0; };
   // reference variants first (they fill the expected outputs)
   run("rsA_592x512", true, dim3(8 * ((4 * sms + 7) / 8)), dim3(512), 0, rsA);
