@@ -525,16 +525,22 @@ def run_pat(args, rank, world, local):
         D.barrier()
         timing = "graph"
         try:
-            if not args.nccl_graph:  # capturing NCCL inside this process hangs (r02, 2 GPUs): eager
-                raise RuntimeError("eager")
+            if not args.nccl_graph:  # capturing NCCL inside this process hangs (r02, 2 GPUs, both with
+                raise RuntimeError("eager")  # raw capture and torch.cuda.graph): eager; graph-mode NCCL is in bench_sweep.py
             def nbody(kinds, count):
                 def run():
                     for k in range(count):
                         nccl_call(kinds, sets[k % S])
                 return run
+            def ncapture(body):  # as bench_sweep.py: torch.cuda.graph (global capture mode) on the timing stream
+                d = devices[0]
+                g_ = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_, stream=D.streams[d]):
+                    body()
+                return {d: g_}
             ngraphs = {}
             for kinds in (("ag", "rs"), ("ag",), ("rs",)):
-                ngraphs[kinds] = (D.capture(nbody(kinds, G)), D.capture(nbody(kinds, rem)) if rem else None)
+                ngraphs[kinds] = (ncapture(nbody(kinds, G)), ncapture(nbody(kinds, rem)) if rem else None)
             for pair in ngraphs.values():
                 replay_k(pair)()
             D.barrier()
