@@ -454,15 +454,29 @@ def run_pat(args, rank, world, local):
     # while step k-1 runs, and step k-1's results come down on another copy stream (PCIe is full
     # duplex); every step still copies all of its inputs in and its results out inside the
     # timed region.
-    h_ag_send = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(L)]
-    h_rs_send = [torch.empty(n * elems, dtype=torch.float32).pin_memory() for _ in range(L)]
-    h_ag_recv = [torch.empty(n * elems, dtype=torch.float32).pin_memory() for _ in range(L)]
-    h_rs_recv = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(L)]
+    # host buffers: one pinned block per direction and buffer kind, rank slices of it, so the ranks
+    # of one device move in ONE copy per kind (fewer, larger PCIe transfers)
+    hb = {k: torch.empty(L * m * elems, dtype=torch.float32).pin_memory()
+          for k, m in (("ag_send", 1), ("rs_send", n), ("ag_recv", n), ("rs_recv", 1))}
+    h_ag_send = list(hb["ag_send"].view(L, elems))
+    h_rs_send = list(hb["rs_send"].view(L, n * elems))
+    h_ag_recv = list(hb["ag_recv"].view(L, n * elems))
+    h_rs_recv = list(hb["rs_recv"].view(L, elems))
     for i in range(L):
         h_ag_send[i].copy_(sets[0]["ag_send"][i].cpu())
         h_rs_send[i].copy_(sets[0]["rs_send"][i].cpu())
     E = max(3, min(K, 20))
-    dsets = [sets[j % len(sets)] for j in range(2)]
+    one_dev = len(D.devs) == 1
+    if one_dev:  # device side likewise: the ranks' buffers are slices of one allocation per kind
+        def cset():
+            blk = {k: torch.empty(L * m * elems, device=dev0) for k, m in
+                   (("ag_send", 1), ("rs_send", n), ("ag_recv", n), ("rs_recv", 1))}
+            d_ = {k: list(v.view(L, -1)) for k, v in blk.items()}
+            d_["_blk"] = blk
+            return d_
+        dsets = [cset() for _ in range(2)]
+    else:
+        dsets = [sets[j % len(sets)] for j in range(2)]
     s_in = {d: torch.cuda.Stream(d) for d in D.devs}
     s_out = {d: torch.cuda.Stream(d) for d in D.devs}
     ev = lambda: {d: torch.cuda.Event() for d in D.devs}  # noqa: E731
@@ -479,10 +493,14 @@ def run_pat(args, rank, world, local):
             with torch.cuda.device(d), torch.cuda.stream(s_in[d]):
                 if k >= 2:
                     s_in[d].wait_event(comp_done[k - 2][d])  # set k % 2's inputs are free
-                for i, di in enumerate(devices):
-                    if di == d:
-                        bs["ag_send"][i].copy_(h_ag_send[i], non_blocking=True)
-                        bs["rs_send"][i].copy_(h_rs_send[i], non_blocking=True)
+                if one_dev:
+                    bs["_blk"]["ag_send"].copy_(hb["ag_send"], non_blocking=True)
+                    bs["_blk"]["rs_send"].copy_(hb["rs_send"], non_blocking=True)
+                else:
+                    for i, di in enumerate(devices):
+                        if di == d:
+                            bs["ag_send"][i].copy_(h_ag_send[i], non_blocking=True)
+                            bs["rs_send"][i].copy_(h_rs_send[i], non_blocking=True)
                 h2d_done[k][d].record(s_in[d])
             D.streams[d].wait_event(h2d_done[k][d])
             if k >= 2:
@@ -492,10 +510,14 @@ def run_pat(args, rank, world, local):
             comp_done[k][d].record(D.streams[d])
             with torch.cuda.device(d), torch.cuda.stream(s_out[d]):
                 s_out[d].wait_event(comp_done[k][d])
-                for i, di in enumerate(devices):
-                    if di == d:
-                        h_ag_recv[i].copy_(bs["ag_recv"][i], non_blocking=True)
-                        h_rs_recv[i].copy_(bs["rs_recv"][i], non_blocking=True)
+                if one_dev:
+                    hb["ag_recv"].copy_(bs["_blk"]["ag_recv"], non_blocking=True)
+                    hb["rs_recv"].copy_(bs["_blk"]["rs_recv"], non_blocking=True)
+                else:
+                    for i, di in enumerate(devices):
+                        if di == d:
+                            h_ag_recv[i].copy_(bs["ag_recv"][i], non_blocking=True)
+                            h_rs_recv[i].copy_(bs["rs_recv"][i], non_blocking=True)
                 d2h_done[k][d].record(s_out[d])
     for d in D.devs:
         D.streams[d].wait_event(d2h_done[E - 1][d])

@@ -128,6 +128,9 @@ bool env_int(const char* name, long long* out) {
 }  // namespace
 
 struct patComm {
+  // PAT_HOST_PROFILE=1: host nanoseconds spent planning vs submitting calls (printed at destroy)
+  bool host_profile = false;
+  uint64_t hp_calls = 0, hp_plan_ns = 0, hp_submit_ns = 0;
   int n = 0;
   patConfig_t cfg{};
   bool multiprocess = false;
@@ -732,6 +735,10 @@ patResult_t common_init(patComm* comm, int nranks, const patConfig_t* config) {
   comm->cfg = c;
   comm->channels = c.max_channels;
   {
+    long long hp = 0;
+    comm->host_profile = env_int("PAT_HOST_PROFILE", &hp) && hp != 0;
+  }
+  {
     long long v = 0;
     comm->pull_slice = env_int("PAT_PULL_SLICE", &v) && v >= 256 ? (v & ~15LL) : (512 << 10);
     comm->skew = env_int("PAT_SKEW", &v) ? static_cast<int>(std::max(0LL, v)) : 1;
@@ -889,6 +896,7 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   if (!sendbuffs || !recvbuffs) return patInvalidArgument;
   if (patResult_t e = check_async(comm)) return e;
   std::lock_guard<std::mutex> lock(comm->mu);
+  const auto hp_t0 = comm->host_profile ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
   const int n = comm->n;
   const int trees = comm->cfg.trees ? comm->cfg.trees : max_trees(n);
   Compiled* cp = nullptr;
@@ -1082,7 +1090,14 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   P.aligned16 = aligned16;
   P.plans = std::move(plans);
   if (prep) return patSuccess;
-  return submit_prepared(comm, P, nullptr, streams);
+  if (!comm->host_profile) return submit_prepared(comm, P, nullptr, streams);
+  const auto hp_t1 = std::chrono::steady_clock::now();
+  const patResult_t rc = submit_prepared(comm, P, nullptr, streams);
+  const auto hp_t2 = std::chrono::steady_clock::now();
+  ++comm->hp_calls;
+  comm->hp_plan_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(hp_t1 - hp_t0).count();
+  comm->hp_submit_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(hp_t2 - hp_t1).count();
+  return rc;
 }
 
 // Launch a prepared call — or a grouped pair (a = all-gather, b = reduce-scatter sum) as ONE
@@ -1435,6 +1450,10 @@ patResult_t patCommInitRankFinish(patComm_t comm, const void* all_handles) {
 
 patResult_t patCommDestroy(patComm_t comm) {
   if (!comm) return patInvalidArgument;
+  if (comm->host_profile && comm->hp_calls)
+    std::fprintf(stderr, "pat_b200 host profile: %llu calls, plan %.2f us, submit %.2f us per call\n",
+                 (unsigned long long)comm->hp_calls, 1e-3 * comm->hp_plan_ns / comm->hp_calls,
+                 1e-3 * comm->hp_submit_ns / comm->hp_calls);
   for (auto& w : comm->workers) w->shutdown();
   comm->workers.clear();
   {
