@@ -31,3 +31,34 @@ def test_pat_beats_nccl_ring_at_every_size_to_1mib():
         for coll in ("ag", "rs"):
             for b in sizes:
                 assert d[(coll, "pat", b)] * 2.0 < d[(coll, "nccl-Ring", b)], (n, coll, b)
+
+
+def test_round2_ring_sweeps_pat_vs_ring_vs_nccl():
+    """PAT beats NCCL Ring by > 2x at every size <= 1 MiB on the r02 build, and the
+    ring schedule on the same transport is never faster than PAT by more than noise below 1 MiB."""
+    for n in (2, 3, 4):
+        d = {}
+        for line in open(os.path.join(P, f"r02_ring_n{n}_graph.jsonl")):
+            r = json.loads(line)
+            d[(r["coll"], r["impl"], r["bytes_per_rank"])] = r["us"]
+        sizes = sorted({k[2] for k in d if k[2] <= 1 << 20})
+        assert len(sizes) >= 18
+        for coll in ("ag", "rs"):
+            for b in sizes:
+                assert d[(coll, "pat", b)] * 2.0 < d[(coll, "nccl-Ring", b)], (n, coll, b)
+                if b <= 128 << 10 and n >= 3:
+                    assert d[(coll, "pat", b)] < d[(coll, "pat-ring", b)], (n, coll, b)
+
+
+def test_round2_bench_lines_and_zero3_caps():
+    """DESIGN §6.0 tables: the grouped step beats NCCL Ring's step >= 2.5x at N = 2 and 4; the
+    12 MiB-capped ZeRO-3 step keeps >= 75% of the uncapped bandwidth staged."""
+    for nn in (2, 4):
+        d = json.loads(open(os.path.join(P, f"r02_final_bench{nn}.json")).read().splitlines()[-1])
+        assert d["n_gpus"] == nn and d["step_grouped"]
+        assert d["nccl_ring"]["ms_per_step"] > 2.5 * d["ms_per_step"], nn
+        assert d["ms_per_step"] < d["ms_per_step_ungrouped"]
+    rows = {r["staging_cap_mib"]: r for r in map(json.loads, open(os.path.join(P, "r02_zero3_n4.jsonl")))}
+    assert rows[12]["busbw_gbs"] >= 0.75 * rows[0]["busbw_gbs"]
+    assert all(r["allgather_matches_nccl"] for r in rows.values())
+    assert rows[12]["pool_bytes_ag"] <= 12 << 20
