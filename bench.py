@@ -450,7 +450,7 @@ def run_pat(args, rank, world, local):
 
     dbg("e2e")
     # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region.
-    # Double-buffered per device: step k's inputs go up on a copy stream into device set k % 2
+    # Triple-buffered per device: step k's inputs go up on a copy stream into device set k % 3
     # while step k-1 runs, and step k-1's results come down on another copy stream (PCIe is full
     # duplex); every step still copies all of its inputs in and its results out inside the
     # timed region.
@@ -466,6 +466,9 @@ def run_pat(args, rank, world, local):
         h_ag_send[i].copy_(sets[0]["ag_send"][i].cpu())
         h_rs_send[i].copy_(sets[0]["rs_send"][i].cpu())
     E = max(3, min(K, 20))
+    # triple-buffered device sets: step k+1's upload, step k's compute and step k-1's download all
+    # in flight (double buffering left PCIe idle ~17% of a step: tools/e2e_probe.py, 2.04 vs 1.71 ms)
+    NB = 3
     one_dev = len(D.devs) == 1
     if one_dev:  # device side likewise: the ranks' buffers are slices of one allocation per kind
         def cset():
@@ -474,9 +477,10 @@ def run_pat(args, rank, world, local):
             d_ = {k: list(v.view(L, -1)) for k, v in blk.items()}
             d_["_blk"] = blk
             return d_
-        dsets = [cset() for _ in range(2)]
+        dsets = [cset() for _ in range(NB)]
     else:
-        dsets = [sets[j % len(sets)] for j in range(2)]
+        NB = min(NB, len(sets))  # distinct buffer sets only
+        dsets = [sets[j] for j in range(NB)]
     s_in = {d: torch.cuda.Stream(d) for d in D.devs}
     s_out = {d: torch.cuda.Stream(d) for d in D.devs}
     ev = lambda: {d: torch.cuda.Event() for d in D.devs}  # noqa: E731
@@ -488,11 +492,11 @@ def run_pat(args, rank, world, local):
         s_in[d].wait_stream(D.streams[d])
         s_out[d].wait_stream(D.streams[d])
     for k in range(E):
-        bs = dsets[k % 2]
+        bs = dsets[k % NB]
         for d in D.devs:
             with torch.cuda.device(d), torch.cuda.stream(s_in[d]):
-                if k >= 2:
-                    s_in[d].wait_event(comp_done[k - 2][d])  # set k % 2's inputs are free
+                if k >= NB:
+                    s_in[d].wait_event(comp_done[k - NB][d])  # set k % NB's inputs are free
                 if one_dev:
                     bs["_blk"]["ag_send"].copy_(hb["ag_send"], non_blocking=True)
                     bs["_blk"]["rs_send"].copy_(hb["rs_send"], non_blocking=True)
@@ -503,8 +507,8 @@ def run_pat(args, rank, world, local):
                             bs["rs_send"][i].copy_(h_rs_send[i], non_blocking=True)
                 h2d_done[k][d].record(s_in[d])
             D.streams[d].wait_event(h2d_done[k][d])
-            if k >= 2:
-                D.streams[d].wait_event(d2h_done[k - 2][d])  # set k % 2's outputs were read back
+            if k >= NB:
+                D.streams[d].wait_event(d2h_done[k - NB][d])  # set k % NB's outputs were read back
         call(comm, ("ag", "rs"), bs)
         for d in D.devs:
             comp_done[k][d].record(D.streams[d])
@@ -787,7 +791,7 @@ def run_pat(args, rank, world, local):
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host; "
-                            "double-buffered: step k+1 uploads while step k downloads (PCIe full duplex)"},
+                            "triple-buffered: step k+1 uploads while step k-1 downloads (PCIe full duplex)"},
             "gpu_launches": launches_per_gpu * n_gpus,
             "gpu_launches_per_gpu": launches_per_gpu,
             "roofline": roof,
