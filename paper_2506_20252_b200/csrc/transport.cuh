@@ -370,6 +370,17 @@ __device__ __forceinline__ void wait_credits(const KPlan& p, const Step& s, Wait
   const uint64_t* mine = chan_flags(p, s.R, s.c);
   for (int k = 0; k < p.npeers; ++k) wait_flag(mine + 8 + (s.R + p.peers[k]) % p.n, s.g - p.depth + 1, w);
 }
+// The same, one peer per thread (threads [0, npeers) of the caller's group, which then barriers):
+// the npeers acquire loads overlap instead of following one another (a small call waits on
+// ceil(log2 n) distinct peers: 3 at n = 8). PAT_SERIAL_CREDITS builds keep the one-thread form.
+__device__ __forceinline__ void wait_credits_par(const KPlan& p, const Step& s, Waiter& w, int tid) {
+#ifdef PAT_SERIAL_CREDITS
+  if (tid == 0) wait_credits(p, s, w);
+#else
+  if (tid >= p.npeers || s.g < static_cast<uint64_t>(p.depth)) return;
+  wait_flag(chan_flags(p, s.R, s.c) + 8 + (s.R + p.peers[tid]) % p.n, s.g - p.depth + 1, w);
+#endif
+}
 
 // ------------------------------------------------------------------------- live occupancy
 // (PAT_STATS) Counted by the device as the step runs: the receiver role, once round t's flag is
@@ -488,7 +499,7 @@ __device__ void send_role(const KPlan& p, uint64_t base, int R, int lr, int c, W
     uint32_t& wm = waited[i % kMaxRounds];
     if (t == 0) {  // first push of step i: the peers' buffers (g % depth) must be free
       wm = 0;
-      if (tid == 0 && !p.direct) wait_credits(p, s, w);
+      if (!p.direct) wait_credits_par(p, s, w, tid);
       tr.rec(kEvCredit, s.g, 0);
       named_bar(1, nthr);
       // leaves first: every round's dependency-free chunks go out now, so the link is busy while
@@ -1093,7 +1104,7 @@ __device__ __forceinline__ void pat_body(const KPlan& p, int vb) {
     // times; profiles/r01f_ll32_{skew,noskew}_n*.jsonl.)
     for (int i = 0; i < p.iters; ++i) {
       const Step s = make_step(p, base, i, R, lr, c);
-      if (threadIdx.x == 0) wait_credits(p, s, w);
+      wait_credits_par(p, s, w, threadIdx.x);
       __syncthreads();
       if (p.proto == kProtoLL) {
         step_ll<DT, OP, KIND>(p, s, w);
