@@ -125,6 +125,8 @@ struct Waiter {
   int* err;
   bool aborted;
   bool gpu;  // flag scope
+  const uint64_t* cred0 = nullptr;  // credits read at kernel entry, per peer (valid for step `base`)
+  uint64_t base = 0;
 };
 
 // ------------------------------------------------------------------------- device trace
@@ -378,7 +380,9 @@ __device__ __forceinline__ void wait_credits_par(const KPlan& p, const Step& s, 
   if (tid == 0) wait_credits(p, s, w);
 #else
   if (tid >= p.npeers || s.g < static_cast<uint64_t>(p.depth)) return;
-  wait_flag(chan_flags(p, s.R, s.c) + 8 + (s.R + p.peers[tid]) % p.n, s.g - p.depth + 1, w);
+  const uint64_t want = s.g - p.depth + 1;
+  if (w.cred0 && s.g == w.base && w.cred0[tid] >= want) return;  // the entry read already saw it
+  wait_flag(chan_flags(p, s.R, s.c) + 8 + (s.R + p.peers[tid]) % p.n, want, w);
 #endif
 }
 
@@ -1057,13 +1061,23 @@ __device__ __forceinline__ void pat_body(const KPlan& p, int vb) {
   // flushed. No early launch_dependents: a successor made resident early would take registers
   // from this grid's later CTAs (measured: the fused reduce-scatter lost half its occupancy).
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the step counter and the first step's credits are read at the same time (threads 0 and
+  // 1..npeers): the credit loads' addresses do not depend on the counter, only the comparison does
+  __shared__ uint64_t s_cred[kMaxRounds];
   if (threadIdx.x == 0) {
     s_base = p.iter_state[lr][c];
     s_sent = 0;
+  } else if (static_cast<int>(threadIdx.x) <= p.npeers) {
+    const int k = threadIdx.x - 1;
+    s_cred[k] = ld_acquire(chan_flags(p, R, c) + 8 + (R + p.peers[k]) % p.n, p.gpu_scope != 0);
   }
   __syncthreads();
   const uint64_t base = s_base;
   Waiter w{p.timeout_ns, p.err, false, p.gpu_scope != 0};
+#ifndef PAT_NO_CRED0  // A/B builds: the first step's credits waited for as every later step's
+  w.cred0 = s_cred;
+#endif
+  w.base = base;
 
   // done(step) for the previous call's last step on this channel: a polling-protocol call defers
   // it from its exit (below), and EVERY protocol publishes it here — a bulk call that follows a
