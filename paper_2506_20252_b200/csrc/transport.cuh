@@ -623,13 +623,6 @@ __device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
   const int B = blockDim.x;
   PAT_BOUND(16 * nlines <= p.slot_stride);
 
-  if constexpr (KIND == kAG) {
-    if (out + s.R * Cb != snd)
-      for (int64_t q = threadIdx.x; q < nlines; q += B) {
-        const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
-        store_word(out + s.R * Cb + s.off + 8 * q, load_word(snd + s.off + 8 * q, valid, p), valid, p);
-      }
-  }
   for (int pass = 0; pass < passes; ++pass)
   for (int t = 0; t < p.nrounds; ++t) {
     const KRound& r = p.rounds[t];
@@ -665,6 +658,13 @@ __device__ void step_ll(const KPlan& p, const Step& s, Waiter& w) {
     }
   }
   if constexpr (KIND == kAG) {
+    // own chunk placement (simulate.cpp:160-165) after every send: local work that would
+    // otherwise delay the first line onto the link
+    if (out + s.R * Cb != snd)
+      for (int64_t q = threadIdx.x; q < nlines; q += B) {
+        const int valid = static_cast<int>(min(int64_t{8}, s.len - 8 * q));
+        store_word(out + s.R * Cb + s.off + 8 * q, load_word(snd + s.off + 8 * q, valid, p), valid, p);
+      }
     for (int j = 0; j < p.nslots; ++j) {
       const int origin = (s.R - p.slot_offset[j] + n) % n;
       const char* slot = slot_ptr(p, s.R, s.c, s.buf, j);
