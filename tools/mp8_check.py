@@ -56,6 +56,31 @@ def main():
                     print(f"rank {rank} RS mismatch proto={proto} dt={dt} elems={elems}", flush=True)
         comm.raise_async_error()
         comm.destroy()
+    # grouped all-gather + reduce-scatter (the bench's step), both orders, LL32 and SIMPLE sizes
+    from paper_2506_20252_b200 import group
+    comm = PatComm.from_process_group(device=dev.index)
+    for elems in (1 << 18, 1 << 21):
+        for rs_first in (False, True):
+            p = O.random_payload(O.FLOAT32, n, elems, elems + 3 + rs_first)
+            q = O.random_payload(O.FLOAT32, n * n, elems, elems + 5 + rs_first)
+            s = torch.from_numpy(p[rank * elems:(rank + 1) * elems].copy()).to(dev)
+            r = torch.zeros(n * elems, device=dev)
+            s2 = torch.from_numpy(q[rank * n * elems:(rank + 1) * n * elems].copy()).to(dev)
+            r2 = torch.zeros(elems, device=dev)
+            with group():
+                if rs_first:
+                    comm.reduce_scatter([s2], [r2], elems, O.FLOAT32, O.SUM)
+                    comm.all_gather([s], [r], elems, O.FLOAT32)
+                else:
+                    comm.all_gather([s], [r], elems, O.FLOAT32)
+                    comm.reduce_scatter([s2], [r2], elems, O.FLOAT32, O.SUM)
+            torch.cuda.synchronize(dev)
+            want, _ = O.run_allgather(O.pat_allgather(n, O.max_trees(n)), O.FLOAT32, p, elems)
+            fails += r.cpu().numpy().tobytes() != want[rank].tobytes()
+            want, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, O.max_trees(n)), O.FLOAT32, O.SUM, q, elems)
+            fails += r2.cpu().numpy().tobytes() != want[rank].tobytes()
+    comm.raise_async_error()
+    comm.destroy()
     # the bench step, informative
     comm = PatComm.from_process_group(device=dev.index)
     e = 1 << 18
