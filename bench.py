@@ -422,7 +422,8 @@ def run_pat(args, rank, world, local):
             for k in range(K):
                 call(comm, kinds, sets[k % S])
         return run
-    eager_bb = max_over_ranks(torch, dist, dev0, [D.time_ms(eager_k(("ag",))), D.time_ms(eager_k(("rs",)))])
+    eager_bb = max_over_ranks(torch, dist, dev0, [D.time_ms(eager_k(("ag",))), D.time_ms(eager_k(("rs",))),
+                                                   D.time_ms(eager_k(("ag", "rs")))])
     # ---- isolated eager calls (events per call on an idle stream: host submission included)
     KE = min(K, 100)
     eev = [D.events() for _ in range(3 * KE)]
@@ -446,7 +447,8 @@ def run_pat(args, rank, world, local):
                     "timing": "one eager call at a time on an idle GPU, events around each call: includes the "
                               "host's submission time (Python binding + C ABI)"}
     eager_us = {"all_gather": 1e3 * eager_bb[0] / K, "reduce_scatter": 1e3 * eager_bb[1] / K,
-                "timing": "K back-to-back eager calls through the Python binding, events around the K"}
+                "step": 1e3 * eager_bb[2] / K,
+                "timing": "K back-to-back eager calls (steps: grouped) through the Python binding, events around the K"}
 
     dbg("e2e")
     # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region.
@@ -593,9 +595,13 @@ def run_pat(args, rank, world, local):
                 "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()), "timing": timing,
                 "pat_speedup_step": nt[0] / step_ms,
                 "pat_speedup_step_ungrouped": nt[0] / step_ung_ms,
-                "note": "NCCL's all-gather and reduce-scatter run one after the other (torch.distributed cannot "
-                        "coalesce two different collectives); compare with pat_speedup_step_ungrouped for the "
-                        "same call sequence, pat_speedup_step for PAT's grouped launch"}
+                "pat_eager_ms_per_step": eager_bb[2] / K,
+                "pat_speedup_step_eager": nt[0] / eager_bb[2],
+                "note": "NCCL is timed eagerly (K back-to-back calls); pat_speedup_step_eager compares PAT timed "
+                        "the same way (eager grouped steps). NCCL's all-gather and reduce-scatter run one after "
+                        "the other (torch.distributed cannot coalesce two different collectives); "
+                        "pat_speedup_step_ungrouped compares the same call sequence from CUDA graphs, "
+                        "pat_speedup_step PAT's grouped launch"}
 
     # ---- N = 1 extras: the same n = 8 workload through the PAT transport kernel (per-round
     # messages through the inbox pools with flags), and the repo at the reference arm's dtypes
