@@ -32,7 +32,7 @@ cudaError_t max_blocks_per_sm(int kind, int dtype, int op, int threads, int* out
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel_for(kind, dtype, op), threads, 0);
 }
 
-bool pdl_enabled();  // local.cu
+bool pdl_for(cudaStream_t stream);  // local.cu
 
 // Pool state for a communicator whose step counters start at `start` instead of 0
 // (PAT_ITER_START, tests of the 32-bit flag wrap): every done/credit flag = start, and the LL /
@@ -106,7 +106,7 @@ cudaError_t launch_group(const KPlan2& plans, int dtype, int threads, cudaStream
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cfg.numAttrs = pdl_for(stream) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, *kGroupTable[dtype], plans);
 }
 
@@ -132,7 +132,7 @@ cudaError_t launch(const KPlan& plan, int dtype, int op, int threads, cudaStream
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cfg.numAttrs = pdl_for(stream) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kernel_for(plan.kind, dtype, op), plan);
 }
 

@@ -448,6 +448,25 @@ const char* local_tree_string(int n) {
 }
 
 // PAT_PDL=0 launches without programmatic stream serialization (A/B experiments).
+// Transport launches: programmatic dependent launch pays off inside CUDA graphs (7.05 vs 7.34 us
+// per n = 2 call) but costs eager stream launches 0.4-1 us (10.7 vs 9.7-10.3 us,
+// tools/eager_probe_mp.py, profiles/r02_eager_probe_pdl.txt), so it is requested only while the
+// stream is being captured. The fused executor's kernels keep it either way (eager 12.9 vs 14.8 us
+// per call without it: their launches hide behind the previous kernel's drain).
+bool pdl_for(cudaStream_t stream) {
+  static const int mode = [] {  // PAT_PDL: 0 never, 1 always, unset: graphs only
+    const char* e = std::getenv("PAT_PDL");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (mode >= 0) return mode != 0;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs == cudaStreamCaptureStatusActive;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PAT_PDL");

@@ -57,6 +57,22 @@ def main():
         e1.record(st)
         torch.cuda.synchronize(dev)
         out["device_us_per_call_queued"] = 1e3 * e0.elapsed_time(e1) / K
+        # the same K calls from a CUDA graph, same buffers and streams
+        g = torch.cuda.CUDAGraph()
+        g.capture_begin(capture_error_mode="relaxed")
+        for _ in range(K):
+            F.all_gather(h, sp, rp, e, FLOAT32, sh)
+        g.capture_end()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        comm.barrier([st])
+        torch.cuda._sleep(int(os.environ.get("PROBE_SPIN", "20000000")))
+        e0.record(st)
+        g.replay()
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        out["graph_us_per_call"] = 1e3 * e0.elapsed_time(e1) / K
     comm.raise_async_error()
     print(json.dumps(out), flush=True)
     dist.barrier()
