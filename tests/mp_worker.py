@@ -83,7 +83,36 @@ def windows_section(rank, n, dev):
             if r.cpu().numpy().tobytes() != want[rank].tobytes():
                 fails += 1
                 print(f"rank {rank} windowed RS mismatch proto={proto} dt={dt}", flush=True)
+        # a grouped pair on windowed buffers (zero-copy all-gather + reduce-scatter in one launch)
+        from paper_2506_20252_b200 import group
+        p = O.random_payload(O.FLOAT32, n, elems, 123 + proto)
+        q = O.random_payload(O.FLOAT32, n * n, elems, 321 + proto)
+        half = n * elems * 4 + pad  # AG in the first half of each window's use, RS after it
+        ws = torch.zeros(2 * half + pad, dtype=torch.uint8, device=dev)
+        wr = torch.zeros(2 * half + pad, dtype=torch.uint8, device=dev)
+        comm.register(ws)
+        comm.register(wr)
+        ag_s = ws[pad:pad + elems * 4]
+        ag_s.copy_(torch.from_numpy(p[rank * elems:(rank + 1) * elems].copy().view(np.uint8)))
+        ag_r = wr[pad:pad + n * elems * 4]
+        rs_s = ws[half + pad:half + pad + n * elems * 4]
+        rs_s.copy_(torch.from_numpy(q[rank * n * elems:(rank + 1) * n * elems].copy().view(np.uint8)))
+        rs_r = wr[half + pad:half + pad + elems * 4]
+        with group():
+            comm.all_gather([ag_s], [ag_r], elems, O.FLOAT32)
+            comm.reduce_scatter([rs_s], [rs_r], elems, O.FLOAT32, O.SUM)
+        torch.cuda.synchronize(dev)
+        want, _ = O.run_allgather(O.pat_allgather(n, O.max_trees(n)), O.FLOAT32, p, elems)
+        if ag_r.cpu().numpy().tobytes() != want[rank].tobytes():
+            fails += 1
+            print(f"rank {rank} windowed grouped AG mismatch proto={proto}", flush=True)
+        want, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, O.max_trees(n)), O.FLOAT32, O.SUM, q, elems)
+        if rs_r.cpu().numpy().tobytes() != want[rank].tobytes():
+            fails += 1
+            print(f"rank {rank} windowed grouped RS mismatch proto={proto}", flush=True)
         comm.raise_async_error()
+        comm.deregister(wr)
+        comm.deregister(ws)
         comm.deregister(win_r)
         comm.deregister(win_s)
         comm.destroy()
