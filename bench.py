@@ -703,10 +703,18 @@ def run_pat(args, rank, world, local):
     else:
         # per GPU: every rank on it receives (n-1)*C over NVLink per launch (ranks sharing a GPU
         # share its links, so the GPU's ingress is ranks_on_gpu * (n-1) * C minus what stays local)
-        algo_bytes = (n - 1) * C
+        coll_bytes = (n - 1) * C
         peak = NVLINK_PEER_COPY_GBS
-        roof = {"bound": "nvlink", "kernel": f"pat_kernel ({dom})", "unit": "GB/s",
-                "algorithmic_bytes_per_launch": algo_bytes,
+        per_coll = {c_: {"kernel": "pat_kernel", "us": 1e3 * t_ / K,
+                         "frac": coll_bytes / (t_ / K * 1e-3) / 1e9 / peak}
+                    for c_, t_ in (("all_gather", ag_ms), ("reduce_scatter", rs_ms))}
+        if not args.no_group:  # the timed step is one grouped launch carrying both collectives
+            algo_bytes, dom_us = 2 * coll_bytes, 1e3 * step_ms / K
+            kern = "pat_group_kernel (the grouped step: all-gather + reduce-scatter in one launch)"
+        else:
+            algo_bytes, kern = coll_bytes, f"pat_kernel ({dom})"
+        roof = {"bound": "nvlink", "kernel": kern, "unit": "GB/s",
+                "algorithmic_bytes_per_launch": algo_bytes, "per_collective": per_coll,
                 "peak_source": "measured NVLink peer copy 770 GB/s per direction (B200_PROFILING.md)"}
         achieved = algo_bytes / (dom_us * 1e-6) / 1e9
         roof["frac_of_nominal_900"] = achieved / NVLINK_NOMINAL_GBS
@@ -722,7 +730,7 @@ def run_pat(args, rank, world, local):
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath))
-            key = (f"local_n{n}_group" if mode == "local" and not args.no_group else
+            key = (f"{'local' if mode == 'local' else 'nvlink'}_n{n}_group" if not args.no_group else
                    f"{'local' if mode == 'local' else 'nvlink'}_n{n}_{dom}")
             if key in tr:
                 roof["traffic"] = tr[key]["dram_bytes_per_launch"]

@@ -6,7 +6,7 @@ device's launches works: the other devices' kernels were launched (unprofiled, a
 just before and run alongside. Kernel replay would re-run the profiled kernel without its
 peers, so the whole application is replayed instead:
 
-  PAT_LAUNCH_THREADS=0 ncu --devices 1 --replay-mode application --clock-control none -k regex:pat_kernel \\
+  PAT_LAUNCH_THREADS=0 ncu --devices 1 --replay-mode application --clock-control none -k regex:pat_ \\
       --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \\
       --csv --log-file gpurun_out/ncu_nvlink.csv python tools/ncu_nvlink.py --gpus 2
 
@@ -38,7 +38,19 @@ def main():
     for case in args.cases.split(","):
         coll, nbytes = case.split(":")
         elems = int(nbytes) // 4
-        if coll == "ag":
+        if coll == "grp":  # a grouped all-gather + reduce-scatter (one pat_group_kernel launch)
+            from paper_2506_20252_b200 import group
+            s = [torch.ones(elems, device=f"cuda:{d}") for d in range(n)]
+            r = [torch.empty(n * elems, device=f"cuda:{d}") for d in range(n)]
+            s2 = [torch.ones(n * elems, device=f"cuda:{d}") for d in range(n)]
+            r2 = [torch.empty(elems, device=f"cuda:{d}") for d in range(n)]
+
+            def fn():
+                with group():
+                    comm.all_gather(s, r, elems, FLOAT32)
+                    comm.reduce_scatter(s2, r2, elems, FLOAT32, SUM)
+            kind = 0
+        elif coll == "ag":
             s = [torch.ones(elems, device=f"cuda:{d}") for d in range(n)]
             r = [torch.empty(n * elems, device=f"cuda:{d}") for d in range(n)]
             fn = lambda: comm.all_gather(s, r, elems, FLOAT32)  # noqa: E731
