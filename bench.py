@@ -756,6 +756,9 @@ def run_pat(args, rank, world, local):
                      "wire_us_at_704gbs": wire_us, "floor_us": zero_us + wire_us, "achieved_us": 1e3 * ag_ms / K,
                      "frac": (zero_us + wire_us) / (1e3 * ag_ms / K),
                      "source": "profiles/r01f_costmodel_fit.json (LL a, b), profiles/r01_bidir_probe_g4.txt"}
+        if not args.no_group:  # the grouped step: one fixed cost, both collectives' bytes on the wire
+            lat_floor["grouped_step"] = {"floor_us": zero_us + 2 * wire_us, "achieved_us": 1e3 * step_ms / K,
+                                         "frac": (zero_us + 2 * wire_us) / (1e3 * step_ms / K)}
 
     clk = clocks.summary()
     if dist is not None:
