@@ -470,7 +470,7 @@ def run_pat(args, rank, world, local):
     E = max(3, min(K, 20))
     # triple-buffered device sets: step k+1's upload, step k's compute and step k-1's download all
     # in flight (double buffering left PCIe idle ~17% of a step: tools/e2e_probe.py, 2.04 vs 1.71 ms)
-    NB = 3
+    NB = int(os.environ.get("BENCH_E2E_BUFFERS", "3"))
     one_dev = len(D.devs) == 1
     if one_dev:  # device side likewise: the ranks' buffers are slices of one allocation per kind
         def cset():

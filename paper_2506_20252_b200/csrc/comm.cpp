@@ -55,14 +55,14 @@ namespace {
 
 // per pool: channel flags (8 KiB), then the barrier words (patCommBarrier), padded so the
 // inbox regions stay 4 KiB aligned
-constexpr size_t kChanFlagBytes = sizeof(uint64_t) * kMaxChannels * kFlagWords;  // 8 KiB
+constexpr size_t kChanFlagBytes = sizeof(uint64_t) * kMaxChannels * kFlagWords;  // 40 KiB
 constexpr size_t kBarrierOff = kChanFlagBytes;
 constexpr size_t kFlagBytes = kChanFlagBytes + 4096;
 constexpr uint32_t kMagic = 0x50415442;                                       // "PATB"
 constexpr size_t kDefaultPoolBytes = 512ull << 20;  // inbox pool budget per rank (all channels)
 constexpr size_t kMaxSlice = 256 << 10;
 constexpr size_t kCapMinSlice = 32 << 10;  // smallest bulk slice a staging cap shrinks to before channels
-constexpr int kDefaultChannels = 128;            // clamped to co-residency at launch
+constexpr int kDefaultChannels = 148;            // one CTA per SM of a B200; clamped to co-residency at launch
 // LL32 vs bulk is chosen by the calibrated cost model below (choose_slicing).
 constexpr int64_t kPullMaxRS = 128 << 20;  // PULL reduce-scatter below this chunk size
 constexpr int64_t kPullMinRS = 1 << 20;    // ... and above this one (LL wins below anyway)

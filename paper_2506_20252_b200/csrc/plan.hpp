@@ -14,7 +14,7 @@ constexpr int kMaxChunks = 8;   // chunk offsets per round
 constexpr int kMaxSlots = 8;    // inbox slots per pipeline step (= n-1 arrivals)
 constexpr int kMaxArr = 8;      // arrivals folded into one forwarded offset
 constexpr int kMaxLocal = 8;    // ranks driven by one kernel (local mode)
-constexpr int kMaxChannels = 128;
+constexpr int kMaxChannels = 160;  // >= the 148 SMs of a B200 (channels are clamped to co-residency)
 constexpr int kMaxThreads = 512;  // per CTA: 128 registers per thread for the unrolled SIMPLE loops
 constexpr int kFlagWords = 32;  // per channel: data flag per round [0,8), done-from per rank [8,16),
                                 // ready-from per rank [16,24) (direct mode entry handshake),
