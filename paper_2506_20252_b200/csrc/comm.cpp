@@ -1100,6 +1100,25 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   return rc;
 }
 
+// Threads per CTA of a transport launch. The polling protocols give every thread whole lines, so
+// a call whose step has few lines per channel runs smaller CTAs: their barriers are cheaper
+// (tools/gpurun/r02bh.sh: 256- and 384-thread CTAs were 2-7% faster on calls <= 32 KiB).
+// SIMPLE / PULL keep the configured size (warp-specialised roles, per-thread vector pipelines).
+// PAT_POLL_THREADS=0 turns the sizing off.
+int launch_threads(const patComm* comm, const KPlan& p) {
+  static const bool on = [] {
+    long long v = 1;
+    return !env_int("PAT_POLL_THREADS", &v) || v != 0;
+  }();
+  const int cfg = comm->cfg.threads;
+  if (!on || (p.proto != kProtoLL && p.proto != kProtoLL32)) return cfg;
+  const int64_t lines = p.proto == kProtoLL ? (p.slice_bytes + 7) / 8
+                                            : (p.slice_bytes + ll32_group(p.kind, p.esize) - 1) /
+                                                  ll32_group(p.kind, p.esize) * 32;
+  const int64_t want = std::max<int64_t>(64, (lines + 31) / 32 * 32);
+  return static_cast<int>(std::min<int64_t>(cfg, want));
+}
+
 // Launch a prepared call — or a grouped pair (a = all-gather, b = reduce-scatter sum) as ONE
 // launch per device — on the streams of the local ranks.
 patResult_t submit_prepared(patComm* comm, const Prepared& a, const Prepared* b, const patStream_t* streams) {
@@ -1109,7 +1128,8 @@ patResult_t submit_prepared(patComm* comm, const Prepared& a, const Prepared* b,
     const DevGroup& g = comm->groups[gi];
     const KPlan& p = a.plans[gi];
     CUDA_TRY(cudaSetDevice(g.device));
-    const int threads = comm->cfg.threads;
+    const int threads = b ? std::max(launch_threads(comm, p), launch_threads(comm, b->plans[gi]))
+                          : launch_threads(comm, p);
     cudaStream_t s0 = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr;
     for (size_t i = 1; i < g.lidx.size(); ++i) {  // join the other local ranks' streams
       cudaStream_t si = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[i]]) : nullptr;
