@@ -62,6 +62,10 @@
   } while (0)
 #endif
 
+#ifndef PAT_EXTRA_BARRIERS  // A/B builds: 1 restores the barriers the r02 prologue / epilogue dropped
+#define PAT_EXTRA_BARRIERS 0
+#endif
+
 namespace pat {
 
 // ------------------------------------------------------------------------- memory primitives
@@ -1086,7 +1090,11 @@ __device__ __forceinline__ void pat_body(const KPlan& p, int vb) {
   // Every step before `base` finished: the previous kernel completed before this one started.
   if (threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
     st_relaxed(chan_flags(p, threadIdx.x, c) + 8 + R, base, w.gpu);
-  __syncthreads();  // orders it before any later done store of another thread (release cumulativity)
+  // SIMPLE / PULL publish later done values from other threads: a barrier orders this store before
+  // them (release cumulativity). The polling protocols' later done stores come from these same
+  // threads (program order), and their first barrier follows the credit wait.
+  const bool polling = p.proto == kProtoLL || p.proto == kProtoLL32;
+  if (!polling || PAT_EXTRA_BARRIERS) __syncthreads();
 
   if (p.direct && KIND == kAG) {
     // entry handshake: a peer may be written directly only once it entered this call
@@ -1162,7 +1170,9 @@ __device__ __forceinline__ void pat_body(const KPlan& p, int vb) {
       tr.rec(kEvEnd, base + p.iters, 0);
     }
   }
-  __syncthreads();
+  // thread 0 advances the step counter; the next call reads it only after this grid completed, so
+  // no barrier is needed before it
+  if (PAT_EXTRA_BARRIERS) __syncthreads();
   if (threadIdx.x == 0) p.iter_state[lr][c] = base + p.iters;
 }
 
