@@ -565,6 +565,7 @@ constexpr CostRow kCostLL32{3.07, 2.42, 608.0, 32.0 / 28.0};  // one fixed cost 
 // (profiles/r01f_ll32_noskew_n*.jsonl, r01f_forced_n*_p2.jsonl, r01f_loopmid_n*.jsonl); the
 // linear model alone would keep it far beyond, where SIMPLE's pipelined pushes reach 670 GB/s.
 constexpr int64_t kLL32MaxPayload = 48ll << 20;
+constexpr int64_t kLLMaxChunk = 256 << 10;  // auto mode sends chunks from here up with LL32 or bulk, never LL
 constexpr double kCappedIterUs = 10.0;  // per extra bulk iteration under a staging cap (fence + flag)
 constexpr size_t kCappedSmallSlot = 64 << 10;  // bulk slots below this make the fence dominate
 constexpr CostRow kCostBulk{5.99, 6.11, 560.0, 1.0};
@@ -639,7 +640,11 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
       proto = chunk_bytes <= static_cast<int64_t>(comm->cfg.ll_threshold) ? kProtoLL32 : bulk;
     } else {  // the cost model picks the fastest of LL, LL32 and the bulk protocol
       double best = 0;
+      bool have = false;
       for (const int cand : std::array<int, 3>{kProtoLL, kProtoLL32, bulk}) {
+        // from 256 KiB chunks LL32 beats LL at n = 2, 3, 4 by 5-20% (r02 forced sweeps,
+        // profiles/r02_forced_n*_p{1,5}.jsonl), where the fitted model still favoured LL
+        if (cand == kProtoLL && chunk_bytes >= kLLMaxChunk) continue;
         // uncapped, SIMPLE's pipelined pushes beat LL32's polled lines beyond 48 MiB of payload;
         // under a cap that shrank the bulk slots every size is a candidate for LL32
         const bool capped = comm->slot_bytes < kMaxSlice;
@@ -655,9 +660,10 @@ Slicing choose_slicing(const patComm* comm, int kind, int64_t chunk_bytes, int m
                    (comm->n - 1) * static_cast<double>(chunk_bytes) / (kCostBulk.gbs * 1e3) +
                kCappedIterUs * std::max(sh.iters - 1, 0);
         }
-        if (cand == kProtoLL || t < best) {
+        if (!have || t < best) {
           best = t;
           proto = cand;
+          have = true;
         }
       }
     }

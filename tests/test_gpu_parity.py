@@ -553,9 +553,9 @@ def test_protocol_switches_share_no_inbox_state(spread, depth):
 def test_cost_model_protocol_choice():
     """Without an explicit ll_threshold the calibrated alpha-beta model picks LL32 or the bulk
     protocol (comm.cpp: predict_us); the crossovers it implies match the forced sweeps
-    (profiles/r01*_forced_n*_p*.jsonl)."""
-    cases = [(2, 64 << 10, _lib.PROTO_LL), (2, 2 << 20, _lib.PROTO_LL32), (2, 16 << 20, _lib.PROTO_LL32),
-             (2, 64 << 20, _lib.PROTO_SIMPLE)]
+    (profiles/r01*_forced_n*_p*.jsonl, r02_forced_n*_p*.jsonl: no LL from 256 KiB)."""
+    cases = [(2, 64 << 10, _lib.PROTO_LL), (2, 128 << 10, _lib.PROTO_LL), (2, 256 << 10, _lib.PROTO_LL32),
+             (2, 2 << 20, _lib.PROTO_LL32), (2, 16 << 20, _lib.PROTO_LL32), (2, 64 << 20, _lib.PROTO_SIMPLE)]
     if NGPU >= 4:
         cases += [(4, 1 << 20, _lib.PROTO_LL32), (4, 16 << 20, _lib.PROTO_LL32), (4, 32 << 20, _lib.PROTO_SIMPLE)]
     for n, nbytes, want in cases:

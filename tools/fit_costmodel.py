@@ -24,7 +24,7 @@ import numpy as np
 
 WIRE = {1: 2.0, 2: 1.0, 5: 32.0 / 28.0}  # protocol -> wire bytes per payload byte
 NAME = {1: "LL", 2: "SIMPLE", 5: "LL32"}
-STEP_BYTES = {"LL": 128 * 16 * 1024, "LL32": 128 * 28 * 1024}  # one polling step: 128 channels x slot payload
+STEP_BYTES = {"LL": 32 * 16 * 1024, "LL32": 148 * 28 * 1024}  # one polling step: channels x slot payload (LL: 32-channel region)
 
 
 def rounds(n):
