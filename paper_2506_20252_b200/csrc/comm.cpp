@@ -1300,8 +1300,15 @@ patResult_t run_group_pair(PendingCall& x, PendingCall& y) {
   if (patResult_t e = run_collective(comm, kRS, rs.send.data(), rs.recv.data(), rs.count, rs.dtype, rs.op, st,
                                      nullptr, 2, &pb))
     return e;
-  if (pa.fused != pb.fused || (!pa.fused && (pa.plans.empty() || pb.plans.empty()))) {
-    // not the same executor: one after the other
+  // zero-copy bulk calls (direct all-gather, PULL reduce-scatter) on half the channels each measured
+  // slower than one after the other (ZeRO-3 shape with windows, n = 4: 0.787 vs 0.646 ms per step,
+  // profiles/r02_zero3_grouped_n4.jsonl); staged and polling pairs gain (0.629 vs 0.670 ms)
+  auto zero_copy_bulk = [](const Prepared& q) {
+    return !q.fused && !q.plans.empty() && (q.plans[0].proto == kProtoPull || q.plans[0].direct);
+  };
+  if (pa.fused != pb.fused || (!pa.fused && (pa.plans.empty() || pb.plans.empty())) || zero_copy_bulk(pa) ||
+      zero_copy_bulk(pb)) {
+    // not the same executor, or a pair that runs better apart: one after the other
     if (patResult_t e = run_pending(x)) return e;
     return run_pending(y);
   }

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--windows", action="store_true", help="register the four tensors as symmetric windows")
     ap.add_argument("--nccl", action="store_true", help="also time NCCL (NCCL_ALGO as set) on the same tensors")
+    ap.add_argument("--group", action="store_true", help="issue each step's two calls as one group (one launch)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -46,9 +47,16 @@ def main():
                 comm.register(t)
         plan_ag, plan_rs = comm.plan(0, shard, BFLOAT16), comm.plan(1, shard, BFLOAT16)
 
+        from paper_2506_20252_b200 import group
+
         def step():
-            comm.all_gather_into_tensor(gathered, params)
-            comm.reduce_scatter_tensor(gshard, grads, SUM)
+            if args.group:
+                with group():
+                    comm.all_gather_into_tensor(gathered, params)
+                    comm.reduce_scatter_tensor(gshard, grads, SUM)
+            else:
+                comm.all_gather_into_tensor(gathered, params)
+                comm.reduce_scatter_tensor(gshard, grads, SUM)
 
         for _ in range(3):
             step()
@@ -95,7 +103,7 @@ def main():
                               "slice_bytes": plan_ag["slice_bytes"], "protocol": [plan_ag["protocol"], plan_rs["protocol"]],
                               "peak_intermediate_slots": plan_ag["peak_intermediate_slots"],
                               "ms_per_step": float(ms), "busbw_gbs": bytes_ / (float(ms) * 1e-3) / 1e9,
-                              "allgather_matches_nccl": bool(ok.item()), "windows": args.windows,
+                              "allgather_matches_nccl": bool(ok.item()), "windows": args.windows, "grouped": args.group,
                               "staging_bytes_used": [plan_ag.get("staging_bytes_used"), plan_rs.get("staging_bytes_used")],
                               "nccl_ms_per_step": nccl_ms, "nccl_algo": os.environ.get("NCCL_ALGO")}), flush=True)
         comm.destroy()
