@@ -79,7 +79,8 @@ def main():
             scheds["pat-ring"] = (S.ring_allgather(n), S.mirror_schedule(S.ring_allgather(n)))
         else:
             scheds["pat"] = (None, None)
-    dts = {"f32": (torch.float32, FLOAT32), "bf16": (torch.bfloat16, BFLOAT16)}
+    from paper_2506_20252_b200 import INT32
+    dts = {"f32": (torch.float32, FLOAT32), "bf16": (torch.bfloat16, BFLOAT16), "i32": (torch.int32, INT32)}
     out = open(args.out, "w") if rank == 0 else None
 
     def timed(fn, big):
