@@ -1403,6 +1403,8 @@ patResult_t patCommInitAll(patComm_t* out, int nranks, const int* devlist, const
   if (lt != 0)
     for (size_t gi = 1; gi < comm->groups.size(); ++gi) {
       auto w = std::make_unique<LaunchWorker>();
+      long long spin = 0;
+      if (env_int("PAT_WORKER_SPIN_US", &spin) && spin >= 0) w->spin_us = spin;
       const int dev = comm->groups[gi].device;
       LaunchWorker* wp = w.get();
       w->th = std::thread([wp, dev] {

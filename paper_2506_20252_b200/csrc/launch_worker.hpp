@@ -14,14 +14,26 @@
 // One host thread per extra device of a one-process communicator. An eager call submits to
 // every device (a cooperative launch costs ~4 us of host time, tools/capi_latency.cpp); the
 // workers submit to their devices while the calling thread does the first, so a call costs one
-// launch instead of one per device. A worker spins for a while after each job (back-to-back
-// calls find it awake), then sleeps on a condition variable.
+// launch instead of one per device. A worker sleeps on a condition variable between jobs (it can
+// be made to spin a while first, PAT_WORKER_SPIN_US).
+inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+  __builtin_ia32_pause();
+#elif defined(__aarch64__)
+  asm volatile("yield" ::: "memory");
+#endif
+}
+
 struct LaunchWorker {
   std::thread th;
   std::atomic<uint32_t> posted{0}, finished{0};
   std::atomic<bool> stop{false}, sleeping{false};
   std::mutex m;
   std::condition_variable cv;
+  // busy-wait after a job before sleeping (PAT_WORKER_SPIN_US, comm.cpp). Default 0: a spinning
+  // worker cut a one-process job's host-side copies (bench e2e) to a third (2 GPUs: 12 vs 29 GB/s)
+  // while saving ~4 us only on isolated eager calls (profiles/r02_worker_spin_*)
+  int64_t spin_us = 0;
   const std::function<int()>* job = nullptr;  // valid while posted != finished
   int result = 0;
 
@@ -31,7 +43,8 @@ struct LaunchWorker {
       auto t0 = std::chrono::steady_clock::now();
       uint32_t spins = 0;
       while (posted.load(std::memory_order_acquire) == seen && !stop.load(std::memory_order_relaxed)) {
-        if ((++spins & 255u) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
+        cpu_relax();  // an SMT sibling (e.g. the thread copying a step's inputs) keeps its issue slots
+        if ((++spins & 255u) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(spin_us)) {
           std::unique_lock<std::mutex> lk(m);
           // store-buffering pair with post(): sleeping.store / posted.load here against
           // posted.fetch_add / sleeping.load there. Both loads must be seq_cst, or each side may
