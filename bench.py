@@ -288,10 +288,17 @@ def run_pat(args, rank, world, local):
     if mode == "torchrun":
         import torch.distributed as dist
 
+        share = os.environ.get("BENCH_SHARE_GPUS") == "1"
+        if share:  # rehearsal of the N-process path on fewer GPUs (NCCL refuses two ranks per GPU)
+            local %= torch.cuda.device_count()
+            args.no_nccl = True
         dev0 = torch.device(f"cuda:{local}")
         torch.cuda.set_device(dev0)
         os.environ.setdefault("NCCL_ALGO", "Ring")  # affects only the NCCL comparison below
-        dist.init_process_group("nccl", device_id=dev0)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev0)
         devices = [local]
         comm = PatComm.from_process_group(device=local)
         desc = f"{n} ranks on {n} GPUs (torchrun: 1 process per GPU, CUDA IPC inbox pools)"
@@ -819,6 +826,8 @@ def run_pat(args, rank, world, local):
         }
         if nccl:
             out["nccl_ring"] = nccl
+        if mode == "torchrun" and os.environ.get("BENCH_SHARE_GPUS") == "1":
+            out["rehearsal"] = f"BENCH_SHARE_GPUS: {n} processes on {torch.cuda.device_count()} GPUs, not a bench value"
         out.update(extras)
     comm.destroy()
     if dist is not None:
