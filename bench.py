@@ -459,37 +459,42 @@ def run_pat(args, rank, world, local):
 
     dbg("e2e")
     # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region.
-    # Triple-buffered per device: step k's inputs go up on a copy stream into device set k % 3
+    # Rotating device sets (4 per device): step k's inputs go up on a copy stream into set k % 4
     # while step k-1 runs, and step k-1's results come down on another copy stream (PCIe is full
     # duplex); every step still copies all of its inputs in and its results out inside the
     # timed region.
-    # host buffers: one pinned block per direction and buffer kind, rank slices of it, so the ranks
-    # of one device move in ONE copy per kind (fewer, larger PCIe transfers)
-    hb = {k: torch.empty(L * m * elems, dtype=torch.float32).pin_memory()
-          for k, m in (("ag_send", 1), ("rs_send", n), ("ag_recv", n), ("rs_recv", 1))}
-    h_ag_send = list(hb["ag_send"].view(L, elems))
-    h_rs_send = list(hb["rs_send"].view(L, n * elems))
-    h_ag_recv = list(hb["ag_recv"].view(L, n * elems))
-    h_rs_recv = list(hb["rs_recv"].view(L, elems))
-    for i in range(L):
-        h_ag_send[i].copy_(sets[0]["ag_send"][i].cpu())
-        h_rs_send[i].copy_(sets[0]["rs_send"][i].cpu())
+    # buffers: per device ONE pinned host block and ONE device block per direction, [all-gather |
+    # reduce-scatter] x the device's ranks, so every step moves each device's inputs in one H2D copy
+    # and its results in one D2H copy (fewer, larger PCIe transfers)
     E = max(3, min(K, 20))
-    # triple-buffered device sets: step k+1's upload, step k's compute and step k-1's download all
-    # in flight (double buffering left PCIe idle ~17% of a step: tools/e2e_probe.py, 2.04 vs 1.71 ms)
-    NB = int(os.environ.get("BENCH_E2E_BUFFERS", "3"))
-    one_dev = len(D.devs) == 1
-    if one_dev:  # device side likewise: the ranks' buffers are slices of one allocation per kind
-        def cset():
-            blk = {k: torch.empty(L * m * elems, device=dev0) for k, m in
-                   (("ag_send", 1), ("rs_send", n), ("ag_recv", n), ("rs_recv", 1))}
-            d_ = {k: list(v.view(L, -1)) for k, v in blk.items()}
-            d_["_blk"] = blk
-            return d_
-        dsets = [cset() for _ in range(NB)]
-    else:
-        NB = min(NB, len(sets))  # distinct buffer sets only
-        dsets = [sets[j] for j in range(NB)]
+    # step k+1's upload, step k's compute and step k-1's download all in flight (double buffering
+    # left PCIe idle ~17% of a step: tools/e2e_probe.py, 2.04 vs 1.71 ms; a 4th set: 39.9 -> 44.5
+    # GB/s at N=2, 90 -> 123 at N=4, profiles/r02_e2e_sets.txt)
+    NB = int(os.environ.get("BENCH_E2E_BUFFERS", "4"))
+    ranks_on = {d: [i for i, di in enumerate(devices) if di == d] for d in D.devs}
+
+    def blocks(mk):
+        """{"in": {d: block}, "out": {d: block}, ag_send/rs_send/ag_recv/rs_recv: per-rank views}"""
+        b = {"in": {}, "out": {}, "ag_send": [None] * L, "rs_send": [None] * L, "ag_recv": [None] * L,
+             "rs_recv": [None] * L}
+        for d, idx in ranks_on.items():
+            m = len(idx)
+            bi, bo = mk(d, m * (1 + n) * elems), mk(d, m * (n + 1) * elems)
+            b["in"][d], b["out"][d] = bi, bo
+            for j, i in enumerate(idx):
+                b["ag_send"][i] = bi[j * elems:(j + 1) * elems]
+                b["rs_send"][i] = bi[m * elems + j * n * elems:m * elems + (j + 1) * n * elems]
+                b["ag_recv"][i] = bo[j * n * elems:(j + 1) * n * elems]
+                b["rs_recv"][i] = bo[m * n * elems + j * elems:m * n * elems + (j + 1) * elems]
+        return b
+
+    hb = blocks(lambda d, sz: torch.empty(sz, dtype=torch.float32).pin_memory())
+    for i in range(L):
+        hb["ag_send"][i].copy_(sets[0]["ag_send"][i].cpu())
+        hb["rs_send"][i].copy_(sets[0]["rs_send"][i].cpu())
+    dsets = [blocks(lambda d, sz: torch.empty(sz, device=f"cuda:{d}")) for _ in range(NB)]
+    for bs in dsets:  # untimed first use of the new buffers
+        call(comm, ("ag", "rs"), bs)
     s_in = {d: torch.cuda.Stream(d) for d in D.devs}
     s_out = {d: torch.cuda.Stream(d) for d in D.devs}
     ev = lambda: {d: torch.cuda.Event() for d in D.devs}  # noqa: E731
@@ -500,20 +505,14 @@ def run_pat(args, rank, world, local):
         e01[d][0].record(D.streams[d])
         s_in[d].wait_stream(D.streams[d])
         s_out[d].wait_stream(D.streams[d])
+    t_host = time.perf_counter()
     for k in range(E):
         bs = dsets[k % NB]
         for d in D.devs:
             with torch.cuda.device(d), torch.cuda.stream(s_in[d]):
                 if k >= NB:
                     s_in[d].wait_event(comp_done[k - NB][d])  # set k % NB's inputs are free
-                if one_dev:
-                    bs["_blk"]["ag_send"].copy_(hb["ag_send"], non_blocking=True)
-                    bs["_blk"]["rs_send"].copy_(hb["rs_send"], non_blocking=True)
-                else:
-                    for i, di in enumerate(devices):
-                        if di == d:
-                            bs["ag_send"][i].copy_(h_ag_send[i], non_blocking=True)
-                            bs["rs_send"][i].copy_(h_rs_send[i], non_blocking=True)
+                bs["in"][d].copy_(hb["in"][d], non_blocking=True)
                 h2d_done[k][d].record(s_in[d])
             D.streams[d].wait_event(h2d_done[k][d])
             if k >= NB:
@@ -523,21 +522,21 @@ def run_pat(args, rank, world, local):
             comp_done[k][d].record(D.streams[d])
             with torch.cuda.device(d), torch.cuda.stream(s_out[d]):
                 s_out[d].wait_event(comp_done[k][d])
-                if one_dev:
-                    hb["ag_recv"].copy_(bs["_blk"]["ag_recv"], non_blocking=True)
-                    hb["rs_recv"].copy_(bs["_blk"]["rs_recv"], non_blocking=True)
-                else:
-                    for i, di in enumerate(devices):
-                        if di == d:
-                            h_ag_recv[i].copy_(bs["ag_recv"][i], non_blocking=True)
-                            h_rs_recv[i].copy_(bs["rs_recv"][i], non_blocking=True)
+                hb["out"][d].copy_(bs["out"][d], non_blocking=True)
                 d2h_done[k][d].record(s_out[d])
     for d in D.devs:
         D.streams[d].wait_event(d2h_done[E - 1][d])
         D.streams[d].wait_event(h2d_done[E - 1][d])
         e01[d][1].record(D.streams[d])
+    e2e_host_us = 1e6 * (time.perf_counter() - t_host) / E  # host submission time per step
     D.barrier()
     e2e_ms = max_over_ranks(torch, dist, dev0, [max(e01[d][0].elapsed_time(e01[d][1]) for d in D.devs) / E])[0]
+    # the host copies of the last step's results equal the device results of the same inputs
+    # (sets[0], timed above): a wrong or partial copy-out fails the run instead of being timed
+    for i in range(L):
+        if not (torch.equal(hb["ag_recv"][i], sets[0]["ag_recv"][i].cpu()) and
+                torch.equal(hb["rs_recv"][i], sets[0]["rs_recv"][i].cpu())):
+            raise RuntimeError(f"e2e: rank slot {i}: host results differ from the device results")
     # bytes of the whole job per step (every rank's inputs up, every rank's outputs down)
     ranks_total = n
     h2d = ranks_total * (elems + n * elems) * 4
@@ -813,9 +812,10 @@ def run_pat(args, rank, world, local):
             "latency_us_eager": eager_us,
             "latency_us_eager_isolated": eager_iso_us,
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "host_submit_us_per_step": e2e_host_us,
                     "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host; "
-                            "triple-buffered: step k+1 uploads while step k-1 downloads (PCIe full duplex)"},
+                            "4 rotating device sets: step k+1 uploads while step k-1 downloads (PCIe full duplex); one H2D and one D2H copy "
+                            "per device per step"},
             "gpu_launches": launches_per_gpu * n_gpus,
             "gpu_launches_per_gpu": launches_per_gpu,
             "roofline": roof,
