@@ -459,7 +459,7 @@ def run_pat(args, rank, world, local):
 
     dbg("e2e")
     # ---- e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region.
-    # Rotating device sets (4 per device): step k's inputs go up on a copy stream into set k % 4
+    # Rotating device sets (3 or 4 per device): step k's inputs go up on a copy stream into set k % NB
     # while step k-1 runs, and step k-1's results come down on another copy stream (PCIe is full
     # duplex); every step still copies all of its inputs in and its results out inside the
     # timed region.
@@ -470,8 +470,11 @@ def run_pat(args, rank, world, local):
     # step k+1's upload, step k's compute and step k-1's download all in flight (double buffering
     # left PCIe idle ~17% of a step: tools/e2e_probe.py, 2.04 vs 1.71 ms; a 4th set: 39.9 -> 44.5
     # GB/s at N=2, 90 -> 123 at N=4, profiles/r02_e2e_sets.txt)
-    NB = int(os.environ.get("BENCH_E2E_BUFFERS", "4"))
     ranks_on = {d: [i for i, di in enumerate(devices) if di == d] for d in D.devs}
+    # 4 sets for small steps, 3 when a device moves >= 32 MiB a step (N=1: 68 vs 64 GB/s on one box;
+    # N=2 one process: 30 vs 26; profiles/r02_e2e_sets.txt)
+    big = max(len(v) for v in ranks_on.values()) * (n + 1) * C >= 32 << 20
+    NB = int(os.environ.get("BENCH_E2E_BUFFERS", "3" if big else "4"))
 
     def blocks(mk):
         """{"in": {d: block}, "out": {d: block}, ag_send/rs_send/ag_recv/rs_recv: per-rank views}"""
@@ -814,7 +817,7 @@ def run_pat(args, rank, world, local):
             "e2e": {"value": busbw_gbs(n, C, e2e_ms / 1e3), "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "host_submit_us_per_step": e2e_host_us,
                     "path": "pinned host -> device copies, patAllGather + patReduceScatter (C ABI), device -> host; "
-                            "4 rotating device sets: step k+1 uploads while step k-1 downloads (PCIe full duplex); one H2D and one D2H copy "
+                            f"{NB} rotating device sets: step k+1 uploads while step k-1 downloads (PCIe full duplex); one H2D and one D2H copy "
                             "per device per step"},
             "gpu_launches": launches_per_gpu * n_gpus,
             "gpu_launches_per_gpu": launches_per_gpu,
