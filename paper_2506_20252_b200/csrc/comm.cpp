@@ -1306,8 +1306,16 @@ patResult_t run_group_pair(PendingCall& x, PendingCall& y) {
   auto zero_copy_bulk = [](const Prepared& q) {
     return !q.fused && !q.plans.empty() && (q.plans[0].proto == kProtoPull || q.plans[0].direct);
   };
+  // the halves index the per-channel flags and step counters by absolute channel: calls of two
+  // protocols whose regions differ in size (an LL half is at most 16 channels, an LL32 or SIMPLE
+  // half 74) can land on common channels, and must then run one after the other
+  auto overlap = [](const Prepared& p, const Prepared& q) {
+    const KPlan& x = p.plans[0];
+    const KPlan& y = q.plans[0];
+    return x.chan_base < y.chan_base + y.channels && y.chan_base < x.chan_base + x.channels;
+  };
   if (pa.fused != pb.fused || (!pa.fused && (pa.plans.empty() || pb.plans.empty())) || zero_copy_bulk(pa) ||
-      zero_copy_bulk(pb)) {
+      zero_copy_bulk(pb) || (!pa.fused && overlap(pa, pb))) {
     // not the same executor, or a pair that runs better apart: one after the other
     if (patResult_t e = run_pending(x)) return e;
     return run_pending(y);

@@ -170,3 +170,50 @@ def test_group_graph_capture():
         comm.raise_async_error()
     finally:
         comm.destroy()
+
+
+@pytest.mark.parametrize("spread", [False, True])
+@pytest.mark.parametrize("n", [2, 4])
+def test_group_mixed_sizes(spread, n):
+    """A pair whose halves take different protocols (an LL half spans fewer channels than an LL32
+    or SIMPLE half): ranges that would share channels run one after the other, the rest as one
+    launch; every combination bit-exact, then the fused single-device executor with unequal sizes."""
+    if spread and NGPU < 2:
+        pytest.skip("needs >= 2 GPUs")
+    devices = [r % NGPU for r in range(n)] if spread else [0] * n
+    comm = PatComm.init_all(n, devices, fused=-1)
+    try:
+        for ag_elems, rs_elems in ((262144, 64), (64, 262144), (1 << 21, 3000), (3000, 1 << 21), (64, 8)):
+            for rs_first in (False, True):
+                a = _bufs(devices, O.FLOAT32, n, ag_elems, 13 * ag_elems + rs_first)
+                b = _bufs(devices, O.FLOAT32, n, rs_elems, 17 * rs_elems + rs_first + 1)
+                with group():
+                    if rs_first:
+                        comm.reduce_scatter(b["rs_sp"], b["rs_rp"], rs_elems, O.FLOAT32, O.SUM)
+                        comm.all_gather(a["ag_sp"], a["ag_rp"], ag_elems, O.FLOAT32)
+                    else:
+                        comm.all_gather(a["ag_sp"], a["ag_rp"], ag_elems, O.FLOAT32)
+                        comm.reduce_scatter(b["rs_sp"], b["rs_rp"], rs_elems, O.FLOAT32, O.SUM)
+                for d in sorted(set(devices)):
+                    torch.cuda.synchronize(d)
+                for r in range(n):
+                    assert a["ag_r"][r].cpu().numpy().tobytes() == a["want_ag"][r].tobytes(), (ag_elems, rs_elems, r)
+                    assert b["rs_r"][r].cpu().numpy().tobytes() == b["want_rs"][r].tobytes(), (ag_elems, rs_elems, r)
+        comm.raise_async_error()
+    finally:
+        comm.destroy()
+    comm = PatComm.init_all(8, [0] * 8)
+    try:
+        for ag_elems, rs_elems in ((8192, 1000), (1000, 65536)):
+            a = _bufs([0] * 8, O.BFLOAT16, 8, ag_elems, ag_elems)
+            b = _bufs([0] * 8, O.BFLOAT16, 8, rs_elems, rs_elems + 1)
+            with group():
+                comm.all_gather(a["ag_sp"], a["ag_rp"], ag_elems, O.BFLOAT16)
+                comm.reduce_scatter(b["rs_sp"], b["rs_rp"], rs_elems, O.BFLOAT16, O.SUM)
+            torch.cuda.synchronize(0)
+            for r in range(8):
+                assert a["ag_r"][r].cpu().numpy().tobytes() == a["want_ag"][r].tobytes(), ("fused", ag_elems, r)
+                assert b["rs_r"][r].cpu().numpy().tobytes() == b["want_rs"][r].tobytes(), ("fused", rs_elems, r)
+        comm.raise_async_error()
+    finally:
+        comm.destroy()
