@@ -96,6 +96,12 @@ struct DevGroup {
   int occ_rounds = -1;             // rounds of the last SIMPLE launch that filled them
   int sm_count = 0;
   std::array<char*, kMaxRanks> pool_view{};  // every rank's pool as seen from this device
+  // calls of one communicator run in issue order on each device even across streams (NCCL's
+  // guarantee; concurrent calls would share channels): recorded after every eager launch, waited
+  // on by the next call when it comes on another stream
+  cudaEvent_t order_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
 };
 
 struct Handle {
@@ -822,6 +828,10 @@ patResult_t setup_groups(patComm* comm) {
     CUDA_TRY(cudaSetDevice(comm->ldevs[l]));
     CUDA_TRY(cudaEventCreateWithFlags(&comm->events[l], cudaEventDisableTiming));
   }
+  for (DevGroup& g : comm->groups) {
+    CUDA_TRY(cudaSetDevice(g.device));
+    CUDA_TRY(cudaEventCreateWithFlags(&g.order_ev, cudaEventDisableTiming));
+  }
   return patSuccess;
 }
 
@@ -1131,12 +1141,19 @@ patResult_t submit_prepared(patComm* comm, const Prepared& a, const Prepared* b,
   const int n = comm->n;
   // submission to one device: join the stream of every local rank of the device, one launch
   auto submit = [&](size_t gi) -> patResult_t {
-    const DevGroup& g = comm->groups[gi];
+    DevGroup& g = comm->groups[gi];
     const KPlan& p = a.plans[gi];
     CUDA_TRY(cudaSetDevice(g.device));
     const int threads = b ? std::max(launch_threads(comm, p), launch_threads(comm, b->plans[gi]))
                           : launch_threads(comm, p);
     cudaStream_t s0 = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[0]]) : nullptr;
+    // transport calls share the channels' flags, step counters and inboxes: each waits for the
+    // previous one when it comes on another stream. The fused executor keeps no state between
+    // calls, and a stream being captured into a graph is ordered by its user (the graph runs later)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    bool ordered = !a.fused && cudaStreamIsCapturing(s0, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+    if (!a.fused && !ordered) cudaGetLastError();  // the legacy stream under a global capture elsewhere
+    if (ordered && g.has_last && g.last_stream != s0) CUDA_TRY(cudaStreamWaitEvent(s0, g.order_ev, 0));
     for (size_t i = 1; i < g.lidx.size(); ++i) {  // join the other local ranks' streams
       cudaStream_t si = streams ? reinterpret_cast<cudaStream_t>(streams[g.lidx[i]]) : nullptr;
       if (si == s0) continue;
@@ -1189,6 +1206,11 @@ patResult_t submit_prepared(patComm* comm, const Prepared& a, const Prepared* b,
       if (!joined) CUDA_TRY(cudaEventRecord(comm->events[g.lidx[0]], s0));
       joined = true;
       CUDA_TRY(cudaStreamWaitEvent(si, comm->events[g.lidx[0]], 0));
+    }
+    if (ordered) {
+      CUDA_TRY(cudaEventRecord(g.order_ev, s0));
+      g.last_stream = s0;
+      g.has_last = true;
     }
     return patSuccess;
   };
@@ -1521,6 +1543,8 @@ patResult_t patCommDestroy(patComm_t comm) {
     }
     for (size_t l = 0; l < comm->events.size(); ++l)
       if (comm->events[l]) cudaEventDestroy(comm->events[l]);
+    for (DevGroup& g : comm->groups)
+      if (g.order_ev) cudaEventDestroy(g.order_ev);
     if (comm->err_host) cudaFreeHost(comm->err_host);
   }
   delete comm;
