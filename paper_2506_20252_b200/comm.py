@@ -95,6 +95,10 @@ class group:
 
 
 class PatComm:
+    # tensors passed to the collectives are checked (size, contiguity, device) before the launch;
+    # raw integer pointers are not (as at the C ABI). Set False to skip the checks (~0.5 us/tensor).
+    validate_tensors = True
+
     def __init__(self, handle: ctypes.c_void_p):
         self._h = handle
         n = ctypes.c_int()
@@ -188,11 +192,30 @@ class PatComm:
             return [0] * len(self.local_ranks)
         return [int(getattr(s, "cuda_stream", s)) for s in streams]
 
+    def _check_tensors(self, bufs, nbytes: int, what: str) -> None:
+        """Every tensor in bufs (one per local rank) holds nbytes contiguous bytes on its rank's device."""
+        if len(bufs) != len(self.local_ranks):
+            raise PatError(4, f"{what}: {len(bufs)} buffers for {len(self.local_ranks)} local ranks")
+        if not self.validate_tensors:
+            return
+        for x, d in zip(bufs, self.devices):
+            if type(x) is int:
+                continue
+            if x.nbytes < nbytes:
+                raise PatError(31, f"{what}: a buffer holds {x.nbytes} bytes, the call needs {nbytes}")
+            if not x.is_contiguous():
+                raise PatError(4, f"{what}: buffers must be contiguous")
+            if x.get_device() != d:
+                raise PatError(4, f"{what}: a buffer is on device {x.get_device()}, its rank on {d}")
+
     def all_gather(self, sendbufs, recvbufs, count: Optional[int] = None, dtype=None, streams=None, schedule=None):
         """sendbufs[l] -> recvbufs[l] (n*count, origin order) for every local rank l."""
         dt = _dtype(dtype, sendbufs[0])
         if count is None:
             count = sendbufs[0].numel()
+        es = _lib.DTYPE_SIZE.get(dt, 0)  # an unknown dtype is refused by the library
+        self._check_tensors(sendbufs, count * es, "all_gather sendbufs")
+        self._check_tensors(recvbufs, self.nranks * count * es, "all_gather recvbufs")
         if schedule is None and self._fast is not None and self._h:
             check(self._fast.all_gather(self._hv, [_ptr(x) for x in sendbufs], [_ptr(x) for x in recvbufs], count, dt,
                                         self._fast_streams(streams)), "patAllGather")
@@ -211,6 +234,9 @@ class PatComm:
         dt = _dtype(dtype, sendbufs[0])
         if count is None:
             count = recvbufs[0].numel()
+        es = _lib.DTYPE_SIZE.get(dt, 0)  # an unknown dtype is refused by the library
+        self._check_tensors(sendbufs, self.nranks * count * es, "reduce_scatter sendbufs")
+        self._check_tensors(recvbufs, count * es, "reduce_scatter recvbufs")
         if schedule is None and self._fast is not None and self._h:
             check(self._fast.reduce_scatter(self._hv, [_ptr(x) for x in sendbufs], [_ptr(x) for x in recvbufs], count,
                                             dt, int(op), self._fast_streams(streams)), "patReduceScatter")
@@ -232,6 +258,7 @@ class PatComm:
             raise PatError(5, "all_gather_into_tensor needs a one-rank-per-process communicator")
         if output.numel() != self.nranks * input.numel() or output.dtype != input.dtype:
             raise PatError(31, "all_gather_into_tensor: output must hold nranks * input.numel() of input's dtype")
+        self._check_pair(output, input, "all_gather_into_tensor")
         if self._fast is not None and self._h:
             st = self._fast_streams(None if stream is None else [stream])
             check(self._fast.all_gather(self._hv, input.data_ptr(), output.data_ptr(), input.numel(),
@@ -247,6 +274,7 @@ class PatComm:
             raise PatError(5, "reduce_scatter_tensor needs a one-rank-per-process communicator")
         if input.numel() != self.nranks * output.numel() or output.dtype != input.dtype:
             raise PatError(31, "reduce_scatter_tensor: input must hold nranks * output.numel() of output's dtype")
+        self._check_pair(output, input, "reduce_scatter_tensor")
         if self._fast is not None and self._h:
             st = self._fast_streams(None if stream is None else [stream])
             check(self._fast.reduce_scatter(self._hv, input.data_ptr(), output.data_ptr(), output.numel(),
@@ -254,6 +282,11 @@ class PatComm:
                   "patReduceScatter")
             return
         self.reduce_scatter([input], [output], output.numel(), None, op, None if stream is None else [stream])
+
+    def _check_pair(self, output, input, what: str) -> None:
+        if self.validate_tensors and not (output.is_contiguous() and input.is_contiguous() and
+                                          output.get_device() == input.get_device() == self.devices[0]):
+            raise PatError(4, f"{what}: tensors must be contiguous and on device {self.devices[0]}")
 
     @staticmethod
     def group() -> "group":
