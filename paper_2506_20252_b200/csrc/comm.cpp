@@ -13,6 +13,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -910,6 +911,10 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   if (op < 0 || op >= patNumOps) return patUnsupportedOp;
   if (count == 0) return patSuccess;
   if (!sendbuffs || !recvbuffs) return patInvalidArgument;
+  // n * count * es bytes (the all-gather output, the reduce-scatter input) must fit in int64
+  if (count > static_cast<size_t>(INT64_MAX) / es / static_cast<size_t>(comm->n)) return patInvalidArgument;
+  for (size_t l = 0; l < comm->lranks.size(); ++l)
+    if (!sendbuffs[l] || !recvbuffs[l]) return patInvalidArgument;
   if (patResult_t e = check_async(comm)) return e;
   std::lock_guard<std::mutex> lock(comm->mu);
   const auto hp_t0 = comm->host_profile ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};

@@ -36,6 +36,13 @@ def test_tensor_checks_one_process():
             with pytest.raises(PatError) as ei:
                 comm.all_gather(s[:3] + [s[3].to("cuda:1")], r, e, FLOAT32)
             assert ei.value.kind == "InvalidArgument"
+        # the C ABI's own checks (raw pointers): a null buffer, a count whose n * count bytes overflow
+        with pytest.raises(PatError) as ei:
+            comm.all_gather([x.data_ptr() for x in s[:3]] + [0], [x.data_ptr() for x in r], e, FLOAT32)
+        assert ei.value.kind == "InvalidArgument"
+        with pytest.raises(PatError) as ei:
+            comm.all_gather([x.data_ptr() for x in s], [x.data_ptr() for x in r], 1 << 61, FLOAT32)
+        assert ei.value.kind == "InvalidArgument"
         comm.all_gather(s, r, e, FLOAT32)  # nothing was launched by the refused calls
         torch.cuda.synchronize()
         want = torch.cat([x.cpu() for x in s])
