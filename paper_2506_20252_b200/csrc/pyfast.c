@@ -67,7 +67,7 @@ static PyObject* all_gather(PyObject* self, PyObject* const* args, Py_ssize_t na
     PyErr_SetString(PyExc_RuntimeError, "_patfast not bound");
     return NULL;
   }
-  void *s[MAXR], *r[MAXR], *st[MAXR];
+  void *s[MAXR] = {0}, *r[MAXR] = {0}, *st[MAXR] = {0}; /* short lists: the ABI sees NULL buffers */
   void* comm = PyLong_AsVoidPtr(args[0]);
   const size_t count = PyLong_AsSize_t(args[3]);
   const int dtype = (int)PyLong_AsLong(args[4]);
@@ -94,7 +94,7 @@ static PyObject* reduce_scatter(PyObject* self, PyObject* const* args, Py_ssize_
     PyErr_SetString(PyExc_RuntimeError, "_patfast not bound");
     return NULL;
   }
-  void *s[MAXR], *r[MAXR], *st[MAXR];
+  void *s[MAXR] = {0}, *r[MAXR] = {0}, *st[MAXR] = {0}; /* short lists: the ABI sees NULL buffers */
   void* comm = PyLong_AsVoidPtr(args[0]);
   const size_t count = PyLong_AsSize_t(args[3]);
   const int dtype = (int)PyLong_AsLong(args[4]);
