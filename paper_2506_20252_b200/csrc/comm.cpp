@@ -995,10 +995,17 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
   const bool direct = direct_ok && sl.proto == kProtoSimple;
   // window tag the kernels compare at entry (transport.cuh: sym_check)
   uint64_t sym_tag = 0;
+  // an in-place all-gather (sendbuf = recvbuf + rank * count, NCCL's form) has its send buffer at a
+  // rank-dependent window offset: the peers' send buffers are found through their recv windows
+  const bool inplace_ag = comm->multiprocess && kind == kAG && wrecv &&
+                          static_cast<const char*>(sendbuffs[0]) ==
+                              static_cast<const char*>(recvbuffs[0]) + comm->lranks[0] * chunk_bytes;
   if (comm->multiprocess && (direct || sl.proto == kProtoPull)) {
     auto mix = [](uint64_t h, uint64_t x) { return (h ^ x) * 0x100000001B3ull + (h >> 29); };
     uint64_t h = 0xcbf29ce484222325ull;
-    if (sl.proto == kProtoPull)
+    if (sl.proto == kProtoPull && inplace_ag)
+      h = mix(h, 0x1b9ace0000000000ull);  // every rank must call in place
+    else if (sl.proto == kProtoPull)
       h = mix(mix(h, wsend->id), static_cast<uint64_t>(static_cast<const char*>(sendbuffs[0]) - wsend->local));
     if (direct || (sl.proto == kProtoPull && kind == kAG))
       h = mix(mix(h, wrecv->id + 0x10000ull), static_cast<uint64_t>(static_cast<char*>(recvbuffs[0]) - wrecv->local));
@@ -1057,7 +1064,9 @@ patResult_t run_collective(patComm* comm, int kind, const void* const* sendbuffs
       const int me = comm->lranks[0];
       for (int r = 0; r < n; ++r) {
         if (r == me) continue;
-        if (wsend && sl.proto == kProtoPull)
+        if (sl.proto == kProtoPull && inplace_ag)
+          p.peer_send[r] = wrecv->peer[r] + (static_cast<char*>(recvbuffs[0]) - wrecv->local) + r * chunk_bytes;
+        else if (wsend && sl.proto == kProtoPull)
           p.peer_send[r] = wsend->peer[r] + (static_cast<const char*>(sendbuffs[0]) - wsend->local);
         if (wrecv && (direct || kind == kAG))
           p.peer_recv[r] = wrecv->peer[r] + (static_cast<char*>(recvbuffs[0]) - wrecv->local);

@@ -83,6 +83,25 @@ def windows_section(rank, n, dev):
             if r.cpu().numpy().tobytes() != want[rank].tobytes():
                 fails += 1
                 print(f"rank {rank} windowed RS mismatch proto={proto} dt={dt}", flush=True)
+            # in place inside the window: the send slice is the rank's slot of the receive buffer
+            # (all-gather) / the receive slice is the rank's block of the send buffer (reduce-scatter)
+            r = win_r[pad:pad + n * elems * 4]
+            r.zero_()
+            r[rank * elems * 4:(rank + 1) * elems * 4].copy_(torch.from_numpy(mine.copy().view(np.uint8)))
+            comm.all_gather([r[rank * elems * 4:(rank + 1) * elems * 4]], [r], elems, dt)
+            torch.cuda.synchronize(dev)
+            want, _ = O.run_allgather(O.pat_allgather(n, O.max_trees(n)), dt, p, elems)
+            if comm.async_error() or r.cpu().numpy().tobytes() != want[rank].tobytes():
+                fails += 1
+                print(f"rank {rank} windowed in-place AG mismatch proto={proto} dt={dt}", flush=True)
+            s = win_s[pad:pad + n * elems * 4]
+            s.copy_(torch.from_numpy(q[rank * n * elems:(rank + 1) * n * elems].copy().view(np.uint8)))
+            comm.reduce_scatter([s], [s[rank * elems * 4:(rank + 1) * elems * 4]], elems, dt, O.SUM)
+            torch.cuda.synchronize(dev)
+            want, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, O.max_trees(n)), dt, O.SUM, q, elems)
+            if comm.async_error() or s[rank * elems * 4:(rank + 1) * elems * 4].cpu().numpy().tobytes() != want[rank].tobytes():
+                fails += 1
+                print(f"rank {rank} windowed in-place RS mismatch proto={proto} dt={dt}", flush=True)
         # a grouped pair on windowed buffers (zero-copy all-gather + reduce-scatter in one launch)
         from paper_2506_20252_b200 import group
         p = O.random_payload(O.FLOAT32, n, elems, 123 + proto)
@@ -202,6 +221,26 @@ def main():
         if shard.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() != want[rank].tobytes():
             fails += 1
             print(f"rank {rank} reduce_scatter_tensor differs from the oracle elems={elems}", flush=True)
+    # in-place forms (FSDP): the input is the rank's slot of the output / the output is the rank's
+    # block of the input
+    for elems in (4099, 3 << 20):
+        x = torch.randn(elems, device=dev)
+        out, ref = torch.zeros(n * elems, device=dev), torch.empty(n * elems, device=dev)
+        out[rank * elems:(rank + 1) * elems] = x
+        comm.all_gather_into_tensor(out, out[rank * elems:(rank + 1) * elems])
+        dist.all_gather_into_tensor(ref, x)
+        torch.cuda.synchronize(dev)
+        if not torch.equal(out, ref):
+            fails += 1
+            print(f"rank {rank} in-place all_gather_into_tensor differs from NCCL elems={elems}", flush=True)
+        q = O.random_payload(O.FLOAT32, n * n, elems, elems + 29)
+        g = torch.from_numpy(q[rank * n * elems:(rank + 1) * n * elems].copy()).to(dev)
+        comm.reduce_scatter_tensor(g[rank * elems:(rank + 1) * elems], g)
+        torch.cuda.synchronize(dev)
+        want, _ = O.run_reduce_scatter(O.pat_reduce_scatter(n, O.max_trees(n)), O.FLOAT32, O.SUM, q, elems)
+        if g[rank * elems:(rank + 1) * elems].cpu().numpy().tobytes() != want[rank].tobytes():
+            fails += 1
+            print(f"rank {rank} in-place reduce_scatter_tensor differs from the oracle elems={elems}", flush=True)
     comm.raise_async_error()
     comm.destroy()
     fails += group_section(rank, n, dev)

@@ -13,16 +13,17 @@ pytestmark = pytest.mark.gpu
 from paper_2506_20252_b200 import PatComm  # noqa: E402
 
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
-CASES = [(4, False, 0), (4, False, -1), (2, True, 0), (4, True, 0)]  # (n, spread, fused)
+CASES = [(4, False, 0, 0), (4, False, -1, 0), (2, True, 0, 0), (4, True, 0, 0), (4, False, -1, 3), (4, True, 0, 3),
+         (4, True, 0, 2)]  # (n, spread, fused, protocol: 0 auto, 3 PULL, 2 SIMPLE)
 
 
-@pytest.mark.parametrize("n,spread,fused", CASES)
+@pytest.mark.parametrize("n,spread,fused,proto", CASES)
 @pytest.mark.parametrize("elems", [1, 3000, 262144, 1 << 21])
-def test_inplace(n, spread, fused, elems):
+def test_inplace(n, spread, fused, proto, elems):
     if spread and NGPU < 2:
         pytest.skip("needs >= 2 GPUs")
     devices = [r % NGPU for r in range(n)] if spread else [0] * n
-    comm = PatComm.init_all(n, devices, fused=fused)
+    comm = PatComm.init_all(n, devices, fused=fused, protocol=proto)
     dt = O.FLOAT32
     try:
         p = O.random_payload(dt, n, elems, 7 * elems + n)
