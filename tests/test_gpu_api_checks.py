@@ -54,3 +54,23 @@ def test_tensor_checks_one_process():
         comm.raise_async_error()
     finally:
         comm.destroy()
+
+
+@pytest.mark.parametrize("fused", [0, -1])
+def test_single_rank(fused):
+    """n = 1 (the reference accepts it: zero rounds): all-gather and reduce-scatter are copies."""
+    comm = PatComm.init_all(1, [0], fused=fused)
+    try:
+        for e in (1, 3000, 1 << 20):
+            s = torch.rand(e, device="cuda:0")
+            r = torch.empty(e, device="cuda:0")
+            comm.all_gather([s], [r], e, FLOAT32)
+            torch.cuda.synchronize()
+            assert torch.equal(r, s)
+            r.zero_()
+            comm.reduce_scatter([s], [r], e, FLOAT32, SUM)
+            torch.cuda.synchronize()
+            assert torch.equal(r, s)
+        comm.raise_async_error()
+    finally:
+        comm.destroy()
