@@ -87,6 +87,7 @@ def main():
         fn()
     torch.cuda.synchronize(dev)
     dist.barrier()
+    comm.barrier()  # device barrier: both GPUs start the traced call together, host skew excluded
     fn()
     torch.cuda.synchronize(dev)
     tr = comm.trace()
