@@ -134,6 +134,9 @@ struct Waiter {
 };
 
 // ------------------------------------------------------------------------- device trace
+#ifndef PAT_TRACE_POLL
+#define PAT_TRACE_POLL 0  // trace events in the LL / LL32 path (diagnostic builds only)
+#endif
 // Event codes (bits 56..63 event, 40..55 step, 32..39 round); one writer thread per role.
 enum TraceEv : uint64_t {
   kEvStart = 1, kEvCredit = 2, kEvPushed = 3, kEvFenced = 4, kEvArrived = 5, kEvDelivered = 6, kEvDone = 7,
@@ -1124,19 +1127,31 @@ __device__ __forceinline__ void pat_body(const KPlan& p, int vb) {
     // Steps in order. (A wavefront — phase t of step k - t in iteration k, as send_role — was
     // built and measured slower: LL32 is bound by the polled lines' bandwidth, not by flight
     // times; profiles/r01f_ll32_{skew,noskew}_n*.jsonl.)
+    // PAT_TRACE in a -DPAT_TRACE_POLL=1 build (tools/build_variant.sh; compiled out by default, so
+    // the polling path's code is unchanged): thread 0's view (role 1): start, credits in, each LL32
+    // phase done (round t: its lines sent and, for t > 0, its arrivals of round t-1 consumed), end
+    Tracer tr;
+    if (PAT_TRACE_POLL && threadIdx.x == 0) tr.init(p, 1);
+    tr.rec(kEvStart, base, 0);
     for (int i = 0; i < p.iters; ++i) {
       const Step s = make_step(p, base, i, R, lr, c);
       wait_credits_par(p, s, w, threadIdx.x);
       __syncthreads();
+      tr.rec(kEvCredit, s.g, 0);
       if (p.proto == kProtoLL) {
         step_ll<DT, OP, KIND>(p, s, w);
+        tr.rec(kEvDelivered, s.g, 0);
       } else {
         if (p.leaves_first) {  // every round's leaf lines, then the forwards, then the finish
           for (int t = 0; t < p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w, kLeafPos);
           for (int t = 0; t < p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w, kFwdPos);
           ll32_phase<DT, OP, KIND, U>(p, s, p.nrounds, w);
+          tr.rec(kEvDelivered, s.g, p.nrounds);
         } else {
-          for (int t = 0; t <= p.nrounds; ++t) ll32_phase<DT, OP, KIND, U>(p, s, t, w);
+          for (int t = 0; t <= p.nrounds; ++t) {
+            ll32_phase<DT, OP, KIND, U>(p, s, t, w);
+            tr.rec(t < p.nrounds ? kEvPushed : kEvDelivered, s.g, t);
+          }
         }
       }
       const bool clean = epoch_clean_due(p, s.g);
@@ -1154,6 +1169,7 @@ __device__ __forceinline__ void pat_body(const KPlan& p, int vb) {
       if (i + 1 < p.iters && threadIdx.x < p.n && static_cast<int>(threadIdx.x) != R)
         st_relaxed(chan_flags(p, threadIdx.x, c) + 8 + R, s.g + 1, w.gpu);
     }
+    tr.rec(kEvEnd, base + p.iters, 0);
   } else {
     const int nsend = p.send_warps * 32;
     if (static_cast<int>(threadIdx.x) < nsend) {
