@@ -2,6 +2,9 @@
 
   PAT_TRACE=64 torchrun --nproc-per-node 4 --master-addr 127.0.0.1 tools/trace_run.py --bytes 16777216 --coll ag
 
+SIMPLE calls trace in the default build. LL / LL32 calls need a diagnostic build:
+  bash tools/build_variant.sh tracepoll -DPAT_TRACE_POLL=1    # then PAT_LIB_VARIANT=tracepoll PAT_TRACE=8 ...
+
 Writes gpurun_out/trace_<coll>_<bytes>_r<rank>.npz (ctas x 2 roles x entries x {ns, code}) and
 prints, for rank 0, a timeline summary: per event type, the min / median / max time (us) from
 the kernel's first event, over CTAs.
