@@ -62,3 +62,19 @@ def test_round2_bench_lines_and_zero3_caps():
     assert rows[12]["busbw_gbs"] >= 0.75 * rows[0]["busbw_gbs"]
     assert all(r["allgather_matches_nccl"] for r in rows.values())
     assert rows[12]["pool_bytes_ag"] <= 12 << 20
+
+
+def test_round2_semantics_fixes_are_evidenced():
+    """DESIGN §3.4b / §3.6 / INTEGRATION: the previous build failed the two-stream and mixed-size
+    group tests and the current one passes them; the final 4-GPU suite and the smoke passed."""
+    txt = open(os.path.join(P, "r02_stream_ordering.txt")).read()
+    before, after = txt.split("## current build")[0], txt.split("## current build")[1]
+    assert "Timeout" in before and "1 failed" in before
+    assert "9 passed" in after and "failed" not in after.split("## eager")[0]
+    txt = open(os.path.join(P, "r02_group_mixed_fix.txt")).read()
+    assert "AssertionError" in txt.split("## fixed build")[0] and "4 passed" in txt.split("## fixed build")[1]
+    txt = open(os.path.join(P, "r02_inplace_gpu2.log")).read()
+    assert "28 passed" in txt and "17 passed" in txt
+    last = open(os.path.join(P, "r02_pytest_gpu4.log")).read().strip().splitlines()[-1]
+    assert "passed" in last and "failed" not in last and int(last.split()[0]) >= 400
+    assert "bit-exact" in open(os.path.join(P, "r02_smoke.log")).read()
