@@ -61,7 +61,9 @@ def parse(argv=None):
     ap.add_argument("--no-group", action="store_true", help="issue a step's all-gather and reduce-scatter ungrouped")
     ap.add_argument("--no-extras", action="store_true", help="skip transport_local / ref_dtypes records")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    return ap.parse_args(argv)
+    a = ap.parse_args(argv)
+    a.warmup = max(a.warmup, 3)  # at least 3 untimed warm-up steps (the line reports the count run)
+    return a
 
 
 def dist_env():
